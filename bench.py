@@ -1,0 +1,347 @@
+"""Benchmark of the direct inverse NFFT hot path (Kircheis & Potts, arXiv:1811.05335).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--prec c128|c64]
+    torchrun --nproc-per-node N --master-addr 127.0.0.1 bench.py --gpus N ...
+
+Workload (BASELINE config 5, the largest single-GPU config): M = 2^20, N = 2^21
+jittered nodes (seed 4), sigma = 2, m = 8, Kaiser-Bessel, B_opt from the GPU
+Alg. "Fast optimization of the matrix B" (untimed setup).  One STEP = the
+whole hot path over one batch of R_loc = 64 right-hand
+sides per GPU: the inverse NFFT (spread, FFT, truncate+deconvolve) AND the
+inverse adjoint NFFT (deconvolve+pad, FFT, gather).  A "solve" is one RHS
+through one of the two directions, so a step is 2 R_loc solves per GPU.
+Multi-GPU: RHS sharded across ranks (weak scaling, 64 per GPU; 512 at N = 8 as
+in the config), no data-path collective; time = max over ranks.
+Inputs are 2.1 GB per rank (> 126 MB L2), so no L2 flush is needed.
+"""
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+RLOC = 64
+CFG_ID = 5
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--prec", default="c128", choices=["c128", "c64"])
+    ap.add_argument("--rhs", type=int, default=RLOC, help="right-hand sides per GPU")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--e2e-steps", type=int, default=3)
+    return ap.parse_args()
+
+
+def dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+def model_bytes_per_rhs(N, M, Ms, P, e, ew, R):
+    """SURVEY 8(d) algorithmic bytes: each factor streamed once, FFT = 1 read + 1 write
+    of the grid, B_opt (P weights + one int32 slot base per node) once per batch."""
+    inv = e * (N + 3 * Ms + 2 * M) + (P * ew + 4) * N / R
+    adj = e * (M + 4 * Ms + N) + (P * ew + 4) * N / R
+    spread = e * (N + Ms) + (P * ew + 4) * N / R
+    gather = e * (Ms + N) + (P * ew + 4) * N / R
+    return inv, adj, spread, gather
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled DURING the timed region."""
+
+    FIELDS = ["clocks.sm", "clocks.max.sm", "power.draw", "clocks_event_reasons.hw_slowdown",
+              "clocks_event_reasons.hw_thermal_slowdown", "clocks_event_reasons.sw_thermal_slowdown",
+              "clocks_event_reasons.sw_power_cap"]
+
+    def __init__(self, device_index):
+        self.dev = device_index
+        self.proc = None
+        self.out = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.dev), "--query-gpu=" + ",".join(self.FIELDS),
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"], "samples": 0}
+        self.proc.terminate()
+        try:
+            out, _ = self.proc.communicate(timeout=5)
+        except Exception:
+            self.proc.kill()
+            out = ""
+        sm, smax, reasons, pw = [], [], set(), []
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in out.strip().splitlines():
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) != len(self.FIELDS):
+                continue
+            try:
+                sm.append(float(parts[0]))
+                smax.append(float(parts[1]))
+                pw.append(float(parts[2]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[3:]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        return {"sm_mhz": float(np.median(sm)) if sm else None,
+                "sm_max_mhz": float(max(smax)) if smax else None,
+                "power_w_max": float(max(pw)) if pw else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def measured_peak_hbm():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            return float(json.load(fh)["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+def cpu_baseline(x, M, sigma, m, w, R_sample):
+    """The oracle as it stands (plain C + OpenMP over RHS) on a bounded sample:
+    R_sample right-hand sides through both directions with the same B_opt."""
+    import oracle as O
+    import synth as S
+    f = S.normal_complex(R_sample, x.size, 11)
+    h = S.normal_complex(R_sample, M, 12)
+    O.build_c()
+    t0 = time.perf_counter()
+    O.apply_inverse(x, M, sigma, m, w, 1.0, f)
+    O.apply_adjoint(x, M, sigma, m, w, 1.0, h)
+    dt = time.perf_counter() - t0
+    cores = min(O.num_threads(), R_sample)
+    return {"value": 2 * R_sample / dt, "unit": "solves/s", "cores": cores, "kind": "oracle",
+            "sample": f"config 5, {R_sample} RHS x (inverse + inverse adjoint), same B_opt, {dt:.1f} s wall"}
+
+
+def run_reference(args):
+    """--impl reference: the oracle (this tier's reference arm) on the host cores."""
+    ws, rank, _ = dist_env()
+    if rank != 0:
+        return
+    import oracle as O
+    import synth as S
+    c = S.config(CFG_ID)
+    x = S.make_nodes(c)
+    M, sigma, m = c["M"][0], c["sigma"], c["m"]
+    O.build_c()
+    # weights: the oracle's own window matrix B (the apply's cost does not depend on the
+    # values; the oracle's per-column Gram setup at 2^21 columns is a multi-hour loop)
+    w = O.window_slot_weights(x, M, sigma, m)
+    R_s = max(2, min(16, O.num_threads()))
+    f = S.normal_complex(R_s, x.size, 11)
+    h = S.normal_complex(R_s, M, 12)
+    for _ in range(args.warmup):
+        O.apply_inverse(x, M, sigma, m, w, 1.0, f[:1])
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        O.apply_inverse(x, M, sigma, m, w, 1.0, f)
+        O.apply_adjoint(x, M, sigma, m, w, 1.0, h)
+    dt = time.perf_counter() - t0
+    val = 2 * R_s * args.steps / dt
+    cores = min(O.num_threads(), R_s)
+    line = {"metric": "iNFFT solves/s (complex double, batched)", "value": val, "unit": "solves/s",
+            "impl": "reference", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": 1e3 * dt / args.steps, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "f64", "data": "synthetic",
+            "config": {"workload": "cfg5: 1-D M=2^20, N=2^21 jittered (seed 4), sigma=2, m=8, KB; "
+                                   "inverse + inverse adjoint", "rhs_per_step": R_s},
+            "cpu_baseline": {"value": val, "unit": "solves/s", "cores": cores, "kind": "oracle",
+                             "sample": f"{R_s} RHS per direction per step (bounded sample of the 64-RHS batch)"},
+            "e2e": {"value": val, "unit": "solves/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+        return
+    import torch
+    import torch.distributed as dist
+
+    ws, rank, local = dist_env()
+    if ws > 1:
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev = local if ws > 1 else 0
+    torch.cuda.set_device(dev)
+
+    import synth as S
+    import paper_1811_05335_b200 as P
+
+    c = S.config(CFG_ID)
+    x = S.make_nodes(c)
+    M, sigma, m = c["M"][0], c["sigma"], c["m"]
+    Ms = int(M * sigma)
+    N = x.size
+    R = args.rhs
+    cdt = torch.complex128 if args.prec == "c128" else torch.complex64
+    e = 16 if args.prec == "c128" else 8
+    ew = 8 if args.prec == "c128" else 4
+
+    # ---------------------------------------------------------------- setup (untimed)
+    t0 = time.perf_counter()
+    plan = P.Plan(x, M, sigma, m, precision=args.prec, device=dev)
+    t_plan = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    plan.precompute("alg2")
+    t_setup = time.perf_counter() - t0
+    info = plan.info()
+
+    g = torch.Generator(device=f"cuda:{dev}").manual_seed(1000 + rank)
+    f = torch.randn(R, N, dtype=cdt, device=f"cuda:{dev}", generator=g)
+    h = torch.randn(R, M, dtype=cdt, device=f"cuda:{dev}", generator=g)
+    fhat = torch.empty(R, M, dtype=cdt, device=f"cuda:{dev}")
+    fout = torch.empty(R, N, dtype=cdt, device=f"cuda:{dev}")
+    stream = torch.cuda.current_stream()
+
+    def step():
+        plan.apply(f, out=fhat, stream=stream)
+        plan.adjoint_apply(h, out=fout, stream=stream)
+
+    for _ in range(max(args.warmup, 0)):
+        step()
+    torch.cuda.synchronize()
+
+    # ---------------------------------------------------------------- timed region
+    sampler = ClockSampler(dev)
+    plan.set_profiling(True)
+    plan.get_profile(reset=True)
+    launches0 = plan.kernel_launches()
+    if ws > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    sampler.start()
+    time.sleep(0.3)  # let the sampler attach
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    ev0.record(stream)
+    for _ in range(args.steps):
+        step()
+    ev1.record(stream)
+    torch.cuda.synchronize()
+    if ws > 1:
+        dist.barrier()
+    clocks = sampler.stop()
+    launches = plan.kernel_launches() - launches0
+    ms_total = ev0.elapsed_time(ev1)
+    prof = plan.get_profile(reset=True)
+    plan.set_profiling(False)
+    t_max = torch.tensor([ms_total], dtype=torch.float64, device=f"cuda:{dev}")
+    if ws > 1:
+        dist.all_reduce(t_max, op=dist.ReduceOp.MAX)
+    ms_total = float(t_max.item())
+    ms_step = ms_total / args.steps
+    solves = 2 * R * ws * args.steps
+    value = solves / (ms_total / 1e3)
+
+    # ---------------------------------------------------------------- roofline of the dominant kernel
+    inv_b, adj_b, spread_b, gather_b = model_bytes_per_rhs(N, M, Ms, info["P"], e, ew, R)
+    stage_bytes = {"spread": spread_b * R, "gather": gather_b * R,
+                   "fft_forward": 2 * e * Ms * R, "fft_inverse": 2 * e * Ms * R,
+                   "trunc_deconv": 2 * e * M * R, "deconv_pad": e * (M + Ms) * R}
+    stage_ms = {k: (v[0] / v[1] if v[1] else None) for k, v in prof.items()}
+    dom = max((k for k in stage_ms if stage_ms[k]), key=lambda k: prof[k][0])
+    peak, peak_kind = measured_peak_hbm()
+    achieved = stage_bytes[dom] / (stage_ms[dom] / 1e3) / 1e9
+    apply_gbs = (inv_b + adj_b) * R / (ms_step / 1e3) / 1e9
+    roofline = {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak, "unit": "GB/s",
+                "frac": achieved / peak, "traffic": None, "peak_source": peak_kind + " (MEASURED_PEAKS.json hbm_gbs)",
+                "bytes_per_launch": stage_bytes[dom], "ms_per_launch": stage_ms[dom]}
+    stages = {k: {"ms_per_launch": stage_ms[k], "launches": prof[k][1],
+                  "gbs": (stage_bytes[k] / (stage_ms[k] / 1e3) / 1e9) if stage_ms[k] else None,
+                  "share_of_step": (prof[k][0] / ms_total) if ms_total else None} for k in stage_ms}
+
+    # ---------------------------------------------------------------- e2e through the C ABI with host buffers
+    e2e = None
+    if not args.no_e2e:
+        fh_host = torch.empty(R, N, dtype=cdt).pin_memory()
+        hh_host = torch.empty(R, M, dtype=cdt).pin_memory()
+        fh_host.copy_(f.cpu())
+        hh_host.copy_(h.cpu())
+        o1 = torch.empty(R, M, dtype=cdt).pin_memory()
+        o2 = torch.empty(R, N, dtype=cdt).pin_memory()
+        plan.apply(fh_host, out=o1, stream=stream)  # warm staging buffers
+        plan.adjoint_apply(hh_host, out=o2, stream=stream)
+        torch.cuda.synchronize()
+        if ws > 1:
+            dist.barrier()
+        a0 = torch.cuda.Event(enable_timing=True)
+        a1 = torch.cuda.Event(enable_timing=True)
+        a0.record(stream)
+        for _ in range(args.e2e_steps):
+            plan.apply(fh_host, out=o1, stream=stream)
+            plan.adjoint_apply(hh_host, out=o2, stream=stream)
+        a1.record(stream)
+        torch.cuda.synchronize()
+        te = torch.tensor([a0.elapsed_time(a1)], dtype=torch.float64, device=f"cuda:{dev}")
+        if ws > 1:
+            dist.all_reduce(te, op=dist.ReduceOp.MAX)
+        te_ms = float(te.item())
+        e2e = {"value": 2 * R * ws * args.e2e_steps / (te_ms / 1e3), "unit": "solves/s",
+               "h2d_bytes_per_step": int((N + M) * e * R), "d2h_bytes_per_step": int((M + N) * e * R),
+               "steps": args.e2e_steps, "ms_per_step": te_ms / args.e2e_steps,
+               "note": "pinned host f, h in; pinned host fhat, f out; copies pipelined inside the C-ABI call"}
+
+    # ---------------------------------------------------------------- CPU oracle baseline (rank 0, N = 1)
+    cpu = None
+    if rank == 0 and ws == 1 and not args.no_cpu_baseline:
+        try:
+            import oracle as O
+            w = plan.get_bopt()
+            R_s = max(2, min(32, O.num_threads()))
+            cpu = cpu_baseline(x, M, sigma, m, w, R_s)
+        except Exception as ex:  # the baseline must never break the bench line
+            cpu = {"value": None, "unit": "solves/s", "cores": None, "kind": "oracle", "sample": f"failed: {ex}"}
+
+    if rank == 0:
+        line = {
+            "metric": "iNFFT solves/s (complex double, batched)" if args.prec == "c128"
+            else "iNFFT solves/s (complex float, batched)",
+            "value": value, "unit": "solves/s", "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "f64" if args.prec == "c128" else "f32", "data": "synthetic",
+            "config": {"workload": "cfg5: 1-D M=2^20, N=2^21 jittered (seed 4), sigma=2, m=8, Kaiser-Bessel, "
+                                   "Alg. 2 B_opt; step = inverse NFFT + inverse adjoint NFFT",
+                       "rhs_per_gpu": R, "global_batch": R * ws, "parallelism": f"rhs-sharded x{ws}",
+                       "l2": "inputs larger than L2 (no flush needed)", "precision": args.prec},
+            "apply_hbm_gbs": apply_gbs, "apply_hbm_frac": apply_gbs / peak,
+            "roofline": roofline, "stages": stages, "cpu_baseline": cpu, "e2e": e2e,
+            "gpu_launches": launches, "clocks": clocks,
+            "setup": {"plan_s": t_plan, "precompute_s": t_setup, "n_rank_deficient": info["n_rank_deficient"],
+                      "max_col_size": info["max_col_size"], "fast_path": info["fast_path"],
+                      "workspace_bytes": info["workspace_bytes"]},
+        }
+        print(json.dumps(line), flush=True)
+    if ws > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

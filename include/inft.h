@@ -1,0 +1,185 @@
+/*
+ * inft.h -- C ABI of the B200-native (sm_100a) direct inverse NFFT.
+ *
+ * Method: M. Kircheis, D. Potts, "Direct inversion of the nonequispaced fast
+ * Fourier transform", arXiv:1811.05335.  Citations "P:<n>" refer to lines of
+ * the paper's source; readings "A<n>" to DESIGN.md.
+ *
+ * The library solves, for FIXED nodes x_j ("fixed nodes for several
+ * problems") and many right-hand sides,
+ *   problem (1) inverse NFFT          A fhat = f
+ *   problem (2) inverse adjoint NFFT  A^* f  = h
+ * with A = (e^{2 pi i k x_j})_{j, k} (eq. matrix_A), by the paper's
+ * modified (adjoint) NFFT with an optimised (2m+1)-sparse matrix B_opt:
+ *   inverse:          fhat ~= s D^* F^* B_opt^* f
+ *   inverse adjoint:  f    ~= s B_opt F D h
+ * D = diag(1/(M_sigma what(k))) (eq. matrix_D), F the truncated M_sigma-point
+ * Fourier matrix (eq. matrix_F), s = 1/M for the node-wise Alg. "Fast
+ * optimization of the matrix B*" and s = 1 for the grid-wise Alg. "Fast
+ * optimization of the matrix B" (reading A2).
+ *
+ * Conventions (all calls):
+ *  - Every call returns inft_status; nothing throws or aborts across the ABI.
+ *  - Complex data are interleaved (re, im): double pairs for INFT_C128 plans,
+ *    float pairs for INFT_C64 plans (= torch.complex128 / complex64 memory).
+ *  - Batches are RHS-major: f[r*N + j], fhat[r*Mtot + c] with the centered
+ *    spectral index c = k + M/2 (2-D: c = (k1 + M1/2)*M2 + (k2 + M2/2)),
+ *    Mtot = prod(M).
+ *  - "host or device" pointers are detected with cudaPointerGetAttributes;
+ *    host data are staged through plan-owned device buffers with pipelined
+ *    copies (pinned host memory overlaps copies with compute).
+ *  - Calls are stream-ordered on `stream` (a cudaStream_t; NULL = legacy
+ *    default stream) and asynchronous unless stated.  A plan owns scratch
+ *    memory: do not run two applies of one plan concurrently on two streams.
+ *  - The caller owns every buffer it passes; the plan owns copies of nodes,
+ *    bins, B_opt, the deconvolution table, cuFFT plans and workspaces, and
+ *    frees them in inft_destroy.
+ */
+#ifndef INFT_H
+#define INFT_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct inft_plan_s* inft_plan_t; /* opaque plan handle */
+typedef void* inft_stream_t;             /* a cudaStream_t */
+
+typedef enum {
+    INFT_OK = 0,
+    INFT_ERR_INVALID_ARG = 1,     /* bad size/enum/pointer, M odd, sigma*M not an even integer, ... */
+    INFT_ERR_NODE_RANGE = 2,      /* a node coordinate not finite or outside [-1/2, 1/2) */
+    INFT_ERR_ZERO_WINDOW_HAT = 3, /* what(k) <= 0 for some |k| <= M/2 (D would not exist) */
+    INFT_ERR_NOT_PRECOMPUTED = 4, /* apply before inft_precompute / inft_set_bopt */
+    INFT_ERR_CUDA = 5,            /* a CUDA runtime call failed (message: inft_last_error) */
+    INFT_ERR_CUFFT = 6,           /* a cuFFT call failed */
+    INFT_ERR_OOM = 7,             /* device allocation failed */
+    INFT_ERR_UNSUPPORTED = 8      /* valid request this build does not implement */
+} inft_status;
+
+typedef enum {
+    INFT_KAISER_BESSEL = 0 /* reading A7: what(k) = I0(m sqrt(b^2-(2 pi k/M_sigma)^2))/M_sigma, b = pi(2-1/sigma) */
+} inft_window;
+
+typedef enum {
+    INFT_AUTO = 0,           /* Alg. 1 if prod(M) >= N, else Alg. 2 */
+    INFT_ALG1_NODEWISE = 1,  /* Alg. "Fast optimization of the matrix B*", s = 1/M */
+    INFT_ALG2_GRIDWISE = 2,  /* Alg. "Fast optimization of the matrix B",  P:1298-1333, s = 1 */
+    INFT_PLAIN_NFFT = 3      /* B = window matrix (eq. matrix_B), s = 1: the ordinary adjoint NFFT / NFFT */
+} inft_method;
+
+typedef enum { INFT_C128 = 0, INFT_C64 = 1 } inft_precision;
+typedef enum { INFT_WEIGHTS_REAL = 0, INFT_WEIGHTS_COMPLEX = 1 } inft_weights;
+
+typedef struct {
+    int32_t d;                 /* 1 or 2 */
+    int64_t M[2];              /* coefficients per dimension (M[1] = 1 for d = 1) */
+    int64_t Msigma[2];         /* oversampled grid per dimension */
+    int64_t N;                 /* nodes */
+    int32_t m;                 /* cut-off */
+    int32_t P;                 /* slots per node: 2m+1 (1-D), (2m+1)^2 (2-D) */
+    int32_t tile[2];           /* bin / segment width per dimension (reading A19) */
+    int32_t precision;         /* inft_precision */
+    int32_t method;            /* inft_method in effect, -1 before precompute */
+    int32_t weights;           /* inft_weights in effect */
+    double scale;              /* s folded into D (reading A2) */
+    double tau;                /* min-norm cutoff used by inft_precompute (reading A6) */
+    int64_t n_rank_deficient;  /* columns whose system dropped singular directions */
+    int64_t n_empty_cols;      /* grid columns with I(l) empty (Alg. 2) */
+    int64_t max_col_size;      /* max |I(l)| (Alg. 2) or max |I(x_j)| (Alg. 1) */
+    double max_abs_w;          /* max |B_opt entry| */
+    int32_t perm_identity;     /* 1 if the bin sort left the caller's node order unchanged */
+    int32_t fast_path;         /* 1 if the register-window spread/gather kernels are used */
+    size_t workspace_bytes;    /* device bytes currently owned by the plan */
+} inft_info;
+
+/* Build a plan for fixed nodes.
+ *   out     : receives the handle (NULL on failure).
+ *   d       : 1 or 2 (2-D is the tensor-product reading A12).
+ *   M       : [d] even coefficient counts (P:37 M in 2N).
+ *   N       : number of nodes, >= 0.
+ *   nodes   : host or device pointer, N x d row-major doubles, each coordinate
+ *             finite and in [-1/2, 1/2) (else INFT_ERR_NODE_RANGE; no wrapping).
+ *   sigma   : oversampling; sigma*M[i] must be an even integer.
+ *   m       : cut-off, 1 <= m <= M_sigma_i / 2.
+ *   device  : CUDA device ordinal the plan lives on.
+ * Computes l0_j = ceil(M_sigma x_j) - m per dimension with a correctly
+ * rounded product (reading A20), the tile bins and the stable node
+ * permutation (A19), and d_k = s/(M_sigma what(k)) (eq. matrix_D).  Synchronous. */
+inft_status inft_plan(inft_plan_t* out, int d, const int64_t* M, int64_t N, const double* nodes,
+                      double sigma, int m, inft_window window, inft_precision prec, int device,
+                      inft_stream_t stream);
+
+/* Compute B_opt on the GPU (setup stage):
+ *   INFT_ALG2_GRIDWISE: per grid point l minimise ||L_l b - e_l||
+ *     through the normal equations in Gram form.
+ *   INFT_ALG1_NODEWISE: per node j minimise ||K_j b - M e_j||.
+ *   INFT_PLAIN_NFFT: B = window matrix (eq. matrix_B).
+ *   INFT_AUTO: Alg. 1 if prod(M) >= N else Alg. 2.
+ *   wt  : real-constrained ("B in R^{N x M_sigma}", default) or complex.
+ *   tau : relative singular-value cutoff of the min-norm solution (A6);
+ *         <= 0 selects the default 1e-6.
+ * Synchronous.  Errors: INFT_ERR_UNSUPPORTED for combinations this build lacks. */
+inft_status inft_precompute(inft_plan_t plan, inft_method method, inft_weights wt, double tau,
+                            inft_stream_t stream);
+
+/* Inverse NFFT, problem (1): fhat[r] = s D^* F^* B_opt^* f[r], r < R.
+ *   f    : host or device, [R][N] complex (caller node order).
+ *   fhat : host or device, [R][Mtot] complex, centered.
+ * Steps: spread (B_opt^*), M_sigma-point FFT (F^*), truncate + deconvolve (D^*).
+ * R = 0 is a no-op.  Errors: INFT_ERR_NOT_PRECOMPUTED, INFT_ERR_INVALID_ARG. */
+inft_status inft_apply(inft_plan_t plan, const void* f, void* fhat, int64_t R, inft_stream_t stream);
+
+/* Inverse adjoint NFFT, problem (2): f[r] = s B_opt F D h[r].
+ *   h : host or device, [R][Mtot] complex centered;  f : host or device, [R][N].
+ * Steps: deconvolve + zero-pad (D), FFT (F), gather (B_opt). */
+inft_status inft_adjoint_apply(inft_plan_t plan, const void* h, void* f, int64_t R,
+                               inft_stream_t stream);
+
+/* Release every allocation of the plan (NULL is accepted). */
+inft_status inft_destroy(inft_plan_t plan);
+
+/* Introspection / checkpoint of the expensive setup.  All output pointers are
+ * HOST pointers; calls are synchronous.
+ *   inft_get_bins : l0 [N*d] (caller order, row-major), bin [N] (caller order),
+ *                   perm [N] (sorted position -> caller index).  Any may be NULL.
+ *   inft_get_bopt : w [N][P] doubles (real weights) or [N][P] complex doubles
+ *                   (complex weights), caller order, slot t <-> grid l0_j + t
+ *                   (2-D: t = t1*(2m+1) + t2).
+ *   inft_set_bopt : import such a w (host pointer) as B_opt for `method`
+ *                   (sets s: 1/prod(M) for INFT_ALG1_NODEWISE, else 1).
+ *   inft_get_deconv: d [sum M_i] doubles, the per-dimension tables with s
+ *                   folded into the first dimension (D = diag(d1 (x) d2)). */
+inft_status inft_get_bins(inft_plan_t plan, int32_t* l0, int32_t* bin, int32_t* perm);
+inft_status inft_get_bopt(inft_plan_t plan, void* w);
+inft_status inft_set_bopt(inft_plan_t plan, inft_method method, inft_weights wt, const void* w);
+inft_status inft_get_deconv(inft_plan_t plan, double* d);
+inft_status inft_get_info(inft_plan_t plan, inft_info* info);
+
+/* Per-stage device time of the apply, measured with CUDA events recorded on
+ * the launching stream around every stage of every apply while profiling is
+ * enabled (stages: 0 spread a2, 1 FFT a3, 2 truncate+deconvolve a4,
+ * 3 deconvolve+pad a5, 4 FFT a6, 5 gather a7).  inft_get_profile synchronises
+ * with the recorded events; reset != 0 clears the accumulators. */
+typedef struct {
+    double ms[6];
+    int64_t count[6];
+} inft_profile;
+inft_status inft_set_profiling(inft_plan_t plan, int enable);
+inft_status inft_get_profile(inft_plan_t plan, inft_profile* out, int reset);
+
+/* Number of kernel launches this plan issued since creation (evidence for
+ * benchmarks; cuFFT's internal kernels are not counted). */
+int64_t inft_kernel_launches(inft_plan_t plan);
+
+const char* inft_status_string(inft_status status);
+/* Thread-local text of the last error (CUDA / cuFFT message), "" if none. */
+const char* inft_last_error(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* INFT_H */

@@ -1,0 +1,253 @@
+"""Python binding of the sm_100a direct inverse NFFT library (libinft.so).
+
+Argument marshalling only: every step of the method runs in the CUDA kernels
+behind the C ABI declared in include/inft.h.  There is no CPU fallback -- if
+the shared library is missing this module raises on import.
+
+Low-level functions carry the C names (inft_plan, inft_precompute, inft_apply,
+inft_adjoint_apply, inft_destroy, inft_get_bins, inft_get_bopt, inft_set_bopt,
+inft_get_deconv, inft_get_info) and take raw pointers; ``Plan`` wraps them for
+torch tensors (CUDA or CPU/pinned) and numpy arrays.
+"""
+import ctypes
+import os
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libinft.so")
+
+if not os.path.exists(LIB_PATH):
+    raise ImportError(f"{LIB_PATH} is missing: build it with `python build_native.py` "
+                      "(there is no CPU fallback)")
+
+_lib = ctypes.CDLL(LIB_PATH)
+
+# enums (include/inft.h)
+INFT_OK = 0
+STATUS = {0: "INFT_OK", 1: "INFT_ERR_INVALID_ARG", 2: "INFT_ERR_NODE_RANGE", 3: "INFT_ERR_ZERO_WINDOW_HAT",
+          4: "INFT_ERR_NOT_PRECOMPUTED", 5: "INFT_ERR_CUDA", 6: "INFT_ERR_CUFFT", 7: "INFT_ERR_OOM",
+          8: "INFT_ERR_UNSUPPORTED"}
+INFT_KAISER_BESSEL = 0
+INFT_AUTO, INFT_ALG1_NODEWISE, INFT_ALG2_GRIDWISE, INFT_PLAIN_NFFT = 0, 1, 2, 3
+INFT_C128, INFT_C64 = 0, 1
+INFT_WEIGHTS_REAL, INFT_WEIGHTS_COMPLEX = 0, 1
+METHODS = {"auto": 0, "alg1": 1, "alg2": 2, "plain": 3}
+
+
+class InftInfo(ctypes.Structure):
+    _fields_ = [("d", ctypes.c_int32), ("M", ctypes.c_int64 * 2), ("Msigma", ctypes.c_int64 * 2),
+                ("N", ctypes.c_int64), ("m", ctypes.c_int32), ("P", ctypes.c_int32), ("tile", ctypes.c_int32 * 2),
+                ("precision", ctypes.c_int32), ("method", ctypes.c_int32), ("weights", ctypes.c_int32),
+                ("scale", ctypes.c_double), ("tau", ctypes.c_double), ("n_rank_deficient", ctypes.c_int64),
+                ("n_empty_cols", ctypes.c_int64), ("max_col_size", ctypes.c_int64), ("max_abs_w", ctypes.c_double),
+                ("perm_identity", ctypes.c_int32), ("fast_path", ctypes.c_int32),
+                ("workspace_bytes", ctypes.c_size_t)]
+
+
+class InftProfile(ctypes.Structure):
+    _fields_ = [("ms", ctypes.c_double * 6), ("count", ctypes.c_int64 * 6)]
+
+
+STAGES = ("spread", "fft_forward", "trunc_deconv", "deconv_pad", "fft_inverse", "gather")
+
+_P = ctypes.c_void_p
+_I64 = ctypes.c_int64
+_I = ctypes.c_int
+
+EXPORTS = {
+    "inft_plan": ([ctypes.POINTER(_P), _I, ctypes.POINTER(_I64), _I64, _P, ctypes.c_double, _I, _I, _I, _I, _P], _I),
+    "inft_precompute": ([_P, _I, _I, ctypes.c_double, _P], _I),
+    "inft_apply": ([_P, _P, _P, _I64, _P], _I),
+    "inft_adjoint_apply": ([_P, _P, _P, _I64, _P], _I),
+    "inft_destroy": ([_P], _I),
+    "inft_get_bins": ([_P, _P, _P, _P], _I),
+    "inft_get_bopt": ([_P, _P], _I),
+    "inft_set_bopt": ([_P, _I, _I, _P], _I),
+    "inft_get_deconv": ([_P, _P], _I),
+    "inft_get_info": ([_P, ctypes.POINTER(InftInfo)], _I),
+    "inft_set_profiling": ([_P, _I], _I),
+    "inft_get_profile": ([_P, ctypes.POINTER(InftProfile), _I], _I),
+    "inft_kernel_launches": ([_P], _I64),
+    "inft_status_string": ([_I], ctypes.c_char_p),
+    "inft_last_error": ([], ctypes.c_char_p),
+}
+for _name, (_args, _res) in EXPORTS.items():
+    _fn = getattr(_lib, _name)
+    _fn.argtypes = _args
+    _fn.restype = _res
+    globals()[_name] = _fn
+
+
+class InftError(RuntimeError):
+    def __init__(self, status, where):
+        msg = _lib.inft_last_error().decode(errors="replace")
+        super().__init__(f"{where}: {STATUS.get(status, status)} {msg}")
+        self.status = status
+
+
+def _check(st, where):
+    if st != INFT_OK:
+        raise InftError(st, where)
+
+
+def _ptr(a):
+    """Raw data pointer of a torch tensor or numpy array (must be contiguous)."""
+    if a is None:
+        return None
+    if hasattr(a, "data_ptr"):
+        if not a.is_contiguous():
+            raise ValueError("tensor must be contiguous")
+        return a.data_ptr()
+    if isinstance(a, np.ndarray):
+        if not a.flags["C_CONTIGUOUS"]:
+            raise ValueError("array must be C-contiguous")
+        return a.ctypes.data
+    raise TypeError(f"unsupported buffer type {type(a)}")
+
+
+def _stream_ptr(stream):
+    if stream is None:
+        try:
+            import torch
+            if torch.cuda.is_available():
+                return torch.cuda.current_stream().cuda_stream
+        except Exception:
+            pass
+        return None
+    if hasattr(stream, "cuda_stream"):
+        return stream.cuda_stream
+    return int(stream)
+
+
+class Plan:
+    """A plan for fixed nodes: nodes [N] or [N][2] float64 in [-1/2, 1/2)."""
+
+    def __init__(self, nodes, M, sigma, m, precision="c128", device=0, stream=None):
+        if isinstance(M, int):
+            M = (M,)
+        self.d = len(M)
+        self.M = tuple(int(v) for v in M)
+        nodes_np = None
+        if hasattr(nodes, "data_ptr"):
+            nd = nodes.contiguous()
+            self._nodes_ref = nd
+            N = nd.shape[0]
+            nptr = nd.data_ptr()
+        else:
+            nodes_np = np.ascontiguousarray(np.asarray(nodes, dtype=np.float64))
+            N = nodes_np.shape[0]
+            nptr = nodes_np.ctypes.data if N > 0 else None
+        self.N = int(N)
+        self.prec = INFT_C128 if precision in ("c128", INFT_C128) else INFT_C64
+        Marr = (ctypes.c_int64 * self.d)(*self.M)
+        h = ctypes.c_void_p()
+        _check(inft_plan(ctypes.byref(h), self.d, Marr, self.N, nptr, float(sigma), int(m), INFT_KAISER_BESSEL,
+                         self.prec, int(device), _stream_ptr(stream)), "inft_plan")
+        self._h = h
+        self.sigma = float(sigma)
+        self.m = int(m)
+        self.device = int(device)
+        self.Mtot = int(np.prod(self.M))
+        self.P = (2 * self.m + 1) ** self.d
+
+    @property
+    def handle(self):
+        return self._h
+
+    def close(self):
+        if getattr(self, "_h", None) is not None and self._h.value:
+            inft_destroy(self._h)
+            self._h = ctypes.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    # setup
+    def precompute(self, method="auto", weights="real", tau=0.0, stream=None):
+        meth = METHODS[method] if isinstance(method, str) else int(method)
+        wt = INFT_WEIGHTS_COMPLEX if weights == "complex" else INFT_WEIGHTS_REAL
+        _check(inft_precompute(self._h, meth, wt, float(tau), _stream_ptr(stream)), "inft_precompute")
+        return self
+
+    def set_bopt(self, w, method="alg2"):
+        w = np.ascontiguousarray(w)
+        meth = METHODS[method] if isinstance(method, str) else int(method)
+        if np.iscomplexobj(w):
+            buf = np.ascontiguousarray(w.astype(np.complex128))
+            wt = INFT_WEIGHTS_COMPLEX
+        else:
+            buf = np.ascontiguousarray(w.astype(np.float64))
+            wt = INFT_WEIGHTS_REAL
+        if buf.shape != (self.N, self.P):
+            raise ValueError(f"B_opt weights must be [{self.N}][{self.P}]")
+        _check(inft_set_bopt(self._h, meth, wt, buf.ctypes.data if buf.size else None), "inft_set_bopt")
+        return self
+
+    def get_bopt(self):
+        info = self.info()
+        dt = np.complex128 if info["weights"] == INFT_WEIGHTS_COMPLEX else np.float64
+        out = np.zeros((self.N, self.P), dtype=dt)
+        _check(inft_get_bopt(self._h, out.ctypes.data), "inft_get_bopt")
+        return out
+
+    def get_bins(self):
+        l0 = np.zeros((self.N, self.d), dtype=np.int32)
+        b = np.zeros(self.N, dtype=np.int32)
+        perm = np.zeros(self.N, dtype=np.int32)
+        if self.N:
+            _check(inft_get_bins(self._h, l0.ctypes.data, b.ctypes.data, perm.ctypes.data), "inft_get_bins")
+        return (l0[:, 0] if self.d == 1 else l0), b, perm
+
+    def get_deconv(self):
+        out = np.zeros(sum(self.M), dtype=np.float64)
+        _check(inft_get_deconv(self._h, out.ctypes.data), "inft_get_deconv")
+        return out
+
+    def info(self):
+        inf = InftInfo()
+        _check(inft_get_info(self._h, ctypes.byref(inf)), "inft_get_info")
+        return {k: (list(getattr(inf, k)) if k in ("M", "Msigma", "tile") else getattr(inf, k))
+                for k, _ in InftInfo._fields_}
+
+    def set_profiling(self, enable=True):
+        _check(inft_set_profiling(self._h, 1 if enable else 0), "inft_set_profiling")
+
+    def get_profile(self, reset=False):
+        """{stage: (total ms, launches)} from CUDA events on the launching stream."""
+        pr = InftProfile()
+        _check(inft_get_profile(self._h, ctypes.byref(pr), 1 if reset else 0), "inft_get_profile")
+        return {s: (pr.ms[i], pr.count[i]) for i, s in enumerate(STAGES)}
+
+    def kernel_launches(self):
+        return int(inft_kernel_launches(self._h))
+
+    # apply
+    def _out(self, like, shape):
+        import torch
+        dt = torch.complex128 if self.prec == INFT_C128 else torch.complex64
+        if hasattr(like, "device"):
+            return torch.empty(shape, dtype=dt, device=like.device, pin_memory=False)
+        return np.empty(shape, dtype=np.complex128 if self.prec == INFT_C128 else np.complex64)
+
+    def apply(self, f, out=None, stream=None):
+        """Inverse NFFT (problem (1)): fhat = s D^* F^* B_opt^* f; f [R][N] -> [R][prod M]."""
+        R = f.shape[0] if f.ndim == 2 else 1
+        if out is None:
+            out = self._out(f, (R, self.Mtot))
+        _check(inft_apply(self._h, _ptr(f), _ptr(out), R, _stream_ptr(stream)), "inft_apply")
+        return out
+
+    def adjoint_apply(self, h, out=None, stream=None):
+        """Inverse adjoint NFFT (problem (2)): f = s B_opt F D h; h [R][prod M] -> [R][N]."""
+        R = h.shape[0] if h.ndim == 2 else 1
+        if out is None:
+            out = self._out(h, (R, self.N))
+        _check(inft_adjoint_apply(self._h, _ptr(h), _ptr(out), R, _stream_ptr(stream)), "inft_adjoint_apply")
+        return out
+
+
+__all__ = ["Plan", "InftError", "LIB_PATH", "EXPORTS", "STAGES"] + list(EXPORTS)

@@ -1,0 +1,159 @@
+// Internal declarations of the sm_100a iNFFT library (not part of the ABI).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <cufft.h>
+
+#include <cstdint>
+#include <map>
+#include <string>
+#include <vector>
+
+#include "../../include/inft.h"
+
+namespace inft {
+
+// ------------------------------------------------------------ errors
+void set_error(const std::string& msg);
+
+struct Fail {
+    inft_status st;
+};
+
+#define INFT_CUDA(call)                                                                  \
+    do {                                                                                 \
+        cudaError_t e_ = (call);                                                         \
+        if (e_ != cudaSuccess) {                                                         \
+            ::inft::set_error(std::string(#call) + ": " + cudaGetErrorString(e_));       \
+            throw ::inft::Fail{e_ == cudaErrorMemoryAllocation ? INFT_ERR_OOM : INFT_ERR_CUDA}; \
+        }                                                                                \
+    } while (0)
+
+#define INFT_CUFFT(call)                                                                 \
+    do {                                                                                 \
+        cufftResult r_ = (call);                                                         \
+        if (r_ != CUFFT_SUCCESS) {                                                       \
+            ::inft::set_error(std::string(#call) + ": cufftResult " + std::to_string((int)r_)); \
+            throw ::inft::Fail{r_ == CUFFT_ALLOC_FAILED ? INFT_ERR_OOM : INFT_ERR_CUFFT}; \
+        }                                                                                \
+    } while (0)
+
+#define INFT_CHECK_LAUNCH() INFT_CUDA(cudaGetLastError())
+
+// ------------------------------------------------------------ device buffer
+struct DevBuf {
+    void* p = nullptr;
+    size_t bytes = 0;
+    void alloc(size_t b);
+    void free_();
+    ~DevBuf() { free_(); }
+    template <typename T>
+    T* as() const { return reinterpret_cast<T*>(p); }
+};
+
+// ------------------------------------------------------------ plan
+struct FftKey {
+    int batch;
+    bool operator<(const FftKey& o) const { return batch < o.batch; }
+};
+
+struct Plan {
+    int device = 0;
+    int d = 1;
+    int64_t M[2] = {1, 1};
+    int64_t Ms[2] = {1, 1};
+    int64_t Mtot = 1, Mstot = 1;
+    int64_t N = 0;
+    int m = 1;
+    int P1 = 3;          // 2m+1
+    int P = 3;           // P1^d
+    int PP = 4;          // padded slot stride of the sorted weight records (elements)
+    double sigma = 2.0;
+    inft_precision prec = INFT_C128;
+    int S[2] = {16, 1};  // tile (segment) width per dim
+    int64_t nseg[2] = {1, 1};
+    int64_t nseg_tot = 1;
+    bool perm_identity = true;
+    bool fast1d = false;
+
+    // method state
+    int method = -1;
+    inft_weights wt = INFT_WEIGHTS_REAL;
+    double scale = 1.0;
+    double tau = 1e-6;
+    int64_t n_rank_deficient = 0, n_empty_cols = 0, max_col_size = 0;
+    double max_abs_w = 0.0;
+
+    // device arrays (plan-owned)
+    DevBuf nodes;      // double [N*d] caller order
+    DevBuf l0;         // int32 [N*d] caller order
+    DevBuf bin;        // int32 [N] caller order
+    DevBuf perm;       // int32 [N] sorted -> caller
+    DevBuf seg_start;  // int32 [nseg_tot+1]
+    DevBuf n0s;        // int32 [N*d] sorted: n0 = l0 mod Ms per dim
+    DevBuf delta;      // int32 [N] sorted: segment-local offset (1-D: n0 - seg*S)
+    DevBuf dk;         // double [M1 (+M2)] deconvolution tables (s folded into dim 0)
+    DevBuf dkf;        // float copy for C64
+    DevBuf w;          // sorted weights: [N][PP] (real) or [N][PP] complex, in plan precision
+    DevBuf w64;        // sorted weights in double (real: [N][P]; complex: [N][P] pairs) -- checkpoint copy
+
+    // workspace
+    DevBuf grid;          // [Rt][Mstot] complex (plan precision)
+    int64_t grid_rhs = 0; // capacity in RHS
+    DevBuf stage_in[2], stage_out[2];
+    int64_t stage_rhs = 0;
+    std::map<FftKey, cufftHandle> fft;  // batch -> plan
+    cudaStream_t s_h2d = nullptr, s_d2h = nullptr;
+    cudaEvent_t ev_h2d[2] = {nullptr, nullptr}, ev_comp[2] = {nullptr, nullptr},
+                ev_d2h[2] = {nullptr, nullptr}, ev_entry = nullptr, ev_exit = nullptr;
+
+    int64_t launches = 0;
+
+    // per-stage profiling (inft_set_profiling)
+    bool profiling = false;
+    struct Rec {
+        int stage;
+        cudaEvent_t a, b;
+    };
+    std::vector<Rec> recs;
+    std::vector<cudaEvent_t> ev_pool;
+    double prof_ms[6] = {0, 0, 0, 0, 0, 0};
+    int64_t prof_cnt[6] = {0, 0, 0, 0, 0, 0};
+    cudaEvent_t take_event();
+    void drain_profile();
+
+    size_t elem_bytes() const { return prec == INFT_C128 ? 16 : 8; }
+    size_t workspace_bytes() const;
+    ~Plan();
+};
+
+struct DeviceGuard {
+    int prev = -1;
+    explicit DeviceGuard(int dev) {
+        cudaGetDevice(&prev);
+        if (prev != dev) cudaSetDevice(dev);
+    }
+    ~DeviceGuard() {
+        if (prev >= 0) cudaSetDevice(prev);
+    }
+};
+
+// ------------------------------------------------------------ entry points implemented per file
+// plan.cu
+void plan_build(Plan& p, const double* nodes_any, cudaStream_t st);
+void upload_weights(Plan& p, const double* w_host_caller_order, inft_method method, inft_weights wt,
+                    cudaStream_t st);
+void install_weights_from_device(Plan& p, const double* w64_sorted_dev, inft_method method,
+                                 inft_weights wt, cudaStream_t st);
+void compute_deconv(Plan& p, double s, cudaStream_t st);
+// apply.cu
+void apply_inverse(Plan& p, const void* f, void* fhat, int64_t R, cudaStream_t st);
+void apply_adjoint(Plan& p, const void* h, void* f, int64_t R, cudaStream_t st);
+// setup.cu
+void precompute(Plan& p, inft_method method, inft_weights wt, double tau, cudaStream_t st);
+
+bool is_device_pointer(const void* ptr);
+
+inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
+
+}  // namespace inft
