@@ -176,6 +176,36 @@ def run_reference(args):
     print(json.dumps(line), flush=True)
 
 
+def run_e2e(args, plan, f, h, R, N, M, e, cdt, ws, dev, stream, torch, dist):
+    fh_host = torch.empty(R, N, dtype=cdt).pin_memory()
+    hh_host = torch.empty(R, M, dtype=cdt).pin_memory()
+    fh_host.copy_(f.cpu())
+    hh_host.copy_(h.cpu())
+    o1 = torch.empty(R, M, dtype=cdt).pin_memory()
+    o2 = torch.empty(R, N, dtype=cdt).pin_memory()
+    plan.apply(fh_host, out=o1, stream=stream)  # warm the staging buffers
+    plan.adjoint_apply(hh_host, out=o2, stream=stream)
+    torch.cuda.synchronize()
+    if ws > 1:
+        dist.barrier()
+    a0 = torch.cuda.Event(enable_timing=True)
+    a1 = torch.cuda.Event(enable_timing=True)
+    a0.record(stream)
+    for _ in range(args.e2e_steps):
+        plan.apply(fh_host, out=o1, stream=stream)
+        plan.adjoint_apply(hh_host, out=o2, stream=stream)
+    a1.record(stream)
+    torch.cuda.synchronize()
+    te = torch.tensor([a0.elapsed_time(a1)], dtype=torch.float64, device=f"cuda:{dev}")
+    if ws > 1:
+        dist.all_reduce(te, op=dist.ReduceOp.MAX)
+    te_ms = float(te.item())
+    return {"value": 2 * R * ws * args.e2e_steps / (te_ms / 1e3), "unit": "solves/s",
+            "h2d_bytes_per_step": int((N + M) * e * R), "d2h_bytes_per_step": int((M + N) * e * R),
+            "steps": args.e2e_steps, "ms_per_step": te_ms / args.e2e_steps,
+            "note": "pinned host f, h in; pinned host fhat, f out; copies pipelined inside the C-ABI call"}
+
+
 def main():
     args = parse()
     if args.impl == "reference":
@@ -280,33 +310,10 @@ def main():
     # ---------------------------------------------------------------- e2e through the C ABI with host buffers
     e2e = None
     if not args.no_e2e:
-        fh_host = torch.empty(R, N, dtype=cdt).pin_memory()
-        hh_host = torch.empty(R, M, dtype=cdt).pin_memory()
-        fh_host.copy_(f.cpu())
-        hh_host.copy_(h.cpu())
-        o1 = torch.empty(R, M, dtype=cdt).pin_memory()
-        o2 = torch.empty(R, N, dtype=cdt).pin_memory()
-        plan.apply(fh_host, out=o1, stream=stream)  # warm staging buffers
-        plan.adjoint_apply(hh_host, out=o2, stream=stream)
-        torch.cuda.synchronize()
-        if ws > 1:
-            dist.barrier()
-        a0 = torch.cuda.Event(enable_timing=True)
-        a1 = torch.cuda.Event(enable_timing=True)
-        a0.record(stream)
-        for _ in range(args.e2e_steps):
-            plan.apply(fh_host, out=o1, stream=stream)
-            plan.adjoint_apply(hh_host, out=o2, stream=stream)
-        a1.record(stream)
-        torch.cuda.synchronize()
-        te = torch.tensor([a0.elapsed_time(a1)], dtype=torch.float64, device=f"cuda:{dev}")
-        if ws > 1:
-            dist.all_reduce(te, op=dist.ReduceOp.MAX)
-        te_ms = float(te.item())
-        e2e = {"value": 2 * R * ws * args.e2e_steps / (te_ms / 1e3), "unit": "solves/s",
-               "h2d_bytes_per_step": int((N + M) * e * R), "d2h_bytes_per_step": int((M + N) * e * R),
-               "steps": args.e2e_steps, "ms_per_step": te_ms / args.e2e_steps,
-               "note": "pinned host f, h in; pinned host fhat, f out; copies pipelined inside the C-ABI call"}
+        try:
+            e2e = run_e2e(args, plan, f, h, R, N, M, e, cdt, ws, dev, stream, torch, dist)
+        except Exception as ex:
+            e2e = {"value": None, "unit": "solves/s", "error": str(ex)[:300]}
 
     # ---------------------------------------------------------------- CPU oracle baseline (rank 0, N = 1)
     cpu = None

@@ -705,12 +705,13 @@ static void run(Plan& p, const void* in, size_t in_rhs_bytes, void* out, size_t 
     size_t per = std::max(in_dev ? 0 : in_rhs_bytes, out_dev ? 0 : out_rhs_bytes);
     int64_t Rh = std::max<int64_t>(1, std::min<int64_t>(R, (int64_t)(((size_t)256 << 20) / std::max<size_t>(per, 1))));
     Rh = grid_capacity(p, Rh);
-    if (p.stage_rhs < Rh) {
-        for (int i = 0; i < 2; i++) {
-            p.stage_in[i].alloc(in_rhs_bytes * Rh);
-            p.stage_out[i].alloc(out_rhs_bytes * Rh);
-        }
-        p.stage_rhs = Rh;
+    if (!in_dev && p.stage_in_bytes < in_rhs_bytes * Rh) {
+        for (int i = 0; i < 2; i++) p.stage_in[i].alloc(in_rhs_bytes * Rh);
+        p.stage_in_bytes = in_rhs_bytes * Rh;
+    }
+    if (!out_dev && p.stage_out_bytes < out_rhs_bytes * Rh) {
+        for (int i = 0; i < 2; i++) p.stage_out[i].alloc(out_rhs_bytes * Rh);
+        p.stage_out_bytes = out_rhs_bytes * Rh;
     }
     INFT_CUDA(cudaEventRecord(p.ev_entry, st));
     INFT_CUDA(cudaStreamWaitEvent(p.s_h2d, p.ev_entry, 0));

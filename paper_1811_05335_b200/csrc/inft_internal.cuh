@@ -101,7 +101,7 @@ struct Plan {
     DevBuf grid;          // [Rt][Mstot] complex (plan precision)
     int64_t grid_rhs = 0; // capacity in RHS
     DevBuf stage_in[2], stage_out[2];
-    int64_t stage_rhs = 0;
+    size_t stage_in_bytes = 0, stage_out_bytes = 0;
     std::map<FftKey, cufftHandle> fft;  // batch -> plan
     cudaStream_t s_h2d = nullptr, s_d2h = nullptr;
     cudaEvent_t ev_h2d[2] = {nullptr, nullptr}, ev_comp[2] = {nullptr, nullptr},

@@ -170,7 +170,8 @@ __global__ void k_deconv(double* __restrict__ dk, int64_t M, int64_t Ms, int m, 
     const double pi = 3.141592653589793238462643383279502884;
     double b = pi * (2.0 - 1.0 / sigma);
     double u = 2.0 * pi * k / (double)Ms;
-    double arg = b * b - u * u;
+    double arg = __dsub_rn(__dmul_rn(b, b), __dmul_rn(u, u));
+    if (arg < 0.0 && arg > -1e-12 * b * b) arg = 0.0;  // |k| = M/2 at sigma = 1: b = 2 pi k/Ms exactly
     if (arg < 0.0) {
         atomicOr(bad, 1);
         dk[c] = 0.0;

@@ -130,7 +130,7 @@ __global__ void k_inv_what(double* __restrict__ iw, int64_t M, int64_t Ms, int m
     if (k > M / 2) return;
     double b = kPi * (2.0 - 1.0 / sigma);
     double u = 2.0 * kPi * (double)k / (double)Ms;
-    iw[k] = 1.0 / cyl_bessel_i0((double)m * sqrt(fmax(b * b - u * u, 0.0)));
+    iw[k] = 1.0 / cyl_bessel_i0((double)m * sqrt(fmax(__dsub_rn(__dmul_rn(b, b), __dmul_rn(u, u)), 0.0)));
 }
 
 // Exact samples of Re G and Re K+ at the Chebyshev points of every piece:
