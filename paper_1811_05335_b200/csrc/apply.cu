@@ -1,7 +1,8 @@
-// Apply stage on sm_100a.
+// Apply stage on sm_100a: orchestration, generic kernels
+// and the deconvolution passes.
 //
 //   inverse NFFT          fhat = s D^* F^* B_opt^* f
-//       a2 spread  g = B_opt^* f        (register-window kernel, no atomics)
+//       a2 spread  g = B_opt^* f        (stream1d.cu: staged register-window kernel)
 //       a3 FFT     ghat = F^* g         (cuFFT, forward sign)
 //       a4 trunc   fhat_k = d_k ghat_{k mod M_sigma}
 //   inverse adjoint NFFT  f = s B_opt F D h
@@ -9,155 +10,18 @@
 //       a6 FFT     g = F ghat           (cuFFT, inverse sign, unnormalised)
 //       a7 gather  f_j = sum_t w_{j,t} g_{(l0_j + t) mod M_sigma}
 //
-// Grid vectors live in FFT order n = l mod M_sigma (reading A9); spectra are
-// centered (c = k + M/2).  s is folded into d (reading A2).
+// Grid vectors live in FFT order n = l mod M_sigma (reading A9), one row per
+// RHS with row stride GS >= M_sigma (1-D fast path: a 2m halo at the end);
+// spectra are centered (c = k + M/2).  s is folded into d (reading A2).
 #include <algorithm>
 #include <cstring>
-#include <type_traits>
 
+#include "common.cuh"
 #include "inft_internal.cuh"
 
 namespace inft {
 
-template <typename T>
-struct C2T;
-template <>
-struct C2T<double> {
-    using type = double2;
-};
-template <>
-struct C2T<float> {
-    using type = float2;
-};
-template <typename T>
-using C2 = typename C2T<T>::type;
-
-template <typename T>
-__device__ __forceinline__ C2<T> mk(T x, T y) {
-    C2<T> v;
-    v.x = x;
-    v.y = y;
-    return v;
-}
-
-__device__ __forceinline__ int64_t mod64(int64_t a, int64_t n) {
-    int64_t r = a % n;
-    return r < 0 ? r + n : r;
-}
-
 static inline unsigned blocks_for(int64_t n, int bs) { return (unsigned)std::max<int64_t>(1, ceil_div(n, bs)); }
-
-// ---------------------------------------------------------------- uniform weight loads
-// Load the P real weights of one sorted node record (16-byte aligned, padded to PP)
-// with vector loads; every lane of the warp reads the same address (broadcast).
-template <typename T, int P>
-struct WeightLoader;
-
-template <int P>
-struct WeightLoader<double, P> {
-    __device__ __forceinline__ static void load(const double* __restrict__ rec, double (&w)[P]) {
-        const double2* v = reinterpret_cast<const double2*>(rec);
-#pragma unroll
-        for (int q = 0; q < (P + 1) / 2; ++q) {
-            double2 a = __ldg(v + q);
-            w[2 * q] = a.x;
-            if (2 * q + 1 < P) w[2 * q + 1] = a.y;
-        }
-    }
-};
-
-template <int P>
-struct WeightLoader<float, P> {
-    __device__ __forceinline__ static void load(const float* __restrict__ rec, float (&w)[P]) {
-        const float4* v = reinterpret_cast<const float4*>(rec);
-#pragma unroll
-        for (int q = 0; q < (P + 3) / 4; ++q) {
-            float4 a = __ldg(v + q);
-            w[4 * q] = a.x;
-            if (4 * q + 1 < P) w[4 * q + 1] = a.y;
-            if (4 * q + 2 < P) w[4 * q + 2] = a.z;
-            if (4 * q + 3 < P) w[4 * q + 3] = a.w;
-        }
-    }
-};
-
-#define INFT_CASES_32(X) \
-    X(0) X(1) X(2) X(3) X(4) X(5) X(6) X(7) X(8) X(9) X(10) X(11) X(12) X(13) X(14) X(15) \
-    X(16) X(17) X(18) X(19) X(20) X(21) X(22) X(23) X(24) X(25) X(26) X(27) X(28) X(29) X(30) X(31)
-
-// ====================================================================== a2: spread
-// Register-window spread, 1-D, real weights.
-// A warp owns a chunk of Q consecutive grid segments (width SEG >= 2m) for 32
-// right-hand sides (lane = RHS).  Nodes are bin-sorted, so the nodes of a
-// segment are a contiguous range and their slot base n0 lies in the segment:
-// a node adds w[t] f_j to window register delta+t, delta = n0 - seg*SEG (a
-// warp-uniform switch makes every register index static).  After a segment,
-// window[0, SEG) is complete (all nodes with n0 in [n - 2m, n] have been seen)
-// and is stored once; window[SEG, SEG + 2m) is carried.  The chunk starts one
-// segment early (prologue) to collect the carry from its left neighbour.
-// No atomics, deterministic order, every grid point written exactly once.
-template <typename T, int MC, int SEG>
-__global__ void __launch_bounds__(128) k_spread_fast_1d(
-    const int32_t* __restrict__ seg_start, const int32_t* __restrict__ delta, const int32_t* __restrict__ perm,
-    int perm_identity, const T* __restrict__ w, int PP, const C2<T>* __restrict__ f, C2<T>* __restrict__ grid,
-    int64_t N, int64_t Ms, int nseg, int Q, int nchunks, int R, int nrg) {
-    constexpr int P = 2 * MC + 1;
-    constexpr int K = SEG + 2 * MC;
-    static_assert(SEG >= 2 * MC && SEG <= 32, "segment must cover the support");
-    const int lane = threadIdx.x & 31;
-    const int64_t gw = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
-    if (gw >= (int64_t)nchunks * nrg) return;
-    const int chunk = (int)(gw / nrg);
-    const int rg = (int)(gw - (int64_t)chunk * nrg);
-    const int r = rg * 32 + lane;
-    const bool active = r < R;
-    const C2<T>* __restrict__ fr = f + (int64_t)(active ? r : 0) * N;
-    C2<T>* __restrict__ gr = grid + (int64_t)(active ? r : 0) * Ms;
-
-    T ax[K], ay[K];
-#pragma unroll
-    for (int u = 0; u < K; ++u) ax[u] = ay[u] = T(0);
-
-    const int s0 = chunk * Q;
-    const int s1 = min(s0 + Q, nseg);
-    for (int si = s0 - 1; si < s1; ++si) {
-        const int s = si < 0 ? si + nseg : si;
-        const int i0 = __ldg(seg_start + s), i1 = __ldg(seg_start + s + 1);
-        for (int i = i0; i < i1; ++i) {
-            const int dl = __ldg(delta + i);
-            const int64_t j = perm_identity ? (int64_t)i : (int64_t)__ldg(perm + i);
-            C2<T> fv = mk<T>(T(0), T(0));
-            if (active) fv = __ldg(fr + j);
-            T wv[P];
-            WeightLoader<T, P>::load(w + (int64_t)i * PP, wv);
-            switch (dl) {
-#define INFT_SPREAD_CASE(D)                                       \
-    case D:                                                       \
-        if constexpr (D < SEG) {                                  \
-            _Pragma("unroll") for (int t = 0; t < P; ++t) {       \
-                ax[D + t] = fma(wv[t], fv.x, ax[D + t]);          \
-                ay[D + t] = fma(wv[t], fv.y, ay[D + t]);          \
-            }                                                     \
-        }                                                         \
-        break;
-                INFT_CASES_32(INFT_SPREAD_CASE)
-#undef INFT_SPREAD_CASE
-                default:
-                    break;
-            }
-        }
-        if (si >= s0 && active) {
-            C2<T>* out = gr + (int64_t)s * SEG;
-#pragma unroll
-            for (int u = 0; u < SEG; ++u) out[u] = mk<T>(ax[u], ay[u]);
-        }
-#pragma unroll
-        for (int u = 0; u < K; ++u) {
-            ax[u] = (u + SEG < K) ? ax[u + SEG] : T(0);
-            ay[u] = (u + SEG < K) ? ay[u + SEG] : T(0);
-        }
-    }
-}
 
 // Generic spread (any m, any d = 1 layout, real or complex weights, aliasing
 // 2m+1 > M_sigma): one thread per (grid point n, RHS r) sums
@@ -166,7 +30,7 @@ template <typename T, bool WC>
 __global__ void k_spread_generic_1d(const int32_t* __restrict__ seg_start, const int32_t* __restrict__ n0s,
                                     const int32_t* __restrict__ perm, const T* __restrict__ w, int PP, int P,
                                     const C2<T>* __restrict__ f, C2<T>* __restrict__ grid, int64_t N, int64_t Ms,
-                                    int S, int R) {
+                                    int64_t GS, int S, int R) {
     const int64_t total = (int64_t)R * Ms;
     for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
          idx += (int64_t)gridDim.x * blockDim.x) {
@@ -174,13 +38,8 @@ __global__ void k_spread_generic_1d(const int32_t* __restrict__ seg_start, const
         const int64_t n = idx - r * Ms;
         const C2<T>* fr = f + r * N;
         T sx = 0, sy = 0;
-        int64_t span = std::min<int64_t>(P, Ms);
-        int64_t pos = mod64(n - (span - 1), Ms);
-        int64_t rem = span;
-        while (rem > 0) {
-            int64_t s = pos / S;
-            int64_t send = std::min<int64_t>((s + 1) * S, Ms);
-            int64_t len = std::min<int64_t>(send - pos, rem);
+        const int64_t nseg = (Ms + S - 1) / S;
+        for_segments(n, std::min<int64_t>(P, Ms), Ms, S, nseg, [&](int64_t s) {
             for (int i = seg_start[s]; i < seg_start[s + 1]; ++i) {
                 int64_t t = mod64(n - n0s[i], Ms);
                 if (t >= P) continue;
@@ -197,11 +56,8 @@ __global__ void k_spread_generic_1d(const int32_t* __restrict__ seg_start, const
                     }
                 }
             }
-            rem -= len;
-            pos += len;
-            if (pos == Ms) pos = 0;
-        }
-        grid[idx] = mk<T>(sx, sy);
+        });
+        grid[r * GS + n] = mk<T>(sx, sy);
     }
 }
 
@@ -220,15 +76,9 @@ __global__ void k_spread_generic_2d(const int32_t* __restrict__ seg_start, const
         const int64_t n1 = n / Ms2, n2 = n - (n / Ms2) * Ms2;
         const C2<T>* fr = f + r * N;
         T sx = 0, sy = 0;
-        int64_t span1 = std::min<int64_t>(P1, Ms1), span2 = std::min<int64_t>(P1, Ms2);
-        int64_t pos1 = mod64(n1 - (span1 - 1), Ms1), rem1 = span1;
-        while (rem1 > 0) {
-            int64_t s1 = pos1 / S1;
-            int64_t len1 = std::min<int64_t>(std::min<int64_t>((s1 + 1) * S1, Ms1) - pos1, rem1);
-            int64_t pos2 = mod64(n2 - (span2 - 1), Ms2), rem2 = span2;
-            while (rem2 > 0) {
-                int64_t s2 = pos2 / S2;
-                int64_t len2 = std::min<int64_t>(std::min<int64_t>((s2 + 1) * S2, Ms2) - pos2, rem2);
+        const int64_t nseg1 = (Ms1 + S1 - 1) / S1;
+        for_segments(n1, std::min<int64_t>(P1, Ms1), Ms1, S1, nseg1, [&](int64_t s1) {
+            for_segments(n2, std::min<int64_t>(P1, Ms2), Ms2, S2, nseg2, [&](int64_t s2) {
                 int64_t tile = s1 * nseg2 + s2;
                 for (int i = seg_start[tile]; i < seg_start[tile + 1]; ++i) {
                     int64_t t1 = mod64(n1 - n0s[2 * i], Ms1);
@@ -249,93 +99,9 @@ __global__ void k_spread_generic_2d(const int32_t* __restrict__ seg_start, const
                             }
                         }
                 }
-                rem2 -= len2;
-                pos2 += len2;
-                if (pos2 == Ms2) pos2 = 0;
-            }
-            rem1 -= len1;
-            pos1 += len1;
-            if (pos1 == Ms1) pos1 = 0;
-        }
+            });
+        });
         grid[idx] = mk<T>(sx, sy);
-    }
-}
-
-// ====================================================================== a7: gather
-// Register-window gather, 1-D, real weights: lane = RHS, the warp walks the
-// segments of its chunk keeping grid window [seg*SEG, seg*SEG + SEG + 2m) in
-// registers (2m carried, SEG loaded per segment); each node reads its P taps
-// from the window with static indices (warp-uniform switch on delta).
-template <typename T, int MC, int SEG>
-__global__ void __launch_bounds__(128) k_gather_fast_1d(
-    const int32_t* __restrict__ seg_start, const int32_t* __restrict__ delta, const int32_t* __restrict__ perm,
-    int perm_identity, const T* __restrict__ w, int PP, const C2<T>* __restrict__ grid, C2<T>* __restrict__ f,
-    int64_t N, int64_t Ms, int nseg, int Q, int nchunks, int R, int nrg) {
-    constexpr int P = 2 * MC + 1;
-    constexpr int K = SEG + 2 * MC;
-    const int lane = threadIdx.x & 31;
-    const int64_t gw = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
-    if (gw >= (int64_t)nchunks * nrg) return;
-    const int chunk = (int)(gw / nrg);
-    const int rg = (int)(gw - (int64_t)chunk * nrg);
-    const int r = rg * 32 + lane;
-    const bool active = r < R;
-    const C2<T>* __restrict__ gr = grid + (int64_t)(active ? r : 0) * Ms;
-    C2<T>* __restrict__ fr = f + (int64_t)(active ? r : 0) * N;
-
-    T wx[K], wy[K];
-    const int s0 = chunk * Q;
-    const int s1 = min(s0 + Q, nseg);
-    for (int s = s0; s < s1; ++s) {
-        const int64_t base = (int64_t)s * SEG;
-        if (s == s0) {
-#pragma unroll
-            for (int u = 0; u < K; ++u) {
-                int64_t q = base + u;
-                if (q >= Ms) q -= Ms;
-                C2<T> v = active ? __ldg(gr + q) : mk<T>(T(0), T(0));
-                wx[u] = v.x;
-                wy[u] = v.y;
-            }
-        } else {
-#pragma unroll
-            for (int u = 0; u < K; ++u) {
-                if (u + SEG < K) {
-                    wx[u] = wx[u + SEG];
-                    wy[u] = wy[u + SEG];
-                } else {
-                    int64_t q = base + u;
-                    if (q >= Ms) q -= Ms;
-                    C2<T> v = active ? __ldg(gr + q) : mk<T>(T(0), T(0));
-                    wx[u] = v.x;
-                    wy[u] = v.y;
-                }
-            }
-        }
-        const int i0 = __ldg(seg_start + s), i1 = __ldg(seg_start + s + 1);
-        for (int i = i0; i < i1; ++i) {
-            const int dl = __ldg(delta + i);
-            const int64_t j = perm_identity ? (int64_t)i : (int64_t)__ldg(perm + i);
-            T wv[P];
-            WeightLoader<T, P>::load(w + (int64_t)i * PP, wv);
-            T sx = 0, sy = 0;
-            switch (dl) {
-#define INFT_GATHER_CASE(D)                                   \
-    case D:                                                   \
-        if constexpr (D < SEG) {                              \
-            _Pragma("unroll") for (int t = 0; t < P; ++t) {   \
-                sx = fma(wv[t], wx[D + t], sx);               \
-                sy = fma(wv[t], wy[D + t], sy);               \
-            }                                                 \
-        }                                                     \
-        break;
-                INFT_CASES_32(INFT_GATHER_CASE)
-#undef INFT_GATHER_CASE
-                default:
-                    break;
-            }
-            if (active) fr[j] = mk<T>(sx, sy);
-        }
     }
 }
 
@@ -343,14 +109,13 @@ __global__ void __launch_bounds__(128) k_gather_fast_1d(
 template <typename T, bool WC>
 __global__ void k_gather_generic(const int32_t* __restrict__ n0s, const int32_t* __restrict__ perm,
                                  const T* __restrict__ w, int PP, int P1, int d, const C2<T>* __restrict__ grid,
-                                 C2<T>* __restrict__ f, int64_t N, int64_t Ms1, int64_t Ms2, int R) {
-    const int64_t Mst = Ms1 * (d == 2 ? Ms2 : 1);
+                                 C2<T>* __restrict__ f, int64_t N, int64_t Ms1, int64_t Ms2, int64_t GS, int R) {
     const int64_t total = (int64_t)R * N;
     for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
          idx += (int64_t)gridDim.x * blockDim.x) {
         const int64_t r = idx / N;
         const int64_t i = idx - r * N;
-        const C2<T>* gr = grid + r * Mst;
+        const C2<T>* gr = grid + r * GS;
         T sx = 0, sy = 0;
         const int P2 = d == 2 ? P1 : 1;
         const int64_t a1 = n0s[(int64_t)i * d];
@@ -386,8 +151,8 @@ __global__ void k_gather_generic(const int32_t* __restrict__ n0s, const int32_t*
 // a4: fhat[r][c] = d1[c1] d2[c2] ghat[r][q], q_i = (c_i - M_i/2) mod Ms_i.
 template <typename T>
 __global__ void k_trunc_deconv(const C2<T>* __restrict__ grid, C2<T>* __restrict__ fhat, const T* __restrict__ dk,
-                               int64_t M1, int64_t M2, int64_t Ms1, int64_t Ms2, int d, int R) {
-    const int64_t Mt = M1 * M2, Mst = Ms1 * Ms2;
+                               int64_t M1, int64_t M2, int64_t Ms1, int64_t Ms2, int64_t GS, int d, int R) {
+    const int64_t Mt = M1 * M2;
     const int64_t total = (int64_t)R * Mt;
     for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
          idx += (int64_t)gridDim.x * blockDim.x) {
@@ -405,7 +170,7 @@ __global__ void k_trunc_deconv(const C2<T>* __restrict__ grid, C2<T>* __restrict
             q = (k1 < 0 ? k1 + Ms1 : k1) * Ms2 + (k2 < 0 ? k2 + Ms2 : k2);
             dd = dk[c1] * dk[M1 + c2];
         }
-        C2<T> g = grid[r * Mst + q];
+        C2<T> g = grid[r * GS + q];
         fhat[idx] = mk<T>(dd * g.x, dd * g.y);
     }
 }
@@ -413,7 +178,7 @@ __global__ void k_trunc_deconv(const C2<T>* __restrict__ grid, C2<T>* __restrict
 // a5: ghat[r][q] = d_k h[r][k + M/2] for |k| <= M/2 band, 0 elsewhere.
 template <typename T>
 __global__ void k_deconv_pad(const C2<T>* __restrict__ h, C2<T>* __restrict__ grid, const T* __restrict__ dk,
-                             int64_t M1, int64_t M2, int64_t Ms1, int64_t Ms2, int d, int R) {
+                             int64_t M1, int64_t M2, int64_t Ms1, int64_t Ms2, int64_t GS, int d, int R) {
     const int64_t Mt = M1 * M2, Mst = Ms1 * Ms2;
     const int64_t total = (int64_t)R * Mst;
     for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
@@ -438,40 +203,11 @@ __global__ void k_deconv_pad(const C2<T>* __restrict__ h, C2<T>* __restrict__ gr
                 out = mk<T>(dd * v.x, dd * v.y);
             }
         }
-        grid[idx] = out;
+        grid[r * GS + q] = out;
     }
 }
 
 // ====================================================================== host orchestration
-static constexpr int kQ = 32;  // segments per warp chunk
-
-template <typename T>
-using SpreadFastFn = void (*)(const int32_t*, const int32_t*, const int32_t*, int, const T*, int, const C2<T>*,
-                              C2<T>*, int64_t, int64_t, int, int, int, int, int);
-template <typename T>
-using GatherFastFn = void (*)(const int32_t*, const int32_t*, const int32_t*, int, const T*, int, const C2<T>*,
-                              C2<T>*, int64_t, int64_t, int, int, int, int, int);
-
-template <typename T>
-static SpreadFastFn<T> spread_fast_for(int m, int S) {
-#define INFT_SF(MC, SG) \
-    if (m == MC && S == SG) return k_spread_fast_1d<T, MC, SG>;
-    INFT_SF(1, 16) INFT_SF(2, 16) INFT_SF(3, 16) INFT_SF(4, 16) INFT_SF(5, 16) INFT_SF(6, 16) INFT_SF(7, 16)
-    INFT_SF(8, 16) INFT_SF(10, 32) INFT_SF(12, 32) INFT_SF(16, 32)
-#undef INFT_SF
-    return nullptr;
-}
-
-template <typename T>
-static GatherFastFn<T> gather_fast_for(int m, int S) {
-#define INFT_GF(MC, SG) \
-    if (m == MC && S == SG) return k_gather_fast_1d<T, MC, SG>;
-    INFT_GF(1, 16) INFT_GF(2, 16) INFT_GF(3, 16) INFT_GF(4, 16) INFT_GF(5, 16) INFT_GF(6, 16) INFT_GF(7, 16)
-    INFT_GF(8, 16) INFT_GF(10, 32) INFT_GF(12, 32) INFT_GF(16, 32)
-#undef INFT_GF
-    return nullptr;
-}
-
 static unsigned sm_blocks(int per_sm = 8) {
     static int nsm = 0;
     if (!nsm) {
@@ -487,33 +223,23 @@ static unsigned gs_blocks(int64_t total, int bs) {
     return (unsigned)std::min<int64_t>(blocks_for(total, bs), (int64_t)sm_blocks(16));
 }
 
-static bool use_fast(const Plan& p) {
-    if (!p.fast1d || p.wt != INFT_WEIGHTS_REAL) return false;
-    return p.prec == INFT_C128 ? spread_fast_for<double>(p.m, p.S[0]) != nullptr
-                               : spread_fast_for<float>(p.m, p.S[0]) != nullptr;
-}
-
 template <typename T>
 static void spread(Plan& p, const C2<T>* f, C2<T>* grid, int64_t R, cudaStream_t st) {
+    if (stream1d_available(p)) {
+        spread_stream1d(p, f, grid, R, st);
+        return;
+    }
     const T* w = p.w.as<T>();
-    if (p.d == 1 && use_fast(p)) {
-        int nseg = (int)p.nseg[0];
-        int nchunks = (int)ceil_div(nseg, kQ);
-        int nrg = (int)ceil_div(R, 32);
-        int64_t warps = (int64_t)nchunks * nrg;
-        spread_fast_for<T>(p.m, p.S[0])<<<blocks_for(warps * 32, 128), 128, 0, st>>>(
-            p.seg_start.as<int32_t>(), p.delta.as<int32_t>(), p.perm.as<int32_t>(), p.perm_identity ? 1 : 0, w,
-            p.PP, f, grid, p.N, p.Ms[0], nseg, kQ, nchunks, (int)R, nrg);
-    } else if (p.d == 1) {
+    if (p.d == 1) {
         int64_t total = R * p.Ms[0];
         if (p.wt == INFT_WEIGHTS_COMPLEX)
             k_spread_generic_1d<T, true><<<gs_blocks(total, 256), 256, 0, st>>>(
                 p.seg_start.as<int32_t>(), p.n0s.as<int32_t>(), p.perm.as<int32_t>(), w, p.PP, p.P, f, grid, p.N,
-                p.Ms[0], p.S[0], (int)R);
+                p.Ms[0], p.GS, p.S[0], (int)R);
         else
             k_spread_generic_1d<T, false><<<gs_blocks(total, 256), 256, 0, st>>>(
                 p.seg_start.as<int32_t>(), p.n0s.as<int32_t>(), p.perm.as<int32_t>(), w, p.PP, p.P, f, grid, p.N,
-                p.Ms[0], p.S[0], (int)R);
+                p.Ms[0], p.GS, p.S[0], (int)R);
     } else {
         int64_t total = R * p.Mstot;
         if (p.wt == INFT_WEIGHTS_COMPLEX)
@@ -532,33 +258,27 @@ static void spread(Plan& p, const C2<T>* f, C2<T>* grid, int64_t R, cudaStream_t
 template <typename T>
 static void gather(Plan& p, const C2<T>* grid, C2<T>* f, int64_t R, cudaStream_t st) {
     if (p.N == 0) return;
-    const T* w = p.w.as<T>();
-    if (p.d == 1 && use_fast(p)) {
-        int nseg = (int)p.nseg[0];
-        int nchunks = (int)ceil_div(nseg, kQ);
-        int nrg = (int)ceil_div(R, 32);
-        int64_t warps = (int64_t)nchunks * nrg;
-        gather_fast_for<T>(p.m, p.S[0])<<<blocks_for(warps * 32, 128), 128, 0, st>>>(
-            p.seg_start.as<int32_t>(), p.delta.as<int32_t>(), p.perm.as<int32_t>(), p.perm_identity ? 1 : 0, w,
-            p.PP, grid, f, p.N, p.Ms[0], nseg, kQ, nchunks, (int)R, nrg);
-    } else {
-        int64_t total = R * p.N;
-        if (p.wt == INFT_WEIGHTS_COMPLEX)
-            k_gather_generic<T, true><<<gs_blocks(total, 256), 256, 0, st>>>(
-                p.n0s.as<int32_t>(), p.perm.as<int32_t>(), w, p.PP, p.P1, p.d, grid, f, p.N, p.Ms[0], p.Ms[1],
-                (int)R);
-        else
-            k_gather_generic<T, false><<<gs_blocks(total, 256), 256, 0, st>>>(
-                p.n0s.as<int32_t>(), p.perm.as<int32_t>(), w, p.PP, p.P1, p.d, grid, f, p.N, p.Ms[0], p.Ms[1],
-                (int)R);
+    if (stream1d_available(p)) {
+        gather_stream1d(p, grid, f, R, st);
+        return;
     }
+    const T* w = p.w.as<T>();
+    int64_t total = R * p.N;
+    if (p.wt == INFT_WEIGHTS_COMPLEX)
+        k_gather_generic<T, true><<<gs_blocks(total, 256), 256, 0, st>>>(p.n0s.as<int32_t>(), p.perm.as<int32_t>(), w,
+                                                                       p.PP, p.P1, p.d, grid, f, p.N, p.Ms[0],
+                                                                       p.Ms[1], p.GS, (int)R);
+    else
+        k_gather_generic<T, false><<<gs_blocks(total, 256), 256, 0, st>>>(p.n0s.as<int32_t>(), p.perm.as<int32_t>(),
+                                                                        w, p.PP, p.P1, p.d, grid, f, p.N, p.Ms[0],
+                                                                        p.Ms[1], p.GS, (int)R);
     INFT_CHECK_LAUNCH();
     p.launches++;
 }
 
 static void ensure_grid(Plan& p, int64_t rhs) {
     if (p.grid_rhs >= rhs && p.grid.p) return;
-    p.grid.alloc((size_t)rhs * p.Mstot * p.elem_bytes());
+    p.grid.alloc((size_t)rhs * p.GS * p.elem_bytes());
     p.grid_rhs = rhs;
 }
 
@@ -567,7 +287,7 @@ static int64_t grid_capacity(Plan& p, int64_t want) {
     size_t fr = 0, tot = 0;
     cudaMemGetInfo(&fr, &tot);
     size_t budget = std::min<size_t>(fr / 3, (size_t)8 << 30);
-    int64_t cap = std::max<int64_t>(1, (int64_t)(budget / ((size_t)p.Mstot * p.elem_bytes())));
+    int64_t cap = std::max<int64_t>(1, (int64_t)(budget / ((size_t)p.GS * p.elem_bytes())));
     cap = std::max<int64_t>(cap, p.grid_rhs);
     return std::min<int64_t>(want, cap);
 }
@@ -578,7 +298,9 @@ static cufftHandle fft_plan(Plan& p, int batch) {
     cufftHandle h;
     int n[2] = {(int)p.Ms[0], (int)p.Ms[1]};
     cufftType ty = p.prec == INFT_C128 ? CUFFT_Z2Z : CUFFT_C2C;
-    INFT_CUFFT(cufftPlanMany(&h, p.d, n, nullptr, 1, (int)p.Mstot, nullptr, 1, (int)p.Mstot, ty, batch));
+    // 1-D rows carry a halo: storage length GS >= M_sigma per batch entry
+    int emb[2] = {(int)(p.d == 1 ? p.GS : p.Ms[0]), (int)p.Ms[1]};
+    INFT_CUFFT(cufftPlanMany(&h, p.d, n, emb, 1, (int)p.GS, emb, 1, (int)p.GS, ty, batch));
     p.fft[FftKey{batch}] = h;
     return h;
 }
@@ -642,7 +364,7 @@ static void inverse_chunk(Plan& p, const void* f, void* fhat, int64_t Rc, cudaSt
     int64_t total = Rc * p.Mtot;
     k_trunc_deconv<T><<<gs_blocks(total, 256), 256, 0, st>>>(g, static_cast<C2<T>*>(fhat), dtable<T>(p), p.M[0],
                                                              p.d == 2 ? p.M[1] : 1, p.Ms[0],
-                                                             p.d == 2 ? p.Ms[1] : 1, p.d, (int)Rc);
+                                                             p.d == 2 ? p.Ms[1] : 1, p.GS, p.d, (int)Rc);
     INFT_CHECK_LAUNCH();
     p.launches++;
 }
@@ -657,7 +379,7 @@ static void adjoint_chunk(Plan& p, const void* h, void* f, int64_t Rc, cudaStrea
         StageTimer t(p, 3, st);
         k_deconv_pad<T><<<gs_blocks(total, 256), 256, 0, st>>>(static_cast<const C2<T>*>(h), g, dtable<T>(p), p.M[0],
                                                                p.d == 2 ? p.M[1] : 1, p.Ms[0],
-                                                               p.d == 2 ? p.Ms[1] : 1, p.d, (int)Rc);
+                                                               p.d == 2 ? p.Ms[1] : 1, p.GS, p.d, (int)Rc);
         INFT_CHECK_LAUNCH();
         p.launches++;
     }

@@ -75,6 +75,7 @@ struct Plan {
     int64_t nseg_tot = 1;
     bool perm_identity = true;
     bool fast1d = false;
+    int64_t GS = 1;  // grid row stride in complex elements (1-D fast path: M_sigma + halo)
 
     // method state
     int method = -1;
@@ -149,11 +150,51 @@ void compute_deconv(Plan& p, double s, cudaStream_t st);
 // apply.cu
 void apply_inverse(Plan& p, const void* f, void* fhat, int64_t R, cudaStream_t st);
 void apply_adjoint(Plan& p, const void* h, void* f, int64_t R, cudaStream_t st);
+// stream1d.cu
+bool stream1d_available(const Plan& p);
+void spread_stream1d(Plan& p, const void* f, void* grid, int64_t R, cudaStream_t st);
+void gather_stream1d(Plan& p, const void* grid, void* f, int64_t R, cudaStream_t st);
 // setup.cu
 void precompute(Plan& p, inft_method method, inft_weights wt, double tau, cudaStream_t st);
 
 bool is_device_pointer(const void* ptr);
 
 inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
+
+#ifdef __CUDACC__
+__device__ __forceinline__ int64_t dmod(int64_t a, int64_t n) {
+    int64_t r = a % n;
+    return r < 0 ? r + n : r;
+}
+
+// Call fn(s) once for every distinct segment (width S, nseg = ceil(Ms/S)) that
+// touches the periodic grid range [n - span + 1, n] (mod Ms).  A range may
+// re-enter its first segment after wrapping (Ms <= 2S, or span >= Ms); each
+// segment is still visited once, so no node is counted twice.
+template <typename Fn>
+__device__ __forceinline__ void for_segments(int64_t n, int64_t span, int64_t Ms, int S, int64_t nseg, Fn&& fn) {
+    if (span >= Ms) {
+        for (int64_t s = 0; s < nseg; ++s) fn(s);
+        return;
+    }
+    int64_t seen[4];
+    int ns = 0;
+    int64_t pos = dmod(n - (span - 1), Ms), rem = span;
+    while (rem > 0) {
+        int64_t s = pos / S;
+        bool dup = false;
+        for (int k = 0; k < ns; ++k) dup |= (seen[k] == s);
+        if (!dup) {
+            if (ns < 4) seen[ns++] = s;
+            fn(s);
+        }
+        int64_t send = ((s + 1) * S < Ms) ? (s + 1) * S : Ms;
+        int64_t len = (send - pos < rem) ? send - pos : rem;
+        rem -= len;
+        pos += len;
+        if (pos == Ms) pos = 0;
+    }
+}
+#endif
 
 }  // namespace inft

@@ -11,6 +11,7 @@
 #include <cstring>
 #include <limits>
 
+#include "common.cuh"
 #include "inft_internal.cuh"
 
 namespace inft {
@@ -104,10 +105,6 @@ bool is_device_pointer(const void* ptr) {
 }
 
 // ------------------------------------------------------------------ kernels
-__device__ __forceinline__ int64_t mod64(int64_t a, int64_t n) {
-    int64_t r = a % n;
-    return r < 0 ? r + n : r;
-}
 
 // One thread per node: range check, l0 (caller order), tile bin.
 __global__ void k_bins(const double* __restrict__ x, int64_t N, int d, int64_t Ms0, int64_t Ms1,
@@ -190,7 +187,8 @@ __global__ void k_d2f(const double* __restrict__ a, float* __restrict__ b, int64
 // Sort caller-order weights into the padded sorted records of the plan precision.
 template <typename T>
 __global__ void k_sort_weights(const double* __restrict__ wcaller, const int32_t* __restrict__ perm, int64_t N,
-                               int P, int PP, int cplx, T* __restrict__ wsorted, double* __restrict__ w64sorted) {
+                               int P, int PP, int cplx, T* __restrict__ wsorted, double* __restrict__ w64sorted,
+                               const int32_t* __restrict__ n0s, int d) {
     int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (idx >= N * PP) return;
     int64_t i = idx / PP;
@@ -207,7 +205,8 @@ __global__ void k_sort_weights(const double* __restrict__ wcaller, const int32_t
         }
     } else {
         double v = t < P ? wcaller[j * P + t] : 0.0;
-        wsorted[idx] = (T)v;
+        // record = P weights, then n0 (int32 bits) in the first padding slot
+        wsorted[idx] = (t == P) ? n0_as(T(0), n0s[i * d]) : (T)v;
         if (t < P) w64sorted[i * P + t] = v;
     }
 }
@@ -215,7 +214,7 @@ __global__ void k_sort_weights(const double* __restrict__ wcaller, const int32_t
 // From sorted double weights (setup output) into padded plan-precision records.
 template <typename T>
 __global__ void k_pack_sorted(const double* __restrict__ w64sorted, int64_t N, int P, int PP, int cplx,
-                              T* __restrict__ wsorted) {
+                              T* __restrict__ wsorted, const int32_t* __restrict__ n0s, int d) {
     int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (idx >= N * PP) return;
     int64_t i = idx / PP;
@@ -224,7 +223,7 @@ __global__ void k_pack_sorted(const double* __restrict__ w64sorted, int64_t N, i
         wsorted[idx * 2] = (T)(t < P ? w64sorted[(i * P + t) * 2] : 0.0);
         wsorted[idx * 2 + 1] = (T)(t < P ? w64sorted[(i * P + t) * 2 + 1] : 0.0);
     } else {
-        wsorted[idx] = (T)(t < P ? w64sorted[i * P + t] : 0.0);
+        wsorted[idx] = (t == P) ? n0_as(T(0), n0s[i * d]) : (T)(t < P ? w64sorted[i * P + t] : 0.0);
     }
 }
 
@@ -261,7 +260,7 @@ void plan_build(Plan& p, const double* nodes_any, cudaStream_t st) {
         p.nseg[0] = ceil_div(p.Ms[0], p.S[0]);
         p.nseg[1] = 1;
     } else {
-        p.S[0] = p.S[1] = 16;
+        p.S[0] = p.S[1] = choose_segment(p.m);
         p.nseg[0] = ceil_div(p.Ms[0], p.S[0]);
         p.nseg[1] = ceil_div(p.Ms[1], p.S[1]);
     }
@@ -336,7 +335,8 @@ void plan_build(Plan& p, const double* nodes_any, cudaStream_t st) {
     p.fast1d = (d == 1) && (p.m <= 16) && (p.Ms[0] % p.S[0] == 0) && (p.nseg[0] >= 2) && (p.P1 <= p.Ms[0]);
     // padded record stride: 16-byte aligned rows
     int vec = p.prec == INFT_C128 ? 2 : 4;
-    p.PP = (int)ceil_div(p.P, vec) * vec;
+    p.PP = (int)ceil_div(p.P + 1, vec) * vec;  // >= 1 padding slot (holds n0 for the streaming kernels)
+    p.GS = p.fast1d ? p.Ms[0] + ceil_div(2 * p.m, 8) * 8 : p.Mstot;
     compute_deconv(p, 1.0, st);
 }
 
@@ -410,11 +410,11 @@ void upload_weights(Plan& p, const double* w_host, inft_method method, inft_weig
         if (p.prec == INFT_C128)
             k_sort_weights<double><<<grid1d(p.N * p.PP), 256, 0, st>>>(tmp.as<double>(), p.perm.as<int32_t>(), p.N,
                                                                       p.P, p.PP, cp == 2, p.w.as<double>(),
-                                                                      p.w64.as<double>());
+                                                                      p.w64.as<double>(), p.n0s.as<int32_t>(), p.d);
         else
             k_sort_weights<float><<<grid1d(p.N * p.PP), 256, 0, st>>>(tmp.as<double>(), p.perm.as<int32_t>(), p.N,
                                                                      p.P, p.PP, cp == 2, p.w.as<float>(),
-                                                                     p.w64.as<double>());
+                                                                     p.w64.as<double>(), p.n0s.as<int32_t>(), p.d);
         INFT_CHECK_LAUNCH();
         p.launches++;
     }
@@ -432,10 +432,10 @@ void install_weights_from_device(Plan& p, const double* w64_sorted_dev, inft_met
         INFT_CUDA(cudaMemcpyAsync(p.w64.p, w64_sorted_dev, sizeof(double) * n, cudaMemcpyDeviceToDevice, st));
         if (p.prec == INFT_C128)
             k_pack_sorted<double><<<grid1d(p.N * p.PP), 256, 0, st>>>(p.w64.as<double>(), p.N, p.P, p.PP, cp == 2,
-                                                                     p.w.as<double>());
+                                                                     p.w.as<double>(), p.n0s.as<int32_t>(), p.d);
         else
             k_pack_sorted<float><<<grid1d(p.N * p.PP), 256, 0, st>>>(p.w64.as<double>(), p.N, p.P, p.PP, cp == 2,
-                                                                    p.w.as<float>());
+                                                                    p.w.as<float>(), p.n0s.as<int32_t>(), p.d);
         INFT_CHECK_LAUNCH();
         p.launches++;
     }

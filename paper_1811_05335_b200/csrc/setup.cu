@@ -80,22 +80,15 @@ template <typename Fn>
 __device__ void for_column(const ColCtx& c, int64_t n, int lane, int nlanes, Fn&& fn) {
     int64_t n1 = c.d == 2 ? n / c.Ms2 : n;
     int64_t n2 = c.d == 2 ? n - (n / c.Ms2) * c.Ms2 : 0;
-    int64_t span1 = std::min<int64_t>(c.P1, c.Ms1);
-    int64_t pos1 = md(n1 - (span1 - 1), c.Ms1), rem1 = span1;
-    while (rem1 > 0) {
-        int64_t s1 = pos1 / c.S1;
-        int64_t len1 = std::min<int64_t>(std::min<int64_t>((s1 + 1) * c.S1, c.Ms1) - pos1, rem1);
+    const int64_t nseg1 = (c.Ms1 + c.S1 - 1) / c.S1;
+    for_segments(n1, std::min<int64_t>(c.P1, c.Ms1), c.Ms1, c.S1, nseg1, [&](int64_t s1) {
         if (c.d == 1) {
             for (int64_t i = c.seg_start[s1] + lane; i < c.seg_start[s1 + 1]; i += nlanes) {
                 int64_t t = live_slot(n1, c.n0s[i], c.xs[i], c.l0s[i], c.P1, c.Ms1, c.m);
                 if (t >= 0) fn(i, t);
             }
         } else {
-            int64_t span2 = std::min<int64_t>(c.P1, c.Ms2);
-            int64_t pos2 = md(n2 - (span2 - 1), c.Ms2), rem2 = span2;
-            while (rem2 > 0) {
-                int64_t s2 = pos2 / c.S2;
-                int64_t len2 = std::min<int64_t>(std::min<int64_t>((s2 + 1) * c.S2, c.Ms2) - pos2, rem2);
+            for_segments(n2, std::min<int64_t>(c.P1, c.Ms2), c.Ms2, c.S2, c.nseg2, [&](int64_t s2) {
                 int64_t tile = s1 * c.nseg2 + s2;
                 for (int64_t i = c.seg_start[tile] + lane; i < c.seg_start[tile + 1]; i += nlanes) {
                     int64_t t1 = live_slot(n1, c.n0s[2 * i], c.xs[2 * i], c.l0s[2 * i], c.P1, c.Ms1, c.m);
@@ -104,15 +97,9 @@ __device__ void for_column(const ColCtx& c, int64_t n, int lane, int nlanes, Fn&
                     if (t2 < 0) continue;
                     fn(i, t1 * c.P1 + t2);
                 }
-                rem2 -= len2;
-                pos2 += len2;
-                if (pos2 == c.Ms2) pos2 = 0;
-            }
+            });
         }
-        rem1 -= len1;
-        pos1 += len1;
-        if (pos1 == c.Ms1) pos1 = 0;
-    }
+    });
 }
 
 __global__ void k_col_count(ColCtx c, int64_t ncol, int32_t* __restrict__ cnt) {

@@ -1,0 +1,616 @@
+// 1-D streaming spread (a2) and gather (a7) kernels for real B_opt weights.
+//
+// Both walk the bin-sorted node stream of a chunk of Q consecutive grid
+// segments (width SEG >= 2m) with lane = right-hand side, keeping a window of
+// SEG + 2m grid values per lane in registers.  A node's slot base n0 lies in
+// its segment, so its P = 2m+1 taps hit window registers delta .. delta+2m,
+// delta = n0 - seg*SEG; a warp-uniform switch on delta makes every register
+// index static.  No atomics, deterministic summation order.
+//
+// k_spread_tma_1d / k_gather_tma_1d (caller node order == sorted order, the 1-D
+// configs): every operand is staged through shared memory by the async copy
+// engines in a kStages-deep mbarrier pipeline issued by one thread --
+//   * node records (P weights + n0) by 1-D bulk copy (cp.async.bulk),
+//   * spread: the f tile [rows = block RHS][16 nodes] by 2-D TMA
+//     (cp.async.bulk.tensor, SWIZZLE_128B, OOB zero fill),
+//   * gather: the next SEG grid points of every row by 2-D TMA over a grid
+//     whose rows carry a 2m halo (filled after the FFT), so windows never wrap.
+// The register-window kernels without staging remain for non-identity node
+// permutations (per-lane gathers of f through perm).
+#include <algorithm>
+
+#include "common.cuh"
+#include "inft_internal.cuh"
+#include "tma.cuh"
+
+namespace inft {
+
+static constexpr int kQ = 32;       // segments per chunk
+static constexpr int kNB = 16;      // nodes per staged batch
+static constexpr int kStages = 4;   // pipeline depth
+
+// ---------------------------------------------------------------------------------
+// Spread, staged.  grid[r][n] (row stride GS) for n in the chunk's segments.
+template <typename T, int MC, int SEG>
+__global__ void __launch_bounds__(128) k_spread_tma_1d(const __grid_constant__ CUtensorMap fmap,
+                                                       const int32_t* __restrict__ seg_start,
+                                                       const T* __restrict__ w, int PP, C2<T>* __restrict__ grid,
+                                                       int64_t GS, int nseg, int Q, int R) {
+    constexpr int P = 2 * MC + 1;
+    constexpr int K = SEG + 2 * MC;
+    constexpr int EB = 128 / (int)sizeof(C2<T>);  // complex values per 128-byte box row
+    constexpr int NBOX = kNB / EB;
+    static_assert(SEG >= 2 * MC && SEG <= 32, "segment must cover the support");
+    const int WPB = blockDim.x >> 5;
+    const int rows = blockDim.x;
+    const int lane = threadIdx.x & 31;
+    const int row = threadIdx.x;
+    const int r = blockIdx.y * rows + row;
+    const bool active = r < R;
+
+    extern __shared__ unsigned char smem_raw[];
+    unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    const uint32_t box_bytes = (uint32_t)rows * 128u;
+    const uint32_t fstage = NBOX * box_bytes;
+    const uint32_t rstage = (uint32_t)((kNB * PP * (int)sizeof(T) + 127) & ~127);
+    unsigned char* fbuf = smem;
+    unsigned char* rbuf = smem + kStages * fstage;
+    uint64_t* full = reinterpret_cast<uint64_t*>(rbuf + kStages * rstage);
+    uint64_t* empty = full + kStages;
+
+    const int s0 = blockIdx.x * Q;
+    const int s1 = min(s0 + Q, nseg);
+    const int sp = s0 == 0 ? nseg - 1 : s0 - 1;
+    const int a0 = __ldg(seg_start + sp), a1 = __ldg(seg_start + sp + 1);
+    const int b0 = __ldg(seg_start + s0), b1 = __ldg(seg_start + s1);
+    const int nA = (a1 - a0 + kNB - 1) / kNB;
+    const int nb = nA + (b1 - b0 + kNB - 1) / kNB;
+
+    auto batch_pos = [&](int b, int& pos, int& cnt) {
+        if (b < nA) {
+            pos = a0 + b * kNB;
+            cnt = min(kNB, a1 - pos);
+        } else {
+            pos = b0 + (b - nA) * kNB;
+            cnt = min(kNB, b1 - pos);
+        }
+    };
+    auto issue = [&](int b, int stage) {
+        int pos, cnt;
+        batch_pos(b, pos, cnt);
+        const uint32_t rbytes = (uint32_t)(cnt * PP * (int)sizeof(T));
+        mbar_arrive_expect_tx(&full[stage], fstage + rbytes);
+#pragma unroll
+        for (int bx = 0; bx < NBOX; ++bx)
+            tma_load_2d(fbuf + stage * fstage + bx * box_bytes, &fmap, 2 * (pos + bx * EB), blockIdx.y * rows,
+                        &full[stage]);
+        bulk_g2s(rbuf + stage * rstage, w + (int64_t)pos * PP, rbytes, &full[stage]);
+    };
+
+    if (threadIdx.x == 0) {
+        prefetch_tmap(&fmap);
+        for (int i = 0; i < kStages; ++i) {
+            mbar_init(&full[i], 1);
+            mbar_init(&empty[i], WPB);
+        }
+        fence_barrier_init();
+    }
+    __syncthreads();
+    if (threadIdx.x == 0)
+        for (int b = 0; b < min(kStages, nb); ++b) issue(b, b);
+
+    T ax[K], ay[K];
+#pragma unroll
+    for (int u = 0; u < K; ++u) ax[u] = ay[u] = T(0);
+    int cur_k = 0;  // 0 = prologue segment sp, k >= 1 = main segment s0 + k - 1
+    C2<T>* __restrict__ gr = grid + (int64_t)(active ? r : 0) * GS;
+    auto flush = [&]() {
+        if (cur_k >= 1 && active) {
+            C2<T>* out = gr + (int64_t)(s0 + cur_k - 1) * SEG;
+#pragma unroll
+            for (int u = 0; u < SEG; ++u) __stcs(out + u, mk<T>(ax[u], ay[u]));
+        }
+#pragma unroll
+        for (int u = 0; u < K; ++u) {
+            ax[u] = (u + SEG < K) ? ax[u + SEG] : T(0);
+            ay[u] = (u + SEG < K) ? ay[u + SEG] : T(0);
+        }
+        ++cur_k;
+    };
+
+    for (int b = 0; b < nb; ++b) {
+        const int stage = b % kStages;
+        const uint32_t parity = (uint32_t)((b / kStages) & 1);
+        int pos, cnt;
+        batch_pos(b, pos, cnt);
+        mbar_wait(&full[stage], parity);
+        const unsigned char* fb = fbuf + stage * fstage;
+        const T* rb = reinterpret_cast<const T*>(rbuf + stage * rstage);
+        const bool pro = b < nA;
+        for (int q = 0; q < cnt; ++q) {
+            const T* rec = rb + q * PP;
+            const int n0 = rec_n0(rec, P);
+            const int seg = n0 / SEG;
+            const int dl = n0 - seg * SEG;
+            const int kq = pro ? 0 : seg - s0 + 1;
+            while (cur_k < kq) flush();
+            const int bx = q / EB, c = q % EB;
+            C2<T> fv;
+            if (sizeof(C2<T>) == 16)
+                fv = *reinterpret_cast<const C2<T>*>(fb + bx * box_bytes + swz128(row, c));
+            else
+                fv = *reinterpret_cast<const C2<T>*>(fb + bx * box_bytes + swz128(row, c >> 1) + (c & 1) * 8);
+            T wv[P];
+            WeightLoader<T, P>::load_smem(rec, wv);
+            switch (dl) {
+#define INFT_SPREAD_CASE(D)                                       \
+    case D:                                                       \
+        if constexpr (D < SEG) {                                  \
+            _Pragma("unroll") for (int t = 0; t < P; ++t) {       \
+                ax[D + t] = fma(wv[t], fv.x, ax[D + t]);          \
+                ay[D + t] = fma(wv[t], fv.y, ay[D + t]);          \
+            }                                                     \
+        }                                                         \
+        break;
+                INFT_CASES_32(INFT_SPREAD_CASE)
+#undef INFT_SPREAD_CASE
+                default:
+                    break;
+            }
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[stage]);
+        if (threadIdx.x == 0 && b + kStages < nb) {
+            mbar_wait(&empty[stage], parity);
+            issue(b + kStages, stage);
+        }
+    }
+    while (cur_k <= s1 - s0) flush();
+}
+
+// ---------------------------------------------------------------------------------
+// Gather, staged.  f[r][j] = sum_t w[j][t] g[r][n0_j + t] (grid rows with a 2m halo).
+template <typename T, int MC, int SEG>
+__global__ void __launch_bounds__(128) k_gather_tma_1d(const __grid_constant__ CUtensorMap gmap,
+                                                       const int32_t* __restrict__ seg_start,
+                                                       const T* __restrict__ w, int PP, C2<T>* __restrict__ f,
+                                                       int64_t N, int nseg, int Q, int R) {
+    constexpr int P = 2 * MC + 1;
+    constexpr int K = SEG + 2 * MC;
+    constexpr int EB = 128 / (int)sizeof(C2<T>);
+    constexpr int NWB = (SEG + EB - 1) / EB;  // boxes per window load
+    const int WPB = blockDim.x >> 5;
+    const int rows = blockDim.x;
+    const int lane = threadIdx.x & 31;
+    const int row = threadIdx.x;
+    const int r = blockIdx.y * rows + row;
+    const bool active = r < R;
+
+    extern __shared__ unsigned char smem_raw[];
+    unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    const uint32_t box_bytes = (uint32_t)rows * 128u;
+    const uint32_t wstage = NWB * box_bytes;
+    const uint32_t rstage = (uint32_t)((kNB * PP * (int)sizeof(T) + 127) & ~127);
+    unsigned char* wbuf = smem;
+    unsigned char* rbuf = smem + kStages * wstage;
+    uint64_t* fullW = reinterpret_cast<uint64_t*>(rbuf + kStages * rstage);
+    uint64_t* emptyW = fullW + kStages;
+    uint64_t* fullR = emptyW + kStages;
+    uint64_t* emptyR = fullR + kStages;
+
+    const int s0 = blockIdx.x * Q;
+    const int s1 = min(s0 + Q, nseg);
+    const int nbox = s1 - s0 + 1;  // box L holds grid [(s0-1+L)*SEG + 2m, ... + SEG)
+    const int b0 = __ldg(seg_start + s0), b1 = __ldg(seg_start + s1);
+    const int nbat = (b1 - b0 + kNB - 1) / kNB;
+
+    auto issueW = [&](int L, int stage) {
+        mbar_arrive_expect_tx(&fullW[stage], wstage);
+        const int col = (s0 - 1 + L) * SEG + 2 * MC;
+#pragma unroll
+        for (int bx = 0; bx < NWB; ++bx)
+            tma_load_2d(wbuf + stage * wstage + bx * box_bytes, &gmap, 2 * (col + bx * EB), blockIdx.y * rows,
+                        &fullW[stage]);
+    };
+    auto issueR = [&](int b, int stage) {
+        const int pos = b0 + b * kNB;
+        const int cnt = min(kNB, b1 - pos);
+        const uint32_t rbytes = (uint32_t)(cnt * PP * (int)sizeof(T));
+        mbar_arrive_expect_tx(&fullR[stage], rbytes);
+        bulk_g2s(rbuf + stage * rstage, w + (int64_t)pos * PP, rbytes, &fullR[stage]);
+    };
+
+    if (threadIdx.x == 0) {
+        prefetch_tmap(&gmap);
+        for (int i = 0; i < kStages; ++i) {
+            mbar_init(&fullW[i], 1);
+            mbar_init(&emptyW[i], WPB);
+            mbar_init(&fullR[i], 1);
+            mbar_init(&emptyR[i], WPB);
+        }
+        fence_barrier_init();
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        for (int L = 0; L < min(kStages, nbox); ++L) issueW(L, L);
+        for (int b = 0; b < min(kStages, nbat); ++b) issueR(b, b);
+    }
+
+    T wx[K], wy[K];
+    int nextL = 0;
+    // load box nextL into window registers [2m, K)
+    auto consume_box = [&]() {
+        const int L = nextL++;
+        const int stage = L % kStages;
+        const uint32_t parity = (uint32_t)((L / kStages) & 1);
+        mbar_wait(&fullW[stage], parity);
+        const unsigned char* wb = wbuf + stage * wstage;
+#pragma unroll
+        for (int v = 0; v < SEG; ++v) {
+            const int bx = v / EB, c = v % EB;
+            C2<T> g;
+            if (sizeof(C2<T>) == 16)
+                g = *reinterpret_cast<const C2<T>*>(wb + bx * box_bytes + swz128(row, c));
+            else
+                g = *reinterpret_cast<const C2<T>*>(wb + bx * box_bytes + swz128(row, c >> 1) + (c & 1) * 8);
+            wx[2 * MC + v] = g.x;
+            wy[2 * MC + v] = g.y;
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&emptyW[stage]);
+        if (threadIdx.x == 0 && L + kStages < nbox) {
+            mbar_wait(&emptyW[stage], parity);
+            issueW(L + kStages, stage);
+        }
+    };
+    int cur_j = -1;
+    auto advance = [&]() {
+#pragma unroll
+        for (int u = 0; u < 2 * MC; ++u) {
+            wx[u] = wx[u + SEG];
+            wy[u] = wy[u + SEG];
+        }
+        consume_box();
+        ++cur_j;
+    };
+    consume_box();
+
+    C2<T>* __restrict__ fr = f + (int64_t)(active ? r : 0) * N;
+    for (int b = 0; b < nbat; ++b) {
+        const int stage = b % kStages;
+        const uint32_t parity = (uint32_t)((b / kStages) & 1);
+        const int pos = b0 + b * kNB;
+        const int cnt = min(kNB, b1 - pos);
+        mbar_wait(&fullR[stage], parity);
+        const T* rb = reinterpret_cast<const T*>(rbuf + stage * rstage);
+        for (int q = 0; q < cnt; ++q) {
+            const T* rec = rb + q * PP;
+            const int n0 = rec_n0(rec, P);
+            const int seg = n0 / SEG;
+            const int dl = n0 - seg * SEG;
+            while (cur_j < seg - s0) advance();
+            T wv[P];
+            WeightLoader<T, P>::load_smem(rec, wv);
+            T sx = 0, sy = 0;
+            switch (dl) {
+#define INFT_GATHER_CASE(D)                                   \
+    case D:                                                   \
+        if constexpr (D < SEG) {                              \
+            _Pragma("unroll") for (int t = 0; t < P; ++t) {   \
+                sx = fma(wv[t], wx[D + t], sx);               \
+                sy = fma(wv[t], wy[D + t], sy);               \
+            }                                                 \
+        }                                                     \
+        break;
+                INFT_CASES_32(INFT_GATHER_CASE)
+#undef INFT_GATHER_CASE
+                default:
+                    break;
+            }
+            if (active) __stcs(fr + pos + q, mk<T>(sx, sy));
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&emptyR[stage]);
+        if (threadIdx.x == 0 && b + kStages < nbat) {
+            mbar_wait(&emptyR[stage], parity);
+            issueR(b + kStages, stage);
+        }
+    }
+    while (nextL < nbox) advance();  // drain: no bulk copy may be in flight at exit
+}
+
+// ---------------------------------------------------------------------------------
+// Register-window kernels without staging (any node permutation).
+template <typename T, int MC, int SEG>
+__global__ void __launch_bounds__(128) k_spread_reg_1d(
+    const int32_t* __restrict__ seg_start, const int32_t* __restrict__ delta, const int32_t* __restrict__ perm,
+    const T* __restrict__ w, int PP, const C2<T>* __restrict__ f, C2<T>* __restrict__ grid, int64_t N, int64_t GS,
+    int nseg, int Q, int nchunks, int R, int nrg) {
+    constexpr int P = 2 * MC + 1;
+    constexpr int K = SEG + 2 * MC;
+    const int lane = threadIdx.x & 31;
+    const int64_t gw = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    if (gw >= (int64_t)nchunks * nrg) return;
+    const int chunk = (int)(gw / nrg);
+    const int rg = (int)(gw - (int64_t)chunk * nrg);
+    const int r = rg * 32 + lane;
+    const bool active = r < R;
+    const C2<T>* __restrict__ fr = f + (int64_t)(active ? r : 0) * N;
+    C2<T>* __restrict__ gr = grid + (int64_t)(active ? r : 0) * GS;
+    T ax[K], ay[K];
+#pragma unroll
+    for (int u = 0; u < K; ++u) ax[u] = ay[u] = T(0);
+    const int s0 = chunk * Q;
+    const int s1 = min(s0 + Q, nseg);
+    for (int si = s0 - 1; si < s1; ++si) {
+        const int s = si < 0 ? si + nseg : si;
+        const int i0 = __ldg(seg_start + s), i1 = __ldg(seg_start + s + 1);
+        for (int i = i0; i < i1; ++i) {
+            const int dl = __ldg(delta + i);
+            const int64_t j = __ldg(perm + i);
+            C2<T> fv = mk<T>(T(0), T(0));
+            if (active) fv = __ldg(fr + j);
+            T wv[P];
+            WeightLoader<T, P>::load(w + (int64_t)i * PP, wv);
+            switch (dl) {
+#define INFT_SPREAD_CASE(D)                                       \
+    case D:                                                       \
+        if constexpr (D < SEG) {                                  \
+            _Pragma("unroll") for (int t = 0; t < P; ++t) {       \
+                ax[D + t] = fma(wv[t], fv.x, ax[D + t]);          \
+                ay[D + t] = fma(wv[t], fv.y, ay[D + t]);          \
+            }                                                     \
+        }                                                         \
+        break;
+                INFT_CASES_32(INFT_SPREAD_CASE)
+#undef INFT_SPREAD_CASE
+                default:
+                    break;
+            }
+        }
+        if (si >= s0 && active) {
+            C2<T>* out = gr + (int64_t)s * SEG;
+#pragma unroll
+            for (int u = 0; u < SEG; ++u) out[u] = mk<T>(ax[u], ay[u]);
+        }
+#pragma unroll
+        for (int u = 0; u < K; ++u) {
+            ax[u] = (u + SEG < K) ? ax[u + SEG] : T(0);
+            ay[u] = (u + SEG < K) ? ay[u + SEG] : T(0);
+        }
+    }
+}
+
+template <typename T, int MC, int SEG>
+__global__ void __launch_bounds__(128) k_gather_reg_1d(
+    const int32_t* __restrict__ seg_start, const int32_t* __restrict__ delta, const int32_t* __restrict__ perm,
+    const T* __restrict__ w, int PP, const C2<T>* __restrict__ grid, C2<T>* __restrict__ f, int64_t N, int64_t GS,
+    int64_t Ms, int nseg, int Q, int nchunks, int R, int nrg) {
+    constexpr int P = 2 * MC + 1;
+    constexpr int K = SEG + 2 * MC;
+    const int lane = threadIdx.x & 31;
+    const int64_t gw = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    if (gw >= (int64_t)nchunks * nrg) return;
+    const int chunk = (int)(gw / nrg);
+    const int rg = (int)(gw - (int64_t)chunk * nrg);
+    const int r = rg * 32 + lane;
+    const bool active = r < R;
+    const C2<T>* __restrict__ gr = grid + (int64_t)(active ? r : 0) * GS;
+    C2<T>* __restrict__ fr = f + (int64_t)(active ? r : 0) * N;
+    T wx[K], wy[K];
+    const int s0 = chunk * Q;
+    const int s1 = min(s0 + Q, nseg);
+    for (int s = s0; s < s1; ++s) {
+        const int64_t base = (int64_t)s * SEG;
+#pragma unroll
+        for (int u = 0; u < K; ++u) {
+            if (s != s0 && u + SEG < K) {
+                wx[u] = wx[u + SEG];
+                wy[u] = wy[u + SEG];
+            } else {
+                int64_t q = base + u;
+                if (q >= Ms) q -= Ms;
+                C2<T> v = active ? __ldg(gr + q) : mk<T>(T(0), T(0));
+                wx[u] = v.x;
+                wy[u] = v.y;
+            }
+        }
+        const int i0 = __ldg(seg_start + s), i1 = __ldg(seg_start + s + 1);
+        for (int i = i0; i < i1; ++i) {
+            const int dl = __ldg(delta + i);
+            const int64_t j = __ldg(perm + i);
+            T wv[P];
+            WeightLoader<T, P>::load(w + (int64_t)i * PP, wv);
+            T sx = 0, sy = 0;
+            switch (dl) {
+#define INFT_GATHER_CASE(D)                                   \
+    case D:                                                   \
+        if constexpr (D < SEG) {                              \
+            _Pragma("unroll") for (int t = 0; t < P; ++t) {   \
+                sx = fma(wv[t], wx[D + t], sx);               \
+                sy = fma(wv[t], wy[D + t], sy);               \
+            }                                                 \
+        }                                                     \
+        break;
+                INFT_CASES_32(INFT_GATHER_CASE)
+#undef INFT_GATHER_CASE
+                default:
+                    break;
+            }
+            if (active) fr[j] = mk<T>(sx, sy);
+        }
+    }
+}
+
+// grid[r][Ms + u] = grid[r][u], u < H: the halo that lets gather windows run past M_sigma.
+template <typename T>
+__global__ void k_halo_fill(C2<T>* __restrict__ grid, int64_t GS, int64_t Ms, int H, int R) {
+    const int64_t total = (int64_t)R * H;
+    for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
+         idx += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t r = idx / H;
+        const int64_t u = idx - r * H;
+        grid[r * GS + Ms + u] = grid[r * GS + (u % Ms)];
+    }
+}
+
+// ===================================================================== host side
+template <typename T>
+struct Fns {
+    using SpreadTma = void (*)(const CUtensorMap, const int32_t*, const T*, int, C2<T>*, int64_t, int, int, int);
+    using GatherTma = void (*)(const CUtensorMap, const int32_t*, const T*, int, C2<T>*, int64_t, int, int, int);
+    using SpreadReg = void (*)(const int32_t*, const int32_t*, const int32_t*, const T*, int, const C2<T>*, C2<T>*,
+                               int64_t, int64_t, int, int, int, int, int);
+    using GatherReg = void (*)(const int32_t*, const int32_t*, const int32_t*, const T*, int, const C2<T>*, C2<T>*,
+                               int64_t, int64_t, int64_t, int, int, int, int, int);
+    SpreadTma st = nullptr;
+    GatherTma gt = nullptr;
+    SpreadReg sr = nullptr;
+    GatherReg gr = nullptr;
+};
+
+template <typename T>
+static Fns<T> fns_for(int m, int S) {
+    Fns<T> F;
+#define INFT_FN(MC, SG)                                  \
+    if (m == MC && S == SG) {                            \
+        F.st = k_spread_tma_1d<T, MC, SG>;               \
+        F.gt = k_gather_tma_1d<T, MC, SG>;               \
+        F.sr = k_spread_reg_1d<T, MC, SG>;               \
+        F.gr = k_gather_reg_1d<T, MC, SG>;               \
+    }
+    INFT_FN(1, 16) INFT_FN(2, 16) INFT_FN(3, 16) INFT_FN(4, 16) INFT_FN(5, 16) INFT_FN(6, 16) INFT_FN(7, 16)
+    INFT_FN(8, 16) INFT_FN(10, 32) INFT_FN(12, 32) INFT_FN(16, 32)
+#undef INFT_FN
+    return F;
+}
+
+bool stream1d_available(const Plan& p) {
+    if (p.d != 1 || !p.fast1d || p.wt != INFT_WEIGHTS_REAL) return false;
+    return p.prec == INFT_C128 ? fns_for<double>(p.m, p.S[0]).st != nullptr
+                               : fns_for<float>(p.m, p.S[0]).st != nullptr;
+}
+
+static int wpb_for(int64_t R) { return (int)std::min<int64_t>(4, std::max<int64_t>(1, ceil_div(R, 32))); }
+
+template <typename T>
+static size_t spread_smem(int rows, int PP) {
+    const int EB = 128 / (int)sizeof(C2<T>);
+    size_t fst = (size_t)(kNB / EB) * rows * 128;
+    size_t rst = (size_t)((kNB * PP * (int)sizeof(T) + 127) & ~127);
+    return 1024 + kStages * (fst + rst) + 2 * kStages * sizeof(uint64_t);
+}
+
+template <typename T>
+static size_t gather_smem(int rows, int PP, int S) {
+    const int EB = 128 / (int)sizeof(C2<T>);
+    size_t wst = (size_t)((S + EB - 1) / EB) * rows * 128;
+    size_t rst = (size_t)((kNB * PP * (int)sizeof(T) + 127) & ~127);
+    return 1024 + kStages * (wst + rst) + 4 * kStages * sizeof(uint64_t);
+}
+
+template <typename T>
+static void spread_t(Plan& p, const void* f, void* grid, int64_t R, cudaStream_t st) {
+    Fns<T> F = fns_for<T>(p.m, p.S[0]);
+    const int nseg = (int)p.nseg[0];
+    const int nchunks = (int)ceil_div(nseg, kQ);
+    if (p.perm_identity) {
+        const int wpb = wpb_for(R);
+        const int rows = 32 * wpb;
+        CUtensorMap map;
+        if (!make_tmap_2d(&map, f, sizeof(T) == 8, 2 * (uint64_t)p.N, (uint64_t)R, 2 * sizeof(T) * (uint64_t)p.N,
+                          (uint32_t)rows)) {
+            set_error("cuTensorMapEncodeTiled failed (spread f tile)");
+            throw Fail{INFT_ERR_CUDA};
+        }
+        size_t smem = spread_smem<T>(rows, p.PP);
+        INFT_CUDA(cudaFuncSetAttribute(F.st, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        dim3 grid_dim((unsigned)nchunks, (unsigned)ceil_div(R, rows));
+        F.st<<<grid_dim, rows, smem, st>>>(map, p.seg_start.as<int32_t>(), p.w.as<T>(), p.PP,
+                                           static_cast<C2<T>*>(grid), p.GS, nseg, kQ, (int)R);
+    } else {
+        const int nrg = (int)ceil_div(R, 32);
+        const int64_t warps = (int64_t)nchunks * nrg;
+        F.sr<<<(unsigned)ceil_div(warps * 32, 128), 128, 0, st>>>(
+            p.seg_start.as<int32_t>(), p.delta.as<int32_t>(), p.perm.as<int32_t>(), p.w.as<T>(), p.PP,
+            static_cast<const C2<T>*>(f), static_cast<C2<T>*>(grid), p.N, p.GS, nseg, kQ, nchunks, (int)R, nrg);
+    }
+    INFT_CHECK_LAUNCH();
+    p.launches++;
+}
+
+template <typename T>
+static void gather_t(Plan& p, const void* grid, void* f, int64_t R, cudaStream_t st) {
+    Fns<T> F = fns_for<T>(p.m, p.S[0]);
+    const int nseg = (int)p.nseg[0];
+    const int nchunks = (int)ceil_div(nseg, kQ);
+    if (p.perm_identity) {
+        const int wpb = wpb_for(R);
+        const int rows = 32 * wpb;
+        // halo: grid[r][Ms + u] = grid[r][u]
+        const int H = (int)(p.GS - p.Ms[0]);
+        k_halo_fill<T><<<(unsigned)std::max<int64_t>(1, std::min<int64_t>(ceil_div(R * H, 256), 4096)), 256, 0, st>>>(
+            static_cast<C2<T>*>(const_cast<void*>(grid)), p.GS, p.Ms[0], H, (int)R);
+        INFT_CHECK_LAUNCH();
+        p.launches++;
+        CUtensorMap map;
+        if (!make_tmap_2d(&map, grid, sizeof(T) == 8, 2 * (uint64_t)p.GS, (uint64_t)R, 2 * sizeof(T) * (uint64_t)p.GS,
+                          (uint32_t)rows)) {
+            set_error("cuTensorMapEncodeTiled failed (gather grid window)");
+            throw Fail{INFT_ERR_CUDA};
+        }
+        size_t smem = gather_smem<T>(rows, p.PP, p.S[0]);
+        INFT_CUDA(cudaFuncSetAttribute(F.gt, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        dim3 grid_dim((unsigned)nchunks, (unsigned)ceil_div(R, rows));
+        F.gt<<<grid_dim, rows, smem, st>>>(map, p.seg_start.as<int32_t>(), p.w.as<T>(), p.PP, static_cast<C2<T>*>(f),
+                                           p.N, nseg, kQ, (int)R);
+    } else {
+        const int nrg = (int)ceil_div(R, 32);
+        const int64_t warps = (int64_t)nchunks * nrg;
+        F.gr<<<(unsigned)ceil_div(warps * 32, 128), 128, 0, st>>>(
+            p.seg_start.as<int32_t>(), p.delta.as<int32_t>(), p.perm.as<int32_t>(), p.w.as<T>(), p.PP,
+            static_cast<const C2<T>*>(grid), static_cast<C2<T>*>(f), p.N, p.GS, p.Ms[0], nseg, kQ, nchunks, (int)R,
+            nrg);
+    }
+    INFT_CHECK_LAUNCH();
+    p.launches++;
+}
+
+void spread_stream1d(Plan& p, const void* f, void* grid, int64_t R, cudaStream_t st) {
+    if (p.prec == INFT_C128)
+        spread_t<double>(p, f, grid, R, st);
+    else
+        spread_t<float>(p, f, grid, R, st);
+}
+
+void gather_stream1d(Plan& p, const void* grid, void* f, int64_t R, cudaStream_t st) {
+    if (p.prec == INFT_C128)
+        gather_t<double>(p, grid, f, R, st);
+    else
+        gather_t<float>(p, grid, f, R, st);
+}
+
+// ------------------------------------------------------------------ tensor maps
+bool make_tmap_2d(CUtensorMap* out, const void* base, bool f64, uint64_t inner, uint64_t rows,
+                  uint64_t row_stride_bytes, uint32_t box_rows) {
+    static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
+    if (!encode) {
+        void* fn = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess ||
+            q != cudaDriverEntryPointSuccess || !fn)
+            return false;
+        encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+    }
+    cuuint64_t dims[2] = {inner, rows};
+    cuuint64_t strides[1] = {row_stride_bytes};
+    cuuint32_t box[2] = {f64 ? 16u : 32u, box_rows};
+    cuuint32_t estr[2] = {1, 1};
+    CUresult r = encode(out, f64 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT64 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2,
+                        const_cast<void*>(base), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                        CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                        CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    return r == CUDA_SUCCESS;
+}
+
+}  // namespace inft
