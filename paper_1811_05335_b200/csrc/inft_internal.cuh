@@ -74,6 +74,7 @@ struct Plan {
     int64_t nseg[2] = {1, 1};
     int64_t nseg_tot = 1;
     bool perm_identity = true;
+    int perm_shift = 0;  // c >= 0 if perm[i] = (i + c) mod N (caller order = cyclic shift of sorted), else -1
     bool fast1d = false;
     int64_t GS = 1;  // grid row stride in complex elements (1-D fast path: M_sigma + halo)
 

@@ -150,6 +150,10 @@ __global__ void k_sorted_ints(const int32_t* __restrict__ perm, const int32_t* _
     if (i >= N) return;
     int32_t j = perm[i];
     if (j != i) atomicOr(not_identity, 1);
+    int64_t c = perm[0];
+    int64_t js = i + c;
+    if (js >= N) js -= N;
+    if (j != js) atomicOr(not_identity + 1, 1);  // not a cyclic shift
     for (int k = 0; k < d; k++) {
         int64_t Ms = k == 0 ? Ms0 : Ms1;
         n0s[i * d + k] = (int32_t)mod64(l0[(int64_t)j * d + k], Ms);
@@ -331,6 +335,9 @@ void plan_build(Plan& p, const double* nodes_any, cudaStream_t st) {
         INFT_CUDA(cudaMemcpyAsync(hflags, dflags, sizeof(int) * 4, cudaMemcpyDeviceToHost, st));
         INFT_CUDA(cudaStreamSynchronize(st));
         p.perm_identity = hflags[1] == 0;
+        int32_t c0 = 0;
+        INFT_CUDA(cudaMemcpy(&c0, p.perm.p, sizeof(int32_t), cudaMemcpyDeviceToHost));
+        p.perm_shift = hflags[2] == 0 ? c0 : -1;
     }
     p.fast1d = (d == 1) && (p.m <= 16) && (p.Ms[0] % p.S[0] == 0) && (p.nseg[0] >= 2) && (p.P1 <= p.Ms[0]);
     // padded record stride: 16-byte aligned rows

@@ -35,7 +35,7 @@ template <typename T, int MC, int SEG>
 __global__ void __launch_bounds__(128) k_spread_tma_1d(const __grid_constant__ CUtensorMap fmap,
                                                        const int32_t* __restrict__ seg_start,
                                                        const T* __restrict__ w, int PP, C2<T>* __restrict__ grid,
-                                                       int64_t GS, int nseg, int Q, int R) {
+                                                       int64_t GS, int nseg, int Q, int R, int N, int cshift) {
     constexpr int P = 2 * MC + 1;
     constexpr int K = SEG + 2 * MC;
     constexpr int EB = 128 / (int)sizeof(C2<T>);  // complex values per 128-byte box row
@@ -63,26 +63,44 @@ __global__ void __launch_bounds__(128) k_spread_tma_1d(const __grid_constant__ C
     const int sp = s0 == 0 ? nseg - 1 : s0 - 1;
     const int a0 = __ldg(seg_start + sp), a1 = __ldg(seg_start + sp + 1);
     const int b0 = __ldg(seg_start + s0), b1 = __ldg(seg_start + s1);
-    const int nA = (a1 - a0 + kNB - 1) / kNB;
-    const int nb = nA + (b1 - b0 + kNB - 1) / kNB;
-
-    auto batch_pos = [&](int b, int& pos, int& cnt) {
-        if (b < nA) {
-            pos = a0 + b * kNB;
-            cnt = min(kNB, a1 - pos);
+    // Batches never straddle the sorted position where the caller column wraps
+    // (node order = cyclic shift cshift of the sorted order), so every f tile is
+    // one contiguous TMA box.  Range origin 1 = prologue segment sp.
+    int rs[4], re_[4], ro[4], rb[5];
+    int nr = 0;
+    const int wrap = N - cshift;
+    auto add_range = [&](int a, int b, int origin) {
+        if (a >= b) return;
+        if (cshift > 0 && a < wrap && wrap < b) {
+            rs[nr] = a; re_[nr] = wrap; ro[nr] = origin; ++nr;
+            rs[nr] = wrap; re_[nr] = b; ro[nr] = origin; ++nr;
         } else {
-            pos = b0 + (b - nA) * kNB;
-            cnt = min(kNB, b1 - pos);
+            rs[nr] = a; re_[nr] = b; ro[nr] = origin; ++nr;
         }
     };
+    add_range(a0, a1, 1);
+    add_range(b0, b1, 0);
+    rb[0] = 0;
+    for (int k = 0; k < nr; ++k) rb[k + 1] = rb[k] + (re_[k] - rs[k] + kNB - 1) / kNB;
+    const int nb = rb[nr];
+
+    auto batch_pos = [&](int b, int& pos, int& cnt, int& origin) {
+        int k = 0;
+        while (k + 1 < nr && b >= rb[k + 1]) ++k;
+        pos = rs[k] + (b - rb[k]) * kNB;
+        cnt = min(kNB, re_[k] - pos);
+        origin = ro[k];
+    };
     auto issue = [&](int b, int stage) {
-        int pos, cnt;
-        batch_pos(b, pos, cnt);
+        int pos, cnt, origin;
+        batch_pos(b, pos, cnt, origin);
         const uint32_t rbytes = (uint32_t)(cnt * PP * (int)sizeof(T));
+        int col = pos + cshift;
+        if (col >= N) col -= N;
         mbar_arrive_expect_tx(&full[stage], fstage + rbytes);
 #pragma unroll
         for (int bx = 0; bx < NBOX; ++bx)
-            tma_load_2d(fbuf + stage * fstage + bx * box_bytes, &fmap, 2 * (pos + bx * EB), blockIdx.y * rows,
+            tma_load_2d(fbuf + stage * fstage + bx * box_bytes, &fmap, 2 * (col + bx * EB), blockIdx.y * rows,
                         &full[stage]);
         bulk_g2s(rbuf + stage * rstage, w + (int64_t)pos * PP, rbytes, &full[stage]);
     };
@@ -121,14 +139,14 @@ __global__ void __launch_bounds__(128) k_spread_tma_1d(const __grid_constant__ C
     for (int b = 0; b < nb; ++b) {
         const int stage = b % kStages;
         const uint32_t parity = (uint32_t)((b / kStages) & 1);
-        int pos, cnt;
-        batch_pos(b, pos, cnt);
+        int pos, cnt, origin;
+        batch_pos(b, pos, cnt, origin);
         mbar_wait(&full[stage], parity);
         const unsigned char* fb = fbuf + stage * fstage;
-        const T* rb = reinterpret_cast<const T*>(rbuf + stage * rstage);
-        const bool pro = b < nA;
+        const T* rbp = reinterpret_cast<const T*>(rbuf + stage * rstage);
+        const bool pro = origin == 1;
         for (int q = 0; q < cnt; ++q) {
-            const T* rec = rb + q * PP;
+            const T* rec = rbp + q * PP;
             const int n0 = rec_n0(rec, P);
             const int seg = n0 / SEG;
             const int dl = n0 - seg * SEG;
@@ -174,7 +192,7 @@ template <typename T, int MC, int SEG>
 __global__ void __launch_bounds__(128) k_gather_tma_1d(const __grid_constant__ CUtensorMap gmap,
                                                        const int32_t* __restrict__ seg_start,
                                                        const T* __restrict__ w, int PP, C2<T>* __restrict__ f,
-                                                       int64_t N, int nseg, int Q, int R) {
+                                                       int64_t N, int nseg, int Q, int R, int cshift) {
     constexpr int P = 2 * MC + 1;
     constexpr int K = SEG + 2 * MC;
     constexpr int EB = 128 / (int)sizeof(C2<T>);
@@ -307,7 +325,9 @@ __global__ void __launch_bounds__(128) k_gather_tma_1d(const __grid_constant__ C
                 default:
                     break;
             }
-            if (active) __stcs(fr + pos + q, mk<T>(sx, sy));
+            int64_t j = pos + q + cshift;
+            if (j >= N) j -= N;
+            if (active) __stcs(fr + j, mk<T>(sx, sy));
         }
         __syncwarp();
         if (lane == 0) mbar_arrive(&emptyR[stage]);
@@ -457,8 +477,9 @@ __global__ void k_halo_fill(C2<T>* __restrict__ grid, int64_t GS, int64_t Ms, in
 // ===================================================================== host side
 template <typename T>
 struct Fns {
-    using SpreadTma = void (*)(const CUtensorMap, const int32_t*, const T*, int, C2<T>*, int64_t, int, int, int);
-    using GatherTma = void (*)(const CUtensorMap, const int32_t*, const T*, int, C2<T>*, int64_t, int, int, int);
+    using SpreadTma = void (*)(const CUtensorMap, const int32_t*, const T*, int, C2<T>*, int64_t, int, int, int, int,
+                               int);
+    using GatherTma = void (*)(const CUtensorMap, const int32_t*, const T*, int, C2<T>*, int64_t, int, int, int, int);
     using SpreadReg = void (*)(const int32_t*, const int32_t*, const int32_t*, const T*, int, const C2<T>*, C2<T>*,
                                int64_t, int64_t, int, int, int, int, int);
     using GatherReg = void (*)(const int32_t*, const int32_t*, const int32_t*, const T*, int, const C2<T>*, C2<T>*,
@@ -486,7 +507,7 @@ static Fns<T> fns_for(int m, int S) {
 }
 
 bool stream1d_available(const Plan& p) {
-    if (p.d != 1 || !p.fast1d || p.wt != INFT_WEIGHTS_REAL) return false;
+    if (p.d != 1 || !p.fast1d || p.wt != INFT_WEIGHTS_REAL || p.N == 0) return false;
     return p.prec == INFT_C128 ? fns_for<double>(p.m, p.S[0]).st != nullptr
                                : fns_for<float>(p.m, p.S[0]).st != nullptr;
 }
@@ -514,7 +535,7 @@ static void spread_t(Plan& p, const void* f, void* grid, int64_t R, cudaStream_t
     Fns<T> F = fns_for<T>(p.m, p.S[0]);
     const int nseg = (int)p.nseg[0];
     const int nchunks = (int)ceil_div(nseg, kQ);
-    if (p.perm_identity) {
+    if (p.perm_shift >= 0) {
         const int wpb = wpb_for(R);
         const int rows = 32 * wpb;
         CUtensorMap map;
@@ -527,7 +548,7 @@ static void spread_t(Plan& p, const void* f, void* grid, int64_t R, cudaStream_t
         INFT_CUDA(cudaFuncSetAttribute(F.st, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         dim3 grid_dim((unsigned)nchunks, (unsigned)ceil_div(R, rows));
         F.st<<<grid_dim, rows, smem, st>>>(map, p.seg_start.as<int32_t>(), p.w.as<T>(), p.PP,
-                                           static_cast<C2<T>*>(grid), p.GS, nseg, kQ, (int)R);
+                                           static_cast<C2<T>*>(grid), p.GS, nseg, kQ, (int)R, (int)p.N, p.perm_shift);
     } else {
         const int nrg = (int)ceil_div(R, 32);
         const int64_t warps = (int64_t)nchunks * nrg;
@@ -544,7 +565,7 @@ static void gather_t(Plan& p, const void* grid, void* f, int64_t R, cudaStream_t
     Fns<T> F = fns_for<T>(p.m, p.S[0]);
     const int nseg = (int)p.nseg[0];
     const int nchunks = (int)ceil_div(nseg, kQ);
-    if (p.perm_identity) {
+    if (p.perm_shift >= 0) {
         const int wpb = wpb_for(R);
         const int rows = 32 * wpb;
         // halo: grid[r][Ms + u] = grid[r][u]
@@ -563,7 +584,7 @@ static void gather_t(Plan& p, const void* grid, void* f, int64_t R, cudaStream_t
         INFT_CUDA(cudaFuncSetAttribute(F.gt, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         dim3 grid_dim((unsigned)nchunks, (unsigned)ceil_div(R, rows));
         F.gt<<<grid_dim, rows, smem, st>>>(map, p.seg_start.as<int32_t>(), p.w.as<T>(), p.PP, static_cast<C2<T>*>(f),
-                                           p.N, nseg, kQ, (int)R);
+                                           p.N, nseg, kQ, (int)R, p.perm_shift);
     } else {
         const int nrg = (int)ceil_div(R, 32);
         const int64_t warps = (int64_t)nchunks * nrg;
