@@ -161,11 +161,12 @@ def slot_live(x, Msig, m):
 
 def bins_1d(x, Msig, m, T):
     """Plan integers (SURVEY 8(a) a0): l0, n0 = l0 mod M_sigma, bin = n0 // T and
-    perm = stable sort of j by (bin, j) (reading A19)."""
+    perm = stable sort of j by (n0_j, j) (reading A19; sorting by n0 also sorts
+    by bin, and keeps increasing node sets a cyclic shift of the caller order)."""
     l0 = node_base(x, Msig, m)
     n0 = np.mod(l0, Msig)
     b = n0 // T
-    perm = np.argsort(b, kind="stable")
+    perm = np.argsort(n0, kind="stable")
     return l0, n0, b, perm
 
 

@@ -132,6 +132,11 @@ __global__ void k_bins(const double* __restrict__ x, int64_t N, int d, int64_t M
     bin[j] = (int32_t)b;
 }
 
+__global__ void k_n0_key(const int32_t* __restrict__ l0, int64_t N, int64_t Ms, int32_t* __restrict__ key) {
+    int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (j < N) key[j] = (int32_t)mod64(l0[j], Ms);
+}
+
 __global__ void k_iota(int32_t* a, int64_t n) {
     int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (i < n) a[i] = (int32_t)i;
@@ -303,14 +308,27 @@ void plan_build(Plan& p, const double* nodes_any, cudaStream_t st) {
         k_iota<<<grid1d(p.N), 256, 0, st>>>(idx_in.as<int32_t>(), p.N);
         INFT_CHECK_LAUNCH();
         p.launches++;
+        // 1-D key: n0 (sorting by n0 also sorts by bin; increasing node sets stay a
+        // cyclic shift of the caller order).  2-D key: the tile bin.
+        DevBuf keys_in;
+        const int32_t* kin = p.bin.as<int32_t>();
+        int64_t kmax = p.nseg_tot;
+        if (d == 1) {
+            keys_in.alloc(sizeof(int32_t) * p.N);
+            k_n0_key<<<grid1d(p.N), 256, 0, st>>>(p.l0.as<int32_t>(), p.N, p.Ms[0], keys_in.as<int32_t>());
+            INFT_CHECK_LAUNCH();
+            p.launches++;
+            kin = keys_in.as<int32_t>();
+            kmax = p.Ms[0];
+        }
         int end_bit = 1;
-        while ((int64_t(1) << end_bit) < p.nseg_tot + 1) end_bit++;
+        while ((int64_t(1) << end_bit) < kmax + 1) end_bit++;
         size_t tmp_bytes = 0;
-        INFT_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, p.bin.as<int32_t>(), keys_out.as<int32_t>(),
+        INFT_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, kin, keys_out.as<int32_t>(),
                                                   idx_in.as<int32_t>(), p.perm.as<int32_t>(), (int)p.N, 0,
                                                   end_bit, st));
         tmp.alloc(tmp_bytes);
-        INFT_CUDA(cub::DeviceRadixSort::SortPairs(tmp.p, tmp_bytes, p.bin.as<int32_t>(), keys_out.as<int32_t>(),
+        INFT_CUDA(cub::DeviceRadixSort::SortPairs(tmp.p, tmp_bytes, kin, keys_out.as<int32_t>(),
                                                   idx_in.as<int32_t>(), p.perm.as<int32_t>(), (int)p.N, 0,
                                                   end_bit, st));
         // segment starts = exclusive scan of the bin histogram

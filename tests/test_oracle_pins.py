@@ -110,11 +110,15 @@ def test_jittered_column_sizes():
 def test_bins_stable_permutation():
     x = S.iid_sorted(200, 9)[::-1].copy()
     l0, n0, b, perm = O.bins_1d(x, 64, 3, 16)
-    assert np.all(np.diff(b[perm]) >= 0)
-    for v in np.unique(b):  # stable: ties keep original order
-        idx = perm[b[perm] == v]
+    assert np.all(np.diff(n0[perm]) >= 0) and np.all(np.diff(b[perm]) >= 0)
+    for v in np.unique(n0):  # stable: ties keep original order
+        idx = perm[n0[perm] == v]
         assert np.all(np.diff(idx) > 0)
     assert np.all(n0 == np.mod(l0, 64))
+    # increasing nodes -> the sorted order is a cyclic shift of the caller order
+    xs = S.jittered(512, 4)
+    _, _, _, pj = O.bins_1d(xs, 512, 8, 16)
+    assert np.all(pj == (np.arange(512) + pj[0]) % 512)
 
 
 def test_node_generators_golden():
