@@ -18,6 +18,7 @@
 // The register-window kernels without staging remain for non-identity node
 // permutations (per-lane gathers of f through perm).
 #include <algorithm>
+#include <cstdlib>
 
 #include "common.cuh"
 #include "inft_internal.cuh"
@@ -35,11 +36,14 @@ template <typename T, int MC, int SEG>
 __global__ void __launch_bounds__(128) k_spread_tma_1d(const __grid_constant__ CUtensorMap fmap,
                                                        const int32_t* __restrict__ seg_start,
                                                        const T* __restrict__ w, int PP, C2<T>* __restrict__ grid,
-                                                       int64_t GS, int nseg, int Q, int R, int N, int cshift) {
+                                                       int64_t GS, int nseg, int Q, int R, int N, int cshift,
+                                                       int dbg) {
     constexpr int P = 2 * MC + 1;
     constexpr int K = SEG + 2 * MC;
     constexpr int EB = 128 / (int)sizeof(C2<T>);  // complex values per 128-byte box row
-    constexpr int NBOX = kNB / EB;
+    constexpr int CE = (int)sizeof(C2<T>) / 8;     // 8-byte tensor-map elements per complex value
+    constexpr int NB = sizeof(T) == 8 ? 16 : 32;  // nodes per staged batch: two 128-byte f boxes
+    constexpr int NBOX = NB / EB;
     static_assert(SEG >= 2 * MC && SEG <= 32, "segment must cover the support");
     const int WPB = blockDim.x >> 5;
     const int rows = blockDim.x;
@@ -52,7 +56,7 @@ __global__ void __launch_bounds__(128) k_spread_tma_1d(const __grid_constant__ C
     unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     const uint32_t box_bytes = (uint32_t)rows * 128u;
     const uint32_t fstage = NBOX * box_bytes;
-    const uint32_t rstage = (uint32_t)((kNB * PP * (int)sizeof(T) + 127) & ~127);
+    const uint32_t rstage = (uint32_t)((NB * PP * (int)sizeof(T) + 127) & ~127);
     unsigned char* fbuf = smem;
     unsigned char* rbuf = smem + kStages * fstage;
     uint64_t* full = reinterpret_cast<uint64_t*>(rbuf + kStages * rstage);
@@ -65,31 +69,30 @@ __global__ void __launch_bounds__(128) k_spread_tma_1d(const __grid_constant__ C
     const int b0 = __ldg(seg_start + s0), b1 = __ldg(seg_start + s1);
     // Batches never straddle the sorted position where the caller column wraps
     // (node order = cyclic shift cshift of the sorted order), so every f tile is
-    // one contiguous TMA box.  Range origin 1 = prologue segment sp.
-    int rs[4], re_[4], ro[4], rb[5];
-    int nr = 0;
+    // one contiguous TMA box.  Sub-ranges (scalars, no local arrays):
+    //   prologue [a0, aw) [aw, a1)  then  main [b0, bw) [bw, b1),
+    // aw / bw = the wrap position if it lies strictly inside, else the range end.
     const int wrap = N - cshift;
-    auto add_range = [&](int a, int b, int origin) {
-        if (a >= b) return;
-        if (cshift > 0 && a < wrap && wrap < b) {
-            rs[nr] = a; re_[nr] = wrap; ro[nr] = origin; ++nr;
-            rs[nr] = wrap; re_[nr] = b; ro[nr] = origin; ++nr;
-        } else {
-            rs[nr] = a; re_[nr] = b; ro[nr] = origin; ++nr;
-        }
-    };
-    add_range(a0, a1, 1);
-    add_range(b0, b1, 0);
-    rb[0] = 0;
-    for (int k = 0; k < nr; ++k) rb[k + 1] = rb[k] + (re_[k] - rs[k] + kNB - 1) / kNB;
-    const int nb = rb[nr];
+    const int aw = (cshift > 0 && a0 < wrap && wrap < a1) ? wrap : a1;
+    const int bw = (cshift > 0 && b0 < wrap && wrap < b1) ? wrap : b1;
+    const int c1 = (aw - a0 + NB - 1) / NB;
+    const int c2 = c1 + (a1 - aw + NB - 1) / NB;
+    const int c3 = c2 + (bw - b0 + NB - 1) / NB;
+    const int nb = c3 + (b1 - bw + NB - 1) / NB;
 
     auto batch_pos = [&](int b, int& pos, int& cnt, int& origin) {
-        int k = 0;
-        while (k + 1 < nr && b >= rb[k + 1]) ++k;
-        pos = rs[k] + (b - rb[k]) * kNB;
-        cnt = min(kNB, re_[k] - pos);
-        origin = ro[k];
+        int s, e, base;
+        if (b < c1) {
+            s = a0; e = aw; base = 0; origin = 1;
+        } else if (b < c2) {
+            s = aw; e = a1; base = c1; origin = 1;
+        } else if (b < c3) {
+            s = b0; e = bw; base = c2; origin = 0;
+        } else {
+            s = bw; e = b1; base = c3; origin = 0;
+        }
+        pos = s + (b - base) * NB;
+        cnt = min(NB, e - pos);
     };
     auto issue = [&](int b, int stage) {
         int pos, cnt, origin;
@@ -97,11 +100,13 @@ __global__ void __launch_bounds__(128) k_spread_tma_1d(const __grid_constant__ C
         const uint32_t rbytes = (uint32_t)(cnt * PP * (int)sizeof(T));
         int col = pos + cshift;
         if (col >= N) col -= N;
-        mbar_arrive_expect_tx(&full[stage], fstage + rbytes);
+        mbar_arrive_expect_tx(&full[stage], ((dbg & 8) ? 0u : fstage) + rbytes);
+        if (!(dbg & 8)) {
 #pragma unroll
-        for (int bx = 0; bx < NBOX; ++bx)
-            tma_load_2d(fbuf + stage * fstage + bx * box_bytes, &fmap, 2 * (col + bx * EB), blockIdx.y * rows,
-                        &full[stage]);
+            for (int bx = 0; bx < NBOX; ++bx)
+                tma_load_2d(fbuf + stage * fstage + bx * box_bytes, &fmap, (col + bx * EB) * CE, blockIdx.y * rows,
+                            &full[stage]);
+        }
         bulk_g2s(rbuf + stage * rstage, w + (int64_t)pos * PP, rbytes, &full[stage]);
     };
 
@@ -123,7 +128,7 @@ __global__ void __launch_bounds__(128) k_spread_tma_1d(const __grid_constant__ C
     int cur_k = 0;  // 0 = prologue segment sp, k >= 1 = main segment s0 + k - 1
     C2<T>* __restrict__ gr = grid + (int64_t)(active ? r : 0) * GS;
     auto flush = [&]() {
-        if (cur_k >= 1 && active) {
+        if (cur_k >= 1 && active && !(dbg & 2)) {
             C2<T>* out = gr + (int64_t)(s0 + cur_k - 1) * SEG;
 #pragma unroll
             for (int u = 0; u < SEG; ++u) __stcs(out + u, mk<T>(ax[u], ay[u]));
@@ -153,14 +158,16 @@ __global__ void __launch_bounds__(128) k_spread_tma_1d(const __grid_constant__ C
             const int kq = pro ? 0 : seg - s0 + 1;
             while (cur_k < kq) flush();
             const int bx = q / EB, c = q % EB;
-            C2<T> fv;
-            if (sizeof(C2<T>) == 16)
-                fv = *reinterpret_cast<const C2<T>*>(fb + bx * box_bytes + swz128(row, c));
-            else
-                fv = *reinterpret_cast<const C2<T>*>(fb + bx * box_bytes + swz128(row, c >> 1) + (c & 1) * 8);
+            C2<T> fv = mk<T>(T(0), T(0));
+            if (!(dbg & 4)) {
+                if (sizeof(C2<T>) == 16)
+                    fv = *reinterpret_cast<const C2<T>*>(fb + bx * box_bytes + swz128(row, c));
+                else
+                    fv = *reinterpret_cast<const C2<T>*>(fb + bx * box_bytes + swz128(row, c >> 1) + (c & 1) * 8);
+            }
             T wv[P];
             WeightLoader<T, P>::load_smem(rec, wv);
-            switch (dl) {
+            switch ((dbg & 1) ? 99 : dl) {
 #define INFT_SPREAD_CASE(D)                                       \
     case D:                                                       \
         if constexpr (D < SEG) {                                  \
@@ -196,6 +203,7 @@ __global__ void __launch_bounds__(128) k_gather_tma_1d(const __grid_constant__ C
     constexpr int P = 2 * MC + 1;
     constexpr int K = SEG + 2 * MC;
     constexpr int EB = 128 / (int)sizeof(C2<T>);
+    constexpr int CE = (int)sizeof(C2<T>) / 8;
     constexpr int NWB = (SEG + EB - 1) / EB;  // boxes per window load
     const int WPB = blockDim.x >> 5;
     const int rows = blockDim.x;
@@ -227,7 +235,7 @@ __global__ void __launch_bounds__(128) k_gather_tma_1d(const __grid_constant__ C
         const int col = (s0 - 1 + L) * SEG + 2 * MC;
 #pragma unroll
         for (int bx = 0; bx < NWB; ++bx)
-            tma_load_2d(wbuf + stage * wstage + bx * box_bytes, &gmap, 2 * (col + bx * EB), blockIdx.y * rows,
+            tma_load_2d(wbuf + stage * wstage + bx * box_bytes, &gmap, (col + bx * EB) * CE, blockIdx.y * rows,
                         &fullW[stage]);
     };
     auto issueR = [&](int b, int stage) {
@@ -478,7 +486,7 @@ __global__ void k_halo_fill(C2<T>* __restrict__ grid, int64_t GS, int64_t Ms, in
 template <typename T>
 struct Fns {
     using SpreadTma = void (*)(const CUtensorMap, const int32_t*, const T*, int, C2<T>*, int64_t, int, int, int, int,
-                               int);
+                               int, int);
     using GatherTma = void (*)(const CUtensorMap, const int32_t*, const T*, int, C2<T>*, int64_t, int, int, int, int);
     using SpreadReg = void (*)(const int32_t*, const int32_t*, const int32_t*, const T*, int, const C2<T>*, C2<T>*,
                                int64_t, int64_t, int, int, int, int, int);
@@ -506,6 +514,15 @@ static Fns<T> fns_for(int m, int S) {
     return F;
 }
 
+static int debug_flags() {
+    static int v = -1;
+    if (v < 0) {
+        const char* e = getenv("INFT_DEBUG_SPREAD");
+        v = e ? atoi(e) : 0;
+    }
+    return v;
+}
+
 bool stream1d_available(const Plan& p) {
     if (p.d != 1 || !p.fast1d || p.wt != INFT_WEIGHTS_REAL || p.N == 0) return false;
     return p.prec == INFT_C128 ? fns_for<double>(p.m, p.S[0]).st != nullptr
@@ -517,8 +534,9 @@ static int wpb_for(int64_t R) { return (int)std::min<int64_t>(4, std::max<int64_
 template <typename T>
 static size_t spread_smem(int rows, int PP) {
     const int EB = 128 / (int)sizeof(C2<T>);
-    size_t fst = (size_t)(kNB / EB) * rows * 128;
-    size_t rst = (size_t)((kNB * PP * (int)sizeof(T) + 127) & ~127);
+    const int NB = sizeof(T) == 8 ? 16 : 32;
+    size_t fst = (size_t)(NB / EB) * rows * 128;
+    size_t rst = (size_t)((NB * PP * (int)sizeof(T) + 127) & ~127);
     return 1024 + kStages * (fst + rst) + 2 * kStages * sizeof(uint64_t);
 }
 
@@ -535,11 +553,13 @@ static void spread_t(Plan& p, const void* f, void* grid, int64_t R, cudaStream_t
     Fns<T> F = fns_for<T>(p.m, p.S[0]);
     const int nseg = (int)p.nseg[0];
     const int nchunks = (int)ceil_div(nseg, kQ);
-    if (p.perm_shift >= 0) {
+    // KNOWN ISSUE: the staged spread faults (illegal instruction at the f-tile TMA)
+    // for complex64; complex64 spreads use the register-window kernel meanwhile.
+    if (p.perm_shift >= 0 && sizeof(T) == 8) {
         const int wpb = wpb_for(R);
         const int rows = 32 * wpb;
         CUtensorMap map;
-        if (!make_tmap_2d(&map, f, sizeof(T) == 8, 2 * (uint64_t)p.N, (uint64_t)R, 2 * sizeof(T) * (uint64_t)p.N,
+        if (!make_tmap_2d(&map, f, (uint64_t)p.N * sizeof(C2<T>) / 8, (uint64_t)R, sizeof(C2<T>) * (uint64_t)p.N,
                           (uint32_t)rows)) {
             set_error("cuTensorMapEncodeTiled failed (spread f tile)");
             throw Fail{INFT_ERR_CUDA};
@@ -548,7 +568,8 @@ static void spread_t(Plan& p, const void* f, void* grid, int64_t R, cudaStream_t
         INFT_CUDA(cudaFuncSetAttribute(F.st, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         dim3 grid_dim((unsigned)nchunks, (unsigned)ceil_div(R, rows));
         F.st<<<grid_dim, rows, smem, st>>>(map, p.seg_start.as<int32_t>(), p.w.as<T>(), p.PP,
-                                           static_cast<C2<T>*>(grid), p.GS, nseg, kQ, (int)R, (int)p.N, p.perm_shift);
+                                           static_cast<C2<T>*>(grid), p.GS, nseg, kQ, (int)R, (int)p.N, p.perm_shift,
+                                           debug_flags());
     } else {
         const int nrg = (int)ceil_div(R, 32);
         const int64_t warps = (int64_t)nchunks * nrg;
@@ -575,7 +596,7 @@ static void gather_t(Plan& p, const void* grid, void* f, int64_t R, cudaStream_t
         INFT_CHECK_LAUNCH();
         p.launches++;
         CUtensorMap map;
-        if (!make_tmap_2d(&map, grid, sizeof(T) == 8, 2 * (uint64_t)p.GS, (uint64_t)R, 2 * sizeof(T) * (uint64_t)p.GS,
+        if (!make_tmap_2d(&map, grid, (uint64_t)p.GS * sizeof(C2<T>) / 8, (uint64_t)R, sizeof(C2<T>) * (uint64_t)p.GS,
                           (uint32_t)rows)) {
             set_error("cuTensorMapEncodeTiled failed (gather grid window)");
             throw Fail{INFT_ERR_CUDA};
@@ -612,8 +633,8 @@ void gather_stream1d(Plan& p, const void* grid, void* f, int64_t R, cudaStream_t
 }
 
 // ------------------------------------------------------------------ tensor maps
-bool make_tmap_2d(CUtensorMap* out, const void* base, bool f64, uint64_t inner, uint64_t rows,
-                  uint64_t row_stride_bytes, uint32_t box_rows) {
+bool make_tmap_2d(CUtensorMap* out, const void* base, uint64_t inner, uint64_t rows, uint64_t row_stride_bytes,
+                  uint32_t box_rows) {
     static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
     if (!encode) {
         void* fn = nullptr;
@@ -625,9 +646,9 @@ bool make_tmap_2d(CUtensorMap* out, const void* base, bool f64, uint64_t inner, 
     }
     cuuint64_t dims[2] = {inner, rows};
     cuuint64_t strides[1] = {row_stride_bytes};
-    cuuint32_t box[2] = {f64 ? 16u : 32u, box_rows};
+    cuuint32_t box[2] = {16u, box_rows};  // 16 x 8 bytes = one 128-byte swizzle row
     cuuint32_t estr[2] = {1, 1};
-    CUresult r = encode(out, f64 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT64 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2,
+    CUresult r = encode(out, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2,
                         const_cast<void*>(base), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
                         CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                         CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);

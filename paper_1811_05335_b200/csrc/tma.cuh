@@ -75,9 +75,10 @@ __device__ __forceinline__ void prefetch_tmap(const CUtensorMap* map) {
 // whose rows are 128 bytes (the 16-B chunk index is XOR-ed with row % 8).
 __device__ __forceinline__ uint32_t swz128(int row, int c) { return (uint32_t)row * 128u + (uint32_t)((c ^ (row & 7)) << 4); }
 
-// Host: 2-D tensor map over a row-major [rows][inner] array of float64/float32
-// scalars with a 128-byte-wide box (SWIZZLE_128B), OOB elements read as zero.
-bool make_tmap_2d(CUtensorMap* out, const void* base, bool f64, uint64_t inner, uint64_t rows,
-                  uint64_t row_stride_bytes, uint32_t box_rows);
+// Host: 2-D tensor map over a row-major [rows][inner] array of 8-byte elements
+// (complex128 = 2 elements, complex64 = 1) with a 128-byte-wide box
+// (SWIZZLE_128B); out-of-bounds elements read as zero.
+bool make_tmap_2d(CUtensorMap* out, const void* base, uint64_t inner, uint64_t rows, uint64_t row_stride_bytes,
+                  uint32_t box_rows);
 
 }  // namespace inft
