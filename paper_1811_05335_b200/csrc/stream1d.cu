@@ -52,8 +52,9 @@ __global__ void __launch_bounds__(128) k_spread_tma_1d(const __grid_constant__ C
     const int r = blockIdx.y * rows + row;
     const bool active = r < R;
 
-    extern __shared__ unsigned char smem_raw[];
-    unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    // dynamic shared memory (no static smem in this kernel): base is 1024-aligned,
+    // and indexing the __shared__ array keeps every access in the shared window (LDS)
+    extern __shared__ __align__(1024) unsigned char smem[];
     const uint32_t box_bytes = (uint32_t)rows * 128u;
     const uint32_t fstage = NBOX * box_bytes;
     const uint32_t rstage = (uint32_t)((NB * PP * (int)sizeof(T) + 127) & ~127);
@@ -122,6 +123,8 @@ __global__ void __launch_bounds__(128) k_spread_tma_1d(const __grid_constant__ C
     if (threadIdx.x == 0)
         for (int b = 0; b < min(kStages, nb); ++b) issue(b, b);
 
+    const uint32_t rowoff = (uint32_t)row * 128u;  // this lane's row in a 128-byte-swizzled box
+    const int rx = row & 7;
     T ax[K], ay[K];
 #pragma unroll
     for (int u = 0; u < K; ++u) ax[u] = ay[u] = T(0);
@@ -152,18 +155,19 @@ __global__ void __launch_bounds__(128) k_spread_tma_1d(const __grid_constant__ C
         const bool pro = origin == 1;
         for (int q = 0; q < cnt; ++q) {
             const T* rec = rbp + q * PP;
-            const int n0 = rec_n0(rec, P);
-            const int seg = n0 / SEG;
-            const int dl = n0 - seg * SEG;
+            const unsigned n0 = (unsigned)rec_n0(rec, P);
+            const int seg = (int)(n0 / SEG);
+            const int dl = (int)(n0 % SEG);
             const int kq = pro ? 0 : seg - s0 + 1;
             while (cur_k < kq) flush();
             const int bx = q / EB, c = q % EB;
             C2<T> fv = mk<T>(T(0), T(0));
             if (!(dbg & 4)) {
                 if (sizeof(C2<T>) == 16)
-                    fv = *reinterpret_cast<const C2<T>*>(fb + bx * box_bytes + swz128(row, c));
+                    fv = *reinterpret_cast<const C2<T>*>(fb + bx * box_bytes + rowoff + ((c ^ rx) << 4));
                 else
-                    fv = *reinterpret_cast<const C2<T>*>(fb + bx * box_bytes + swz128(row, c >> 1) + (c & 1) * 8);
+                    fv = *reinterpret_cast<const C2<T>*>(fb + bx * box_bytes + rowoff + (((c >> 1) ^ rx) << 4) +
+                                                         (c & 1) * 8);
             }
             T wv[P];
             WeightLoader<T, P>::load_smem(rec, wv);
@@ -212,8 +216,9 @@ __global__ void __launch_bounds__(128) k_gather_tma_1d(const __grid_constant__ C
     const int r = blockIdx.y * rows + row;
     const bool active = r < R;
 
-    extern __shared__ unsigned char smem_raw[];
-    unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    // dynamic shared memory (no static smem in this kernel): base is 1024-aligned,
+    // and indexing the __shared__ array keeps every access in the shared window (LDS)
+    extern __shared__ __align__(1024) unsigned char smem[];
     const uint32_t box_bytes = (uint32_t)rows * 128u;
     const uint32_t wstage = NWB * box_bytes;
     const uint32_t rstage = (uint32_t)((kNB * PP * (int)sizeof(T) + 127) & ~127);
@@ -262,6 +267,8 @@ __global__ void __launch_bounds__(128) k_gather_tma_1d(const __grid_constant__ C
         for (int b = 0; b < min(kStages, nbat); ++b) issueR(b, b);
     }
 
+    const uint32_t rowoff = (uint32_t)row * 128u;
+    const int rx = row & 7;
     T wx[K], wy[K];
     int nextL = 0;
     // load box nextL into window registers [2m, K)
@@ -276,9 +283,9 @@ __global__ void __launch_bounds__(128) k_gather_tma_1d(const __grid_constant__ C
             const int bx = v / EB, c = v % EB;
             C2<T> g;
             if (sizeof(C2<T>) == 16)
-                g = *reinterpret_cast<const C2<T>*>(wb + bx * box_bytes + swz128(row, c));
+                g = *reinterpret_cast<const C2<T>*>(wb + bx * box_bytes + rowoff + ((c ^ rx) << 4));
             else
-                g = *reinterpret_cast<const C2<T>*>(wb + bx * box_bytes + swz128(row, c >> 1) + (c & 1) * 8);
+                g = *reinterpret_cast<const C2<T>*>(wb + bx * box_bytes + rowoff + (((c >> 1) ^ rx) << 4) + (c & 1) * 8);
             wx[2 * MC + v] = g.x;
             wy[2 * MC + v] = g.y;
         }
@@ -311,9 +318,9 @@ __global__ void __launch_bounds__(128) k_gather_tma_1d(const __grid_constant__ C
         const T* rb = reinterpret_cast<const T*>(rbuf + stage * rstage);
         for (int q = 0; q < cnt; ++q) {
             const T* rec = rb + q * PP;
-            const int n0 = rec_n0(rec, P);
-            const int seg = n0 / SEG;
-            const int dl = n0 - seg * SEG;
+            const unsigned n0 = (unsigned)rec_n0(rec, P);
+            const int seg = (int)(n0 / SEG);
+            const int dl = (int)(n0 % SEG);
             while (cur_j < seg - s0) advance();
             T wv[P];
             WeightLoader<T, P>::load_smem(rec, wv);
