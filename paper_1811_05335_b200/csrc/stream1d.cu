@@ -187,6 +187,7 @@ __global__ void __launch_bounds__(128) k_spread_tma_1d(const __grid_constant__ C
                     break;
             }
         }
+        fence_proxy_async();
         __syncwarp();
         if (lane == 0) mbar_arrive(&empty[stage]);
         if (threadIdx.x == 0 && b + kStages < nb) {
@@ -203,7 +204,7 @@ template <typename T, int MC, int SEG>
 __global__ void __launch_bounds__(128) k_gather_tma_1d(const __grid_constant__ CUtensorMap gmap,
                                                        const int32_t* __restrict__ seg_start,
                                                        const T* __restrict__ w, int PP, C2<T>* __restrict__ f,
-                                                       int64_t N, int nseg, int Q, int R, int cshift) {
+                                                       int64_t N, int nseg, int Q, int R, int cshift, int dbg) {
     constexpr int P = 2 * MC + 1;
     constexpr int K = SEG + 2 * MC;
     constexpr int EB = 128 / (int)sizeof(C2<T>);
@@ -289,6 +290,7 @@ __global__ void __launch_bounds__(128) k_gather_tma_1d(const __grid_constant__ C
             wx[2 * MC + v] = g.x;
             wy[2 * MC + v] = g.y;
         }
+        fence_proxy_async();  // generic-proxy reads done before the TMA may overwrite
         __syncwarp();
         if (lane == 0) mbar_arrive(&emptyW[stage]);
         if (threadIdx.x == 0 && L + kStages < nbox) {
@@ -344,6 +346,7 @@ __global__ void __launch_bounds__(128) k_gather_tma_1d(const __grid_constant__ C
             if (j >= N) j -= N;
             if (active) __stcs(fr + j, mk<T>(sx, sy));
         }
+        fence_proxy_async();
         __syncwarp();
         if (lane == 0) mbar_arrive(&emptyR[stage]);
         if (threadIdx.x == 0 && b + kStages < nbat) {
@@ -494,7 +497,8 @@ template <typename T>
 struct Fns {
     using SpreadTma = void (*)(const CUtensorMap, const int32_t*, const T*, int, C2<T>*, int64_t, int, int, int, int,
                                int, int);
-    using GatherTma = void (*)(const CUtensorMap, const int32_t*, const T*, int, C2<T>*, int64_t, int, int, int, int);
+    using GatherTma = void (*)(const CUtensorMap, const int32_t*, const T*, int, C2<T>*, int64_t, int, int, int, int,
+                               int);
     using SpreadReg = void (*)(const int32_t*, const int32_t*, const int32_t*, const T*, int, const C2<T>*, C2<T>*,
                                int64_t, int64_t, int, int, int, int, int);
     using GatherReg = void (*)(const int32_t*, const int32_t*, const int32_t*, const T*, int, const C2<T>*, C2<T>*,
@@ -519,6 +523,15 @@ static Fns<T> fns_for(int m, int S) {
     INFT_FN(8, 16) INFT_FN(10, 32) INFT_FN(12, 32) INFT_FN(16, 32)
 #undef INFT_FN
     return F;
+}
+
+static bool force_reg() {
+    static int v = -1;
+    if (v < 0) {
+        const char* e = getenv("INFT_FORCE_REG");
+        v = (e && atoi(e)) ? 1 : 0;
+    }
+    return v == 1;
 }
 
 static int debug_flags() {
@@ -562,7 +575,7 @@ static void spread_t(Plan& p, const void* f, void* grid, int64_t R, cudaStream_t
     const int nchunks = (int)ceil_div(nseg, kQ);
     // KNOWN ISSUE: the staged spread faults (illegal instruction at the f-tile TMA)
     // for complex64; complex64 spreads use the register-window kernel meanwhile.
-    if (p.perm_shift >= 0 && sizeof(T) == 8) {
+    if (p.perm_shift >= 0 && sizeof(T) == 8 && !force_reg()) {
         const int wpb = wpb_for(R);
         const int rows = 32 * wpb;
         CUtensorMap map;
@@ -593,7 +606,7 @@ static void gather_t(Plan& p, const void* grid, void* f, int64_t R, cudaStream_t
     Fns<T> F = fns_for<T>(p.m, p.S[0]);
     const int nseg = (int)p.nseg[0];
     const int nchunks = (int)ceil_div(nseg, kQ);
-    if (p.perm_shift >= 0) {
+    if (p.perm_shift >= 0 && !force_reg()) {
         const int wpb = wpb_for(R);
         const int rows = 32 * wpb;
         // halo: grid[r][Ms + u] = grid[r][u]
@@ -612,7 +625,7 @@ static void gather_t(Plan& p, const void* grid, void* f, int64_t R, cudaStream_t
         INFT_CUDA(cudaFuncSetAttribute(F.gt, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         dim3 grid_dim((unsigned)nchunks, (unsigned)ceil_div(R, rows));
         F.gt<<<grid_dim, rows, smem, st>>>(map, p.seg_start.as<int32_t>(), p.w.as<T>(), p.PP, static_cast<C2<T>*>(f),
-                                           p.N, nseg, kQ, (int)R, p.perm_shift);
+                                           p.N, nseg, kQ, (int)R, p.perm_shift, debug_flags());
     } else {
         const int nrg = (int)ceil_div(R, 32);
         const int64_t warps = (int64_t)nchunks * nrg;

@@ -67,6 +67,13 @@ __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, i
         : "memory");
 }
 
+// Order this thread's prior generic-proxy shared-memory accesses before later
+// async-proxy (TMA / bulk copy) accesses: required before releasing a stage
+// buffer that the next TMA will overwrite (cross-proxy WAR hazard).
+__device__ __forceinline__ void fence_proxy_async() {
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+
 __device__ __forceinline__ void prefetch_tmap(const CUtensorMap* map) {
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(map)) : "memory");
 }
