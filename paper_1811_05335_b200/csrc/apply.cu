@@ -225,6 +225,10 @@ static unsigned gs_blocks(int64_t total, int bs) {
 
 template <typename T>
 static void spread(Plan& p, const C2<T>* f, C2<T>* grid, int64_t R, cudaStream_t st) {
+    if (ring_available(p)) {
+        spread_ring(p, f, grid, R, st);
+        return;
+    }
     if (stream1d_available(p)) {
         spread_stream1d(p, f, grid, R, st);
         return;
@@ -258,6 +262,10 @@ static void spread(Plan& p, const C2<T>* f, C2<T>* grid, int64_t R, cudaStream_t
 template <typename T>
 static void gather(Plan& p, const C2<T>* grid, C2<T>* f, int64_t R, cudaStream_t st) {
     if (p.N == 0) return;
+    if (ring_available(p)) {
+        gather_ring(p, grid, f, R, st);
+        return;
+    }
     if (stream1d_available(p)) {
         gather_stream1d(p, grid, f, R, st);
         return;

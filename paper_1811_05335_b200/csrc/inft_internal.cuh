@@ -155,6 +155,10 @@ void apply_adjoint(Plan& p, const void* h, void* f, int64_t R, cudaStream_t st);
 bool stream1d_available(const Plan& p);
 void spread_stream1d(Plan& p, const void* f, void* grid, int64_t R, cudaStream_t st);
 void gather_stream1d(Plan& p, const void* grid, void* f, int64_t R, cudaStream_t st);
+// stream1d_ring.cu
+bool ring_available(const Plan& p);
+void spread_ring(Plan& p, const void* f, void* grid, int64_t R, cudaStream_t st);
+void gather_ring(Plan& p, const void* grid, void* f, int64_t R, cudaStream_t st);
 // setup.cu
 void precompute(Plan& p, inft_method method, inft_weights wt, double tau, cudaStream_t st);
 

@@ -249,6 +249,7 @@ static inline unsigned grid1d(int64_t n, int bs = 256) { return (unsigned)ceil_d
 
 // ------------------------------------------------------------------ host logic
 static int choose_segment(int m) {
+    if (m == 4) return 8;  // SEG = 2m: register-ring kernels (stream1d_ring.cu)
     if (2 * m <= 16) return 16;
     if (2 * m <= 32) return 32;
     return (int)ceil_div(2 * m, 8) * 8;

@@ -519,7 +519,7 @@ static Fns<T> fns_for(int m, int S) {
         F.sr = k_spread_reg_1d<T, MC, SG>;               \
         F.gr = k_gather_reg_1d<T, MC, SG>;               \
     }
-    INFT_FN(1, 16) INFT_FN(2, 16) INFT_FN(3, 16) INFT_FN(4, 16) INFT_FN(5, 16) INFT_FN(6, 16) INFT_FN(7, 16)
+    INFT_FN(1, 16) INFT_FN(2, 16) INFT_FN(3, 16) INFT_FN(4, 8) INFT_FN(5, 16) INFT_FN(6, 16) INFT_FN(7, 16)
     INFT_FN(8, 16) INFT_FN(10, 32) INFT_FN(12, 32) INFT_FN(16, 32)
 #undef INFT_FN
     return F;

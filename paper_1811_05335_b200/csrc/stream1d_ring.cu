@@ -1,0 +1,558 @@
+// 1-D streaming spread (a2) / gather (a7), "ring" variant for SEG = 2m.
+//
+// Same data flow as stream1d.cu (lane = right-hand side, bin-sorted node
+// stream, warp-uniform switch on the node's slot offset), with three changes
+// that remove most non-FMA instructions:
+//  * Register ring.  With SEG = 2m the per-lane window of 2*SEG grid values
+//    is two halves that swap roles every segment, so instead of shifting
+//    registers the code is specialised on the segment parity (phase): grid
+//    position pos of the window lives in register (pos + SEG*phase) mod 2*SEG.
+//  * Stores through shared memory.  Spread: a finished segment (SEG values per
+//    RHS row) is written to a per-warp SWIZZLE_128B staging tile and stored by
+//    one 2-D TMA store; gather: the outputs of a 16-node batch likewise.
+//  * Operands (node records, f tiles / grid windows) staged by TMA / bulk copy
+//    in a 3-deep mbarrier pipeline as before; every stage release is preceded
+//    by fence.proxy.async (generic reads vs. async-proxy overwrite).
+#include <algorithm>
+#include <cstdlib>
+#include <type_traits>
+
+#include "common.cuh"
+#include "inft_internal.cuh"
+#include "tma.cuh"
+
+namespace inft {
+
+namespace ring {
+
+constexpr int kQ = 32;      // segments per chunk (one CTA)
+constexpr int kNB = 16;     // nodes per staged batch
+constexpr int kStages = 3;  // load pipeline depth
+
+#define INFT_CASES_64(X)                                                                                      \
+    X(0) X(1) X(2) X(3) X(4) X(5) X(6) X(7) X(8) X(9) X(10) X(11) X(12) X(13) X(14) X(15) X(16) X(17) X(18)   \
+    X(19) X(20) X(21) X(22) X(23) X(24) X(25) X(26) X(27) X(28) X(29) X(30) X(31) X(32) X(33) X(34) X(35)     \
+    X(36) X(37) X(38) X(39) X(40) X(41) X(42) X(43) X(44) X(45) X(46) X(47) X(48) X(49) X(50) X(51) X(52)     \
+    X(53) X(54) X(55) X(56) X(57) X(58) X(59) X(60) X(61) X(62) X(63)
+
+// byte offset of complex value v (0..) of this lane's row inside a sequence of
+// SWIZZLE_128B boxes of 32 rows (box = 32 x 128 bytes); sw = lane*128 | (lane&7)<<4
+template <typename T>
+__device__ __forceinline__ uint32_t cofs(int v, uint32_t sw) {
+    constexpr int EB = 128 / (int)sizeof(C2<T>);
+    const int bx = v / EB, c = v % EB;
+    if (sizeof(C2<T>) == 16) return (uint32_t)bx * 4096u + (sw ^ ((uint32_t)c << 4));
+    return (uint32_t)bx * 4096u + (sw ^ ((uint32_t)(c >> 1) << 4)) + (uint32_t)(c & 1) * 8u;
+}
+
+// ------------------------------------------------------------------------- spread
+template <typename T, int MC>
+__global__ void __launch_bounds__(128) k_spread_ring(const __grid_constant__ CUtensorMap fmap,
+                                                     const __grid_constant__ CUtensorMap gmap,
+                                                     const int32_t* __restrict__ seg_start,
+                                                     const T* __restrict__ w, int PP, int nseg, int Q, int N,
+                                                     int cshift) {
+    constexpr int SEG = 2 * MC;
+    constexpr int K = 2 * SEG;
+    constexpr int P = 2 * MC + 1;
+    constexpr int EB = 128 / (int)sizeof(C2<T>);
+    constexpr int CE = (int)sizeof(C2<T>) / 8;
+    constexpr int NBOX = kNB / EB;   // f boxes per batch
+    constexpr int SBOX = SEG / EB;   // store boxes per segment
+    static_assert(SEG % EB == 0 && kNB % EB == 0, "tile shapes");
+    const int WPB = blockDim.x >> 5;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint32_t sw = ((uint32_t)lane << 7) | ((uint32_t)(lane & 7) << 4);
+
+    extern __shared__ __align__(1024) unsigned char smem[];
+    const uint32_t fstage = (uint32_t)NBOX * WPB * 4096u;  // [NBOX][rows][128]
+    const uint32_t rstage = (uint32_t)((kNB * PP * (int)sizeof(T) + 127) & ~127);
+    unsigned char* fbuf = smem;
+    unsigned char* stg = smem + kStages * fstage;                 // [WPB][SBOX][32][128]
+    unsigned char* rbuf = stg + (size_t)WPB * SBOX * 4096u;
+    uint64_t* full = reinterpret_cast<uint64_t*>(rbuf + kStages * rstage);
+    uint64_t* empty = full + kStages;
+    unsigned char* my_stg = stg + (size_t)warp * SBOX * 4096u;
+
+    const int s0 = blockIdx.x * Q;
+    const int s1 = min(s0 + Q, nseg);
+    const int sp = s0 == 0 ? nseg - 1 : s0 - 1;
+    const int a0 = __ldg(seg_start + sp), a1 = __ldg(seg_start + sp + 1);
+    const int b0 = __ldg(seg_start + s0), b1 = __ldg(seg_start + s1);
+    const int wrap = N - cshift;
+    const int aw = (cshift > 0 && a0 < wrap && wrap < a1) ? wrap : a1;
+    const int bw = (cshift > 0 && b0 < wrap && wrap < b1) ? wrap : b1;
+    const int c1 = (aw - a0 + kNB - 1) / kNB;
+    const int c2 = c1 + (a1 - aw + kNB - 1) / kNB;
+    const int c3 = c2 + (bw - b0 + kNB - 1) / kNB;
+    const int nb = c3 + (b1 - bw + kNB - 1) / kNB;
+    auto batch_pos = [&](int b, int& pos, int& cnt, bool& pro) {
+        int s, e, base;
+        if (b < c1) { s = a0; e = aw; base = 0; pro = true; }
+        else if (b < c2) { s = aw; e = a1; base = c1; pro = true; }
+        else if (b < c3) { s = b0; e = bw; base = c2; pro = false; }
+        else { s = bw; e = b1; base = c3; pro = false; }
+        pos = s + (b - base) * kNB;
+        cnt = min(kNB, e - pos);
+    };
+    const int row0 = blockIdx.y * WPB * 32;
+    auto issue = [&](int b, int stage) {
+        int pos, cnt;
+        bool pro;
+        batch_pos(b, pos, cnt, pro);
+        const uint32_t rbytes = (uint32_t)(cnt * PP * (int)sizeof(T));
+        int col = pos + cshift;
+        if (col >= N) col -= N;
+        mbar_arrive_expect_tx(&full[stage], fstage + rbytes);
+#pragma unroll
+        for (int bx = 0; bx < NBOX; ++bx)
+            tma_load_2d(fbuf + stage * fstage + bx * (WPB * 4096u), &fmap, (col + bx * EB) * CE, row0, &full[stage]);
+        bulk_g2s(rbuf + stage * rstage, w + (int64_t)pos * PP, rbytes, &full[stage]);
+    };
+
+    if (threadIdx.x == 0) {
+        prefetch_tmap(&fmap);
+        prefetch_tmap(&gmap);
+        for (int i = 0; i < kStages; ++i) {
+            mbar_init(&full[i], 1);
+            mbar_init(&empty[i], WPB);
+        }
+        fence_barrier_init();
+    }
+    __syncthreads();
+    if (threadIdx.x == 0)
+        for (int b = 0; b < min(kStages, nb); ++b) issue(b, b);
+
+    T ax[K], ay[K];
+#pragma unroll
+    for (int u = 0; u < K; ++u) ax[u] = ay[u] = T(0);
+    int cur_k = 0;  // 0 = prologue segment sp, k >= 1 = main segment s0 + k - 1; phase = cur_k & 1
+    const int rstore = row0 + warp * 32;
+
+    // finish segment cur_k: store its own half (main segments only), zero it, advance.
+    // The half is selected by a branch (never a runtime register index).
+    auto store_half = [&](auto HALF) {
+        constexpr int H0 = decltype(HALF)::value * SEG;
+        if (cur_k >= 1) {
+            if (lane == 0) bulk_wait_read<0>();  // staging tile free again
+            __syncwarp();
+#pragma unroll
+            for (int u = 0; u < SEG; ++u)
+                *reinterpret_cast<C2<T>*>(my_stg + cofs<T>(u, sw)) = mk<T>(ax[H0 + u], ay[H0 + u]);
+            fence_proxy_async();
+            __syncwarp();
+            if (lane == 0) {
+                const int col = (s0 + cur_k - 1) * SEG;
+#pragma unroll
+                for (int bx = 0; bx < SBOX; ++bx) tma_store_2d(&gmap, (col + bx * EB) * CE, rstore, my_stg + bx * 4096u);
+                bulk_commit();
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < SEG; ++u) {
+            ax[H0 + u] = T(0);
+            ay[H0 + u] = T(0);
+        }
+    };
+    // (the spread keeps a shifting window: a two-phase register ring costs more
+    //  registers here than the SEG moves per segment it saves)
+    auto flush = [&]() {
+        store_half(std::integral_constant<int, 0>{});
+#pragma unroll
+        for (int u = 0; u < K; ++u) {
+            ax[u] = (u + SEG < K) ? ax[u + SEG] : T(0);
+            ay[u] = (u + SEG < K) ? ay[u + SEG] : T(0);
+        }
+        ++cur_k;
+    };
+
+    const uint32_t frow = (uint32_t)warp * 4096u;
+    for (int b = 0; b < nb; ++b) {
+        const int stage = b % kStages;
+        const uint32_t parity = (uint32_t)((b / kStages) & 1);
+        int pos, cnt;
+        bool pro;
+        batch_pos(b, pos, cnt, pro);
+        mbar_wait(&full[stage], parity);
+        const unsigned char* fb = fbuf + stage * fstage + frow;
+        const T* rb = reinterpret_cast<const T*>(rbuf + stage * rstage);
+        unsigned n0n = (unsigned)rec_n0(rb, P);
+        for (int q = 0; q < cnt; ++q) {
+            const T* rec = rb + q * PP;
+            const unsigned n0 = n0n;
+            if (q + 1 < cnt) n0n = (unsigned)rec_n0(rec + PP, P);
+            const int seg = (int)(n0 / SEG);
+            const int dl = (int)(n0 % SEG);
+            const int kq = pro ? 0 : seg - s0 + 1;
+            while (cur_k < kq) flush();
+            const C2<T> fv = *reinterpret_cast<const C2<T>*>(fb + cofs<T>(q, sw) + (uint32_t)(q / EB) * (WPB - 1) * 4096u);
+            T wv[P];
+            WeightLoader<T, P>::load_smem(rec, wv);
+            switch (dl) {
+#define INFT_RS_CASE(D)                                                    \
+    case D: {                                                              \
+        if constexpr (D < SEG) {                                           \
+            _Pragma("unroll") for (int t = 0; t < P; ++t) {                \
+                ax[D + t] = fma(wv[t], fv.x, ax[D + t]);                   \
+                ay[D + t] = fma(wv[t], fv.y, ay[D + t]);                   \
+            }                                                              \
+        }                                                                  \
+    } break;
+                INFT_CASES_32(INFT_RS_CASE)
+#undef INFT_RS_CASE
+                default:
+                    break;
+            }
+        }
+        fence_proxy_async();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[stage]);
+        if (threadIdx.x == 0 && b + kStages < nb) {
+            mbar_wait(&empty[stage], parity);
+            issue(b + kStages, stage);
+        }
+    }
+    while (cur_k <= s1 - s0) flush();
+    if (lane == 0) bulk_wait<0>();
+}
+
+// ------------------------------------------------------------------------- gather
+template <typename T, int MC>
+__global__ void __launch_bounds__(128) k_gather_ring(const __grid_constant__ CUtensorMap gmap,
+                                                     const __grid_constant__ CUtensorMap omap,
+                                                     const int32_t* __restrict__ seg_start,
+                                                     const T* __restrict__ w, int PP, C2<T>* __restrict__ f,
+                                                     int64_t Nl, int nseg, int Q, int R, int cshift) {
+    constexpr int SEG = 2 * MC;
+    constexpr int K = 2 * SEG;
+    constexpr int P = 2 * MC + 1;
+    constexpr int EB = 128 / (int)sizeof(C2<T>);
+    constexpr int CE = (int)sizeof(C2<T>) / 8;
+    constexpr int SBOX = SEG / EB;  // window boxes per segment
+    constexpr int OBOX = kNB / EB;  // output boxes per batch
+    static_assert(SEG % EB == 0 && kNB % EB == 0, "tile shapes");
+    const int N = (int)Nl;
+    const int WPB = blockDim.x >> 5;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint32_t sw = ((uint32_t)lane << 7) | ((uint32_t)(lane & 7) << 4);
+    const int row0 = blockIdx.y * WPB * 32;
+    const int r = row0 + threadIdx.x;
+    const bool active = r < R;
+
+    extern __shared__ __align__(1024) unsigned char smem[];
+    const uint32_t wstage = (uint32_t)SBOX * WPB * 4096u;
+    const uint32_t rstage = (uint32_t)((kNB * PP * (int)sizeof(T) + 127) & ~127);
+    unsigned char* wbuf = smem;
+    unsigned char* stg = smem + kStages * wstage;  // [WPB][OBOX][32][128]
+    unsigned char* rbuf = stg + (size_t)WPB * OBOX * 4096u;
+    uint64_t* fullW = reinterpret_cast<uint64_t*>(rbuf + kStages * rstage);
+    uint64_t* emptyW = fullW + kStages;
+    uint64_t* fullR = emptyW + kStages;
+    uint64_t* emptyR = fullR + kStages;
+    unsigned char* my_stg = stg + (size_t)warp * OBOX * 4096u;
+
+    const int s0 = blockIdx.x * Q;
+    const int s1 = min(s0 + Q, nseg);
+    const int nbox = s1 - s0 + 1;  // box L = grid points of segment s0 + L (halo covers L = nseg)
+    const int b0 = __ldg(seg_start + s0), b1 = __ldg(seg_start + s1);
+    const int wrap = N - cshift;
+    const int bw = (cshift > 0 && b0 < wrap && wrap < b1) ? wrap : b1;
+    const int c1 = (bw - b0 + kNB - 1) / kNB;
+    const int nbat = c1 + (b1 - bw + kNB - 1) / kNB;
+    auto batch_pos = [&](int b, int& pos, int& cnt) {
+        if (b < c1) {
+            pos = b0 + b * kNB;
+            cnt = min(kNB, bw - pos);
+        } else {
+            pos = bw + (b - c1) * kNB;
+            cnt = min(kNB, b1 - pos);
+        }
+    };
+    auto issueW = [&](int L, int stage) {
+        mbar_arrive_expect_tx(&fullW[stage], wstage);
+        const int col = (s0 + L) * SEG;
+#pragma unroll
+        for (int bx = 0; bx < SBOX; ++bx)
+            tma_load_2d(wbuf + stage * wstage + bx * (WPB * 4096u), &gmap, (col + bx * EB) * CE, row0, &fullW[stage]);
+    };
+    auto issueR = [&](int b, int stage) {
+        int pos, cnt;
+        batch_pos(b, pos, cnt);
+        const uint32_t rbytes = (uint32_t)(cnt * PP * (int)sizeof(T));
+        mbar_arrive_expect_tx(&fullR[stage], rbytes);
+        bulk_g2s(rbuf + stage * rstage, w + (int64_t)pos * PP, rbytes, &fullR[stage]);
+    };
+
+    if (threadIdx.x == 0) {
+        prefetch_tmap(&gmap);
+        prefetch_tmap(&omap);
+        for (int i = 0; i < kStages; ++i) {
+            mbar_init(&fullW[i], 1);
+            mbar_init(&emptyW[i], WPB);
+            mbar_init(&fullR[i], 1);
+            mbar_init(&emptyR[i], WPB);
+        }
+        fence_barrier_init();
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        for (int L = 0; L < min(kStages, nbox); ++L) issueW(L, L);
+        for (int b = 0; b < min(kStages, nbat); ++b) issueR(b, b);
+    }
+
+    T wx[K], wy[K];
+    int nextL = 0;
+    const uint32_t wrow = (uint32_t)warp * 4096u;
+    // box L -> registers of half (L & 1)
+    auto consume_box = [&]() {
+        const int L = nextL++;
+        const int stage = L % kStages;
+        const uint32_t parity = (uint32_t)((L / kStages) & 1);
+        mbar_wait(&fullW[stage], parity);
+        const unsigned char* wb = wbuf + stage * wstage + wrow;
+        const int half = L & 1;
+#pragma unroll
+        for (int v = 0; v < SEG; ++v) {
+            const C2<T> g = *reinterpret_cast<const C2<T>*>(wb + cofs<T>(v, sw) + (uint32_t)(v / EB) * (WPB - 1) * 4096u);
+            if (half) {
+                wx[SEG + v] = g.x;
+                wy[SEG + v] = g.y;
+            } else {
+                wx[v] = g.x;
+                wy[v] = g.y;
+            }
+        }
+        fence_proxy_async();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&emptyW[stage]);
+        if (threadIdx.x == 0 && L + kStages < nbox) {
+            mbar_wait(&emptyW[stage], parity);
+            issueW(L + kStages, stage);
+        }
+    };
+    consume_box();
+    consume_box();
+    int cur_i = 0;  // window for segment s0 + cur_i: phase cur_i & 1
+
+    C2<T>* __restrict__ fr = f + (int64_t)(active ? r : 0) * N;
+    const int rstore = row0 + warp * 32;
+    for (int b = 0; b < nbat; ++b) {
+        const int stage = b % kStages;
+        const uint32_t parity = (uint32_t)((b / kStages) & 1);
+        int pos, cnt;
+        batch_pos(b, pos, cnt);
+        mbar_wait(&fullR[stage], parity);
+        const T* rb = reinterpret_cast<const T*>(rbuf + stage * rstage);
+        const bool full_tile = cnt == kNB;
+        if (full_tile) {
+            if (lane == 0) bulk_wait_read<0>();
+            __syncwarp();
+        }
+        unsigned n0n = (unsigned)rec_n0(rb, P);
+        for (int q = 0; q < cnt; ++q) {
+            const T* rec = rb + q * PP;
+            const unsigned n0 = n0n;
+            if (q + 1 < cnt) n0n = (unsigned)rec_n0(rec + PP, P);
+            const int seg = (int)(n0 / SEG);
+            const int dl = (int)(n0 % SEG);
+            while (cur_i < seg - s0) {
+                consume_box();
+                ++cur_i;
+            }
+            T wv[P];
+            WeightLoader<T, P>::load_smem(rec, wv);
+            T sx = 0, sy = 0;
+            switch ((cur_i & 1) * 32 + dl) {
+#define INFT_RG_CASE(CID)                                                  \
+    case CID: {                                                            \
+        constexpr int PH = (CID) / 32, D = (CID) % 32;                     \
+        if constexpr (D < SEG) {                                           \
+            _Pragma("unroll") for (int t = 0; t < P; ++t) {                \
+                const int rg = (D + t + SEG * PH) % K;                     \
+                sx = fma(wv[t], wx[rg], sx);                               \
+                sy = fma(wv[t], wy[rg], sy);                               \
+            }                                                              \
+        }                                                                  \
+    } break;
+                INFT_CASES_64(INFT_RG_CASE)
+#undef INFT_RG_CASE
+                default:
+                    break;
+            }
+            if (full_tile) {
+                *reinterpret_cast<C2<T>*>(my_stg + cofs<T>(q, sw)) = mk<T>(sx, sy);
+            } else if (active) {
+                int64_t j = (int64_t)pos + q + cshift;
+                if (j >= N) j -= N;
+                fr[j] = mk<T>(sx, sy);
+            }
+        }
+        if (full_tile) {
+            fence_proxy_async();
+            __syncwarp();
+            if (lane == 0) {
+                int col = pos + cshift;
+                if (col >= N) col -= N;
+#pragma unroll
+                for (int bx = 0; bx < OBOX; ++bx) tma_store_2d(&omap, (col + bx * EB) * CE, rstore, my_stg + bx * 4096u);
+                bulk_commit();
+            }
+        }
+        fence_proxy_async();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&emptyR[stage]);
+        if (threadIdx.x == 0 && b + kStages < nbat) {
+            mbar_wait(&emptyR[stage], parity);
+            issueR(b + kStages, stage);
+        }
+    }
+    while (nextL < nbox) consume_box();  // no copy may be in flight at exit
+    if (lane == 0) bulk_wait<0>();
+}
+
+}  // namespace ring
+
+// =========================================================================== host
+template <typename T>
+struct RingFns {
+    void (*spread)(const CUtensorMap, const CUtensorMap, const int32_t*, const T*, int, int, int, int, int) = nullptr;
+    void (*gather)(const CUtensorMap, const CUtensorMap, const int32_t*, const T*, int, C2<T>*, int64_t, int, int,
+                   int, int) = nullptr;
+};
+
+template <typename T>
+static RingFns<T> ring_fns(int m) {
+    RingFns<T> F;
+    constexpr int EB = 128 / (int)sizeof(C2<T>);
+    if constexpr (8 % EB == 0) {
+        if (m == 4) {
+            F.spread = ring::k_spread_ring<T, 4>;
+            F.gather = ring::k_gather_ring<T, 4>;
+        }
+    }
+    if (m == 8) {
+        F.spread = ring::k_spread_ring<T, 8>;
+        F.gather = ring::k_gather_ring<T, 8>;
+    } else if (m == 16) {
+        F.spread = ring::k_spread_ring<T, 16>;
+        F.gather = ring::k_gather_ring<T, 16>;
+    }
+    return F;
+}
+
+static bool ring_env_disabled() {
+    static int v = -1;
+    if (v < 0) {
+        const char* e = getenv("INFT_NO_RING");
+        v = (e && atoi(e)) ? 1 : 0;
+    }
+    return v == 1;
+}
+
+bool ring_available(const Plan& p) {
+    if (ring_env_disabled() || p.d != 1 || !p.fast1d || p.wt != INFT_WEIGHTS_REAL || p.N == 0 || p.perm_shift < 0)
+        return false;
+    if (p.S[0] != 2 * p.m) return false;
+    return p.prec == INFT_C128 ? ring_fns<double>(p.m).spread != nullptr : ring_fns<float>(p.m).spread != nullptr;
+}
+
+template <typename T>
+static int ring_wpb(int64_t R) {
+    return (int)std::min<int64_t>(4, std::max<int64_t>(1, ceil_div(R, 32)));
+}
+
+template <typename T>
+static size_t ring_spread_smem(int wpb, int PP, int SEG) {
+    const int EB = 128 / (int)sizeof(C2<T>);
+    size_t f = (size_t)ring::kStages * (ring::kNB / EB) * wpb * 4096;
+    size_t st = (size_t)wpb * (SEG / EB) * 4096;
+    size_t r = (size_t)ring::kStages * ((ring::kNB * PP * (int)sizeof(T) + 127) & ~127);
+    return f + st + r + 2 * ring::kStages * sizeof(uint64_t);
+}
+
+template <typename T>
+static size_t ring_gather_smem(int wpb, int PP, int SEG) {
+    const int EB = 128 / (int)sizeof(C2<T>);
+    size_t wsz = (size_t)ring::kStages * (SEG / EB) * wpb * 4096;
+    size_t st = (size_t)wpb * (ring::kNB / EB) * 4096;
+    size_t r = (size_t)ring::kStages * ((ring::kNB * PP * (int)sizeof(T) + 127) & ~127);
+    return wsz + st + r + 4 * ring::kStages * sizeof(uint64_t);
+}
+
+static void tmap_or_throw(CUtensorMap* m, const void* base, uint64_t inner, uint64_t rows, uint64_t stride,
+                          uint32_t box_rows, const char* what) {
+    if (!make_tmap_2d(m, base, inner, rows, stride, box_rows)) {
+        set_error(std::string("cuTensorMapEncodeTiled failed: ") + what);
+        throw Fail{INFT_ERR_CUDA};
+    }
+}
+
+template <typename T>
+static void ring_spread_t(Plan& p, const void* f, void* grid, int64_t R, cudaStream_t st) {
+    RingFns<T> F = ring_fns<T>(p.m);
+    const int wpb = ring_wpb<T>(R);
+    const int nseg = (int)p.nseg[0];
+    const int nchunks = (int)ceil_div(nseg, ring::kQ);
+    const uint64_t ce = sizeof(C2<T>) / 8;
+    CUtensorMap fm, gm;
+    tmap_or_throw(&fm, f, (uint64_t)p.N * ce, (uint64_t)R, sizeof(C2<T>) * (uint64_t)p.N, 32u * wpb, "spread f");
+    tmap_or_throw(&gm, grid, (uint64_t)p.GS * ce, (uint64_t)R, sizeof(C2<T>) * (uint64_t)p.GS, 32u, "spread grid");
+    size_t smem = ring_spread_smem<T>(wpb, p.PP, p.S[0]);
+    INFT_CUDA(cudaFuncSetAttribute(F.spread, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    dim3 g((unsigned)nchunks, (unsigned)ceil_div(R, 32 * wpb));
+    F.spread<<<g, 32 * wpb, smem, st>>>(fm, gm, p.seg_start.as<int32_t>(), p.w.as<T>(), p.PP, nseg, ring::kQ,
+                                        (int)p.N, p.perm_shift);
+    INFT_CHECK_LAUNCH();
+    p.launches++;
+}
+
+template <typename T>
+__global__ void k_ring_halo(C2<T>* __restrict__ grid, int64_t GS, int64_t Ms, int H, int R) {
+    const int64_t total = (int64_t)R * H;
+    for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
+         idx += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t r = idx / H;
+        const int64_t u = idx - r * H;
+        grid[r * GS + Ms + u] = grid[r * GS + (u % Ms)];
+    }
+}
+
+template <typename T>
+static void ring_gather_t(Plan& p, const void* grid, void* f, int64_t R, cudaStream_t st) {
+    RingFns<T> F = ring_fns<T>(p.m);
+    const int wpb = ring_wpb<T>(R);
+    const int nseg = (int)p.nseg[0];
+    const int nchunks = (int)ceil_div(nseg, ring::kQ);
+    const uint64_t ce = sizeof(C2<T>) / 8;
+    const int H = (int)(p.GS - p.Ms[0]);
+    k_ring_halo<T><<<(unsigned)std::max<int64_t>(1, std::min<int64_t>(ceil_div(R * H, 256), 4096)), 256, 0, st>>>(
+        static_cast<C2<T>*>(const_cast<void*>(grid)), p.GS, p.Ms[0], H, (int)R);
+    INFT_CHECK_LAUNCH();
+    p.launches++;
+    CUtensorMap gm, om;
+    tmap_or_throw(&gm, grid, (uint64_t)p.GS * ce, (uint64_t)R, sizeof(C2<T>) * (uint64_t)p.GS, 32u * wpb, "gather grid");
+    tmap_or_throw(&om, f, (uint64_t)p.N * ce, (uint64_t)R, sizeof(C2<T>) * (uint64_t)p.N, 32u, "gather f");
+    size_t smem = ring_gather_smem<T>(wpb, p.PP, p.S[0]);
+    INFT_CUDA(cudaFuncSetAttribute(F.gather, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    dim3 g((unsigned)nchunks, (unsigned)ceil_div(R, 32 * wpb));
+    F.gather<<<g, 32 * wpb, smem, st>>>(gm, om, p.seg_start.as<int32_t>(), p.w.as<T>(), p.PP, static_cast<C2<T>*>(f),
+                                        p.N, nseg, ring::kQ, (int)R, p.perm_shift);
+    INFT_CHECK_LAUNCH();
+    p.launches++;
+}
+
+void spread_ring(Plan& p, const void* f, void* grid, int64_t R, cudaStream_t st) {
+    if (p.prec == INFT_C128)
+        ring_spread_t<double>(p, f, grid, R, st);
+    else
+        ring_spread_t<float>(p, f, grid, R, st);
+}
+
+void gather_ring(Plan& p, const void* grid, void* f, int64_t R, cudaStream_t st) {
+    if (p.prec == INFT_C128)
+        ring_gather_t<double>(p, grid, f, R, st);
+    else
+        ring_gather_t<float>(p, grid, f, R, st);
+}
+
+}  // namespace inft

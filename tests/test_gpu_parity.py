@@ -154,6 +154,14 @@ def test_cfg5_full_size_sampled_parity(P, torch, prec):
     out = plan.apply(f)
     h = torch.randn(R, M, dtype=dt, device="cuda", generator=g)
     outa = plan.adjoint_apply(h)
+    # every RHS of the batch: fast path vs the generic kernels (complex weights with
+    # zero imaginary part take the one-thread-per-output path) -- catches races in any row
+    pg = P.Plan(x, M, sigma, m, precision=prec).set_bopt(w + 0j, "alg2")
+    tol_full = 1e-13 if prec == "c128" else 1e-5
+    ga = pg.apply(f)
+    gb = pg.adjoint_apply(h)
+    assert O.rel_l2(out.cpu().numpy().astype(np.complex128), ga.cpu().numpy().astype(np.complex128)) <= tol_full
+    assert O.rel_l2(outa.cpu().numpy().astype(np.complex128), gb.cpu().numpy().astype(np.complex128)) <= tol_full
     for r in sorted(rng.choice(R, 2, replace=False)):
         fr = f[r:r + 1].cpu().numpy().astype(np.complex128)
         ref = O.apply_inverse(x, M, sigma, m, w, 1.0, fr)
