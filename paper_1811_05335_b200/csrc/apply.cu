@@ -225,7 +225,7 @@ static unsigned gs_blocks(int64_t total, int bs) {
 
 template <typename T>
 static void spread(Plan& p, const C2<T>* f, C2<T>* grid, int64_t R, cudaStream_t st) {
-    if (ring_available(p)) {
+    if (ring_spread_available(p)) {
         spread_ring(p, f, grid, R, st);
         return;
     }

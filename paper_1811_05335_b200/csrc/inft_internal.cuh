@@ -157,6 +157,7 @@ void spread_stream1d(Plan& p, const void* f, void* grid, int64_t R, cudaStream_t
 void gather_stream1d(Plan& p, const void* grid, void* f, int64_t R, cudaStream_t st);
 // stream1d_ring.cu
 bool ring_available(const Plan& p);
+bool ring_spread_available(const Plan& p);
 void spread_ring(Plan& p, const void* f, void* grid, int64_t R, cudaStream_t st);
 void gather_ring(Plan& p, const void* grid, void* f, int64_t R, cudaStream_t st);
 // setup.cu

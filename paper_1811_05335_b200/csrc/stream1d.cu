@@ -545,6 +545,7 @@ static int debug_flags() {
 
 bool stream1d_available(const Plan& p) {
     if (p.d != 1 || !p.fast1d || p.wt != INFT_WEIGHTS_REAL || p.N == 0) return false;
+
     return p.prec == INFT_C128 ? fns_for<double>(p.m, p.S[0]).st != nullptr
                                : fns_for<float>(p.m, p.S[0]).st != nullptr;
 }
