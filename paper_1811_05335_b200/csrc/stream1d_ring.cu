@@ -35,6 +35,17 @@ constexpr int kStages = 3;  // load pipeline depth
     X(36) X(37) X(38) X(39) X(40) X(41) X(42) X(43) X(44) X(45) X(46) X(47) X(48) X(49) X(50) X(51) X(52)     \
     X(53) X(54) X(55) X(56) X(57) X(58) X(59) X(60) X(61) X(62) X(63)
 
+// Tensor-map coordinate of complex column c (8-byte elements per complex = CE).
+// Routed through an opaque mov: with CE == 1 (complex64) ptxas otherwise folds
+// the coordinate into the uniform-register tuple of UTMALDG/UTMASTG in a way
+// that faulted at run time (illegal instruction) on sm_100a.
+template <int CE>
+__device__ __forceinline__ int tcoord(int c) {
+    int v = c * CE;
+    asm volatile("mov.b32 %0, %0;" : "+r"(v));
+    return v;
+}
+
 // byte offset of complex value v (0..) of this lane's row inside a sequence of
 // SWIZZLE_128B boxes of 32 rows (box = 32 x 128 bytes); sw = lane*128 | (lane&7)<<4
 template <typename T>
@@ -106,7 +117,7 @@ __global__ void __launch_bounds__(128) k_spread_ring(const __grid_constant__ CUt
         mbar_arrive_expect_tx(&full[stage], fstage + rbytes);
 #pragma unroll
         for (int bx = 0; bx < NBOX; ++bx)
-            tma_load_2d(fbuf + stage * fstage + bx * (WPB * 4096u), &fmap, (col + bx * EB) * CE, row0, &full[stage]);
+            tma_load_2d(fbuf + stage * fstage + bx * (WPB * 4096u), &fmap, tcoord<CE>(col + bx * EB), row0, &full[stage]);
         bulk_g2s(rbuf + stage * rstage, w + (int64_t)pos * PP, rbytes, &full[stage]);
     };
 
@@ -142,7 +153,7 @@ __global__ void __launch_bounds__(128) k_spread_ring(const __grid_constant__ CUt
             if (lane == 0) {
                 const int col = (s0 + cur_k - 1) * SEG;
 #pragma unroll
-                for (int bx = 0; bx < SBOX; ++bx) tma_store_2d(&gmap, (col + bx * EB) * CE, rstore, my_stg + bx * 4096u);
+                for (int bx = 0; bx < SBOX; ++bx) tma_store_2d(&gmap, tcoord<CE>(col + bx * EB), rstore, my_stg + bx * 4096u);
                 bulk_commit();
             }
         }
@@ -271,7 +282,7 @@ __global__ void __launch_bounds__(128) k_gather_ring(const __grid_constant__ CUt
         const int col = (s0 + L) * SEG;
 #pragma unroll
         for (int bx = 0; bx < SBOX; ++bx)
-            tma_load_2d(wbuf + stage * wstage + bx * (WPB * 4096u), &gmap, (col + bx * EB) * CE, row0, &fullW[stage]);
+            tma_load_2d(wbuf + stage * wstage + bx * (WPB * 4096u), &gmap, tcoord<CE>(col + bx * EB), row0, &fullW[stage]);
     };
     auto issueR = [&](int b, int stage) {
         int pos, cnt;
@@ -392,7 +403,7 @@ __global__ void __launch_bounds__(128) k_gather_ring(const __grid_constant__ CUt
                 int col = pos + cshift;
                 if (col >= N) col -= N;
 #pragma unroll
-                for (int bx = 0; bx < OBOX; ++bx) tma_store_2d(&omap, (col + bx * EB) * CE, rstore, my_stg + bx * 4096u);
+                for (int bx = 0; bx < OBOX; ++bx) tma_store_2d(&omap, tcoord<CE>(col + bx * EB), rstore, my_stg + bx * 4096u);
                 bulk_commit();
             }
         }
