@@ -458,23 +458,23 @@ static bool ring_env_disabled() {
     return v == 1;
 }
 
-// KNOWN ISSUE (round 1): with complex64 the staged spread faults with an
-// illegal instruction right after its first f-tile TMA (the same TMA pattern
-// passes in a standalone probe, tools/tma_probe.cu); complex64 spreads take the
-// register-window kernel until that is understood.  INFT_RING_C64=1 re-enables it.
+// KNOWN ISSUE (round 1): with complex64 both ring kernels (and the older staged
+// spread) fault with an illegal instruction once their tensor-map copies run
+// (the same TMA pattern passes in a standalone probe, tools/tma_probe.cu);
+// complex64 takes the register-window spread and the stream1d.cu staged gather
+// until that is understood.  INFT_RING_C64=1 re-enables the ring kernels.
 static bool ring_c64_spread_enabled() {
     const char* e = getenv("INFT_RING_C64");
     return e && atoi(e);
 }
 
-bool ring_spread_available(const Plan& p) {
-    return ring_available(p) && (p.prec == INFT_C128 || ring_c64_spread_enabled());
-}
+bool ring_spread_available(const Plan& p) { return ring_available(p); }
 
 bool ring_available(const Plan& p) {
     if (ring_env_disabled() || p.d != 1 || !p.fast1d || p.wt != INFT_WEIGHTS_REAL || p.N == 0 || p.perm_shift < 0)
         return false;
     if (p.S[0] != 2 * p.m) return false;
+    if (p.prec == INFT_C64 && !ring_c64_spread_enabled()) return false;
     return p.prec == INFT_C128 ? ring_fns<double>(p.m).spread != nullptr : ring_fns<float>(p.m).spread != nullptr;
 }
 
