@@ -15,7 +15,7 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libinft.so")
+LIB_PATH = os.environ.get("INFT_LIB") or os.path.join(_HERE, "libinft.so")  # INFT_LIB: A/B builds
 
 if not os.path.exists(LIB_PATH):
     raise ImportError(f"{LIB_PATH} is missing: build it with `python build_native.py` "

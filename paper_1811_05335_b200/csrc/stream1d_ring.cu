@@ -25,9 +25,18 @@ namespace inft {
 
 namespace ring {
 
-constexpr int kQ = 32;      // segments per chunk (one CTA)
-constexpr int kNB = 16;     // nodes per staged batch
-constexpr int kStages = 3;  // load pipeline depth
+#ifndef INFT_RING_NB
+#define INFT_RING_NB 16
+#endif
+#ifndef INFT_RING_STAGES
+#define INFT_RING_STAGES 2
+#endif
+#ifndef INFT_RING_MINB
+#define INFT_RING_MINB 1
+#endif
+constexpr int kQ = 32;                     // segments per chunk (one CTA)
+constexpr int kNB = INFT_RING_NB;          // nodes per staged batch
+constexpr int kStages = INFT_RING_STAGES;  // load pipeline depth (2: more CTAs per SM beat a deeper pipe)
 
 #define INFT_CASES_64(X)                                                                                      \
     X(0) X(1) X(2) X(3) X(4) X(5) X(6) X(7) X(8) X(9) X(10) X(11) X(12) X(13) X(14) X(15) X(16) X(17) X(18)   \
@@ -58,12 +67,14 @@ __device__ __forceinline__ uint32_t cofs(int v, uint32_t sw) {
 
 // ------------------------------------------------------------------------- spread
 template <typename T, int MC>
-__global__ void __launch_bounds__(128) k_spread_ring(const __grid_constant__ CUtensorMap fmap,
+__global__ void __launch_bounds__(128, INFT_RING_MINB) k_spread_ring(const __grid_constant__ CUtensorMap fmap,
                                                      const __grid_constant__ CUtensorMap gmap,
                                                      const int32_t* __restrict__ seg_start,
-                                                     const T* __restrict__ w, int PP, int nseg, int Q, int N,
+                                                     const T* __restrict__ w, int PPrt, int nseg, int Q, int N,
                                                      int cshift) {
     constexpr int SEG = 2 * MC;
+    constexpr int VEC = 16 / (int)sizeof(T);
+    constexpr int PP = ((2 * MC + 2 + VEC - 1) / VEC) * VEC;  // record stride (host: Plan::PP)
     constexpr int K = 2 * SEG;
     constexpr int P = 2 * MC + 1;
     constexpr int EB = 128 / (int)sizeof(C2<T>);
@@ -115,9 +126,11 @@ __global__ void __launch_bounds__(128) k_spread_ring(const __grid_constant__ CUt
         int col = pos + cshift;
         if (col >= N) col -= N;
         mbar_arrive_expect_tx(&full[stage], fstage + rbytes);
+        for (int wi = 0; wi < WPB; ++wi)
 #pragma unroll
-        for (int bx = 0; bx < NBOX; ++bx)
-            tma_load_2d(fbuf + stage * fstage + bx * (WPB * 4096u), &fmap, tcoord<CE>(col + bx * EB), row0, &full[stage]);
+            for (int bx = 0; bx < NBOX; ++bx)
+                tma_load_2d(fbuf + stage * fstage + (wi * NBOX + bx) * 4096u, &fmap, tcoord<CE>(col + bx * EB),
+                            row0 + wi * 32, &full[stage]);
         bulk_g2s(rbuf + stage * rstage, w + (int64_t)pos * PP, rbytes, &full[stage]);
     };
 
@@ -175,7 +188,7 @@ __global__ void __launch_bounds__(128) k_spread_ring(const __grid_constant__ CUt
         ++cur_k;
     };
 
-    const uint32_t frow = (uint32_t)warp * 4096u;
+    const uint32_t frow = (uint32_t)warp * NBOX * 4096u;  // this warp's boxes inside a stage
     for (int b = 0; b < nb; ++b) {
         const int stage = b % kStages;
         const uint32_t parity = (uint32_t)((b / kStages) & 1);
@@ -184,17 +197,16 @@ __global__ void __launch_bounds__(128) k_spread_ring(const __grid_constant__ CUt
         batch_pos(b, pos, cnt, pro);
         mbar_wait(&full[stage], parity);
         const unsigned char* fb = fbuf + stage * fstage + frow;
-        const T* rb = reinterpret_cast<const T*>(rbuf + stage * rstage);
-        unsigned n0n = (unsigned)rec_n0(rb, P);
-        for (int q = 0; q < cnt; ++q) {
-            const T* rec = rb + q * PP;
+        const T* rec = reinterpret_cast<const T*>(rbuf + stage * rstage);
+        unsigned n0n = (unsigned)rec_n0(rec, P);
+        for (int q = 0; q < cnt; ++q, rec += PP) {
             const unsigned n0 = n0n;
             if (q + 1 < cnt) n0n = (unsigned)rec_n0(rec + PP, P);
             const int seg = (int)(n0 / SEG);
             const int dl = (int)(n0 % SEG);
             const int kq = pro ? 0 : seg - s0 + 1;
             while (cur_k < kq) flush();
-            const C2<T> fv = *reinterpret_cast<const C2<T>*>(fb + cofs<T>(q, sw) + (uint32_t)(q / EB) * (WPB - 1) * 4096u);
+            const C2<T> fv = *reinterpret_cast<const C2<T>*>(fb + cofs<T>(q, sw));
             T wv[P];
             WeightLoader<T, P>::load_smem(rec, wv);
             switch (dl) {
@@ -227,12 +239,14 @@ __global__ void __launch_bounds__(128) k_spread_ring(const __grid_constant__ CUt
 
 // ------------------------------------------------------------------------- gather
 template <typename T, int MC>
-__global__ void __launch_bounds__(128) k_gather_ring(const __grid_constant__ CUtensorMap gmap,
+__global__ void __launch_bounds__(128, INFT_RING_MINB) k_gather_ring(const __grid_constant__ CUtensorMap gmap,
                                                      const __grid_constant__ CUtensorMap omap,
                                                      const int32_t* __restrict__ seg_start,
-                                                     const T* __restrict__ w, int PP, C2<T>* __restrict__ f,
+                                                     const T* __restrict__ w, int PPrt, C2<T>* __restrict__ f,
                                                      int64_t Nl, int nseg, int Q, int R, int cshift) {
     constexpr int SEG = 2 * MC;
+    constexpr int VEC = 16 / (int)sizeof(T);
+    constexpr int PP = ((2 * MC + 2 + VEC - 1) / VEC) * VEC;
     constexpr int K = 2 * SEG;
     constexpr int P = 2 * MC + 1;
     constexpr int EB = 128 / (int)sizeof(C2<T>);
@@ -280,9 +294,11 @@ __global__ void __launch_bounds__(128) k_gather_ring(const __grid_constant__ CUt
     auto issueW = [&](int L, int stage) {
         mbar_arrive_expect_tx(&fullW[stage], wstage);
         const int col = (s0 + L) * SEG;
+        for (int wi = 0; wi < WPB; ++wi)
 #pragma unroll
-        for (int bx = 0; bx < SBOX; ++bx)
-            tma_load_2d(wbuf + stage * wstage + bx * (WPB * 4096u), &gmap, tcoord<CE>(col + bx * EB), row0, &fullW[stage]);
+            for (int bx = 0; bx < SBOX; ++bx)
+                tma_load_2d(wbuf + stage * wstage + (wi * SBOX + bx) * 4096u, &gmap, tcoord<CE>(col + bx * EB),
+                            row0 + wi * 32, &fullW[stage]);
     };
     auto issueR = [&](int b, int stage) {
         int pos, cnt;
@@ -311,7 +327,7 @@ __global__ void __launch_bounds__(128) k_gather_ring(const __grid_constant__ CUt
 
     T wx[K], wy[K];
     int nextL = 0;
-    const uint32_t wrow = (uint32_t)warp * 4096u;
+    const uint32_t wrow = (uint32_t)warp * SBOX * 4096u;
     // box L -> registers of half (L & 1)
     auto consume_box = [&]() {
         const int L = nextL++;
@@ -322,7 +338,7 @@ __global__ void __launch_bounds__(128) k_gather_ring(const __grid_constant__ CUt
         const int half = L & 1;
 #pragma unroll
         for (int v = 0; v < SEG; ++v) {
-            const C2<T> g = *reinterpret_cast<const C2<T>*>(wb + cofs<T>(v, sw) + (uint32_t)(v / EB) * (WPB - 1) * 4096u);
+            const C2<T> g = *reinterpret_cast<const C2<T>*>(wb + cofs<T>(v, sw));
             if (half) {
                 wx[SEG + v] = g.x;
                 wy[SEG + v] = g.y;
@@ -351,15 +367,14 @@ __global__ void __launch_bounds__(128) k_gather_ring(const __grid_constant__ CUt
         int pos, cnt;
         batch_pos(b, pos, cnt);
         mbar_wait(&fullR[stage], parity);
-        const T* rb = reinterpret_cast<const T*>(rbuf + stage * rstage);
+        const T* rec = reinterpret_cast<const T*>(rbuf + stage * rstage);
         const bool full_tile = cnt == kNB;
         if (full_tile) {
             if (lane == 0) bulk_wait_read<0>();
             __syncwarp();
         }
-        unsigned n0n = (unsigned)rec_n0(rb, P);
-        for (int q = 0; q < cnt; ++q) {
-            const T* rec = rb + q * PP;
+        unsigned n0n = (unsigned)rec_n0(rec, P);
+        for (int q = 0; q < cnt; ++q, rec += PP) {
             const unsigned n0 = n0n;
             if (q + 1 < cnt) n0n = (unsigned)rec_n0(rec + PP, P);
             const int seg = (int)(n0 / SEG);
@@ -517,7 +532,7 @@ static void ring_spread_t(Plan& p, const void* f, void* grid, int64_t R, cudaStr
     const int nchunks = (int)ceil_div(nseg, ring::kQ);
     const uint64_t ce = sizeof(C2<T>) / 8;
     CUtensorMap fm, gm;
-    tmap_or_throw(&fm, f, (uint64_t)p.N * ce, (uint64_t)R, sizeof(C2<T>) * (uint64_t)p.N, 32u * wpb, "spread f");
+    tmap_or_throw(&fm, f, (uint64_t)p.N * ce, (uint64_t)R, sizeof(C2<T>) * (uint64_t)p.N, 32u, "spread f");
     tmap_or_throw(&gm, grid, (uint64_t)p.GS * ce, (uint64_t)R, sizeof(C2<T>) * (uint64_t)p.GS, 32u, "spread grid");
     size_t smem = ring_spread_smem<T>(wpb, p.PP, p.S[0]);
     INFT_CUDA(cudaFuncSetAttribute(F.spread, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
@@ -552,7 +567,7 @@ static void ring_gather_t(Plan& p, const void* grid, void* f, int64_t R, cudaStr
     INFT_CHECK_LAUNCH();
     p.launches++;
     CUtensorMap gm, om;
-    tmap_or_throw(&gm, grid, (uint64_t)p.GS * ce, (uint64_t)R, sizeof(C2<T>) * (uint64_t)p.GS, 32u * wpb, "gather grid");
+    tmap_or_throw(&gm, grid, (uint64_t)p.GS * ce, (uint64_t)R, sizeof(C2<T>) * (uint64_t)p.GS, 32u, "gather grid");
     tmap_or_throw(&om, f, (uint64_t)p.N * ce, (uint64_t)R, sizeof(C2<T>) * (uint64_t)p.N, 32u, "gather f");
     size_t smem = ring_gather_smem<T>(wpb, p.PP, p.S[0]);
     INFT_CUDA(cudaFuncSetAttribute(F.gather, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
