@@ -223,6 +223,7 @@ def main():
 
     import synth as S
     import paper_1811_05335_b200 as P
+    from paper_1811_05335_b200 import dist as D
 
     c = S.config(CFG_ID)
     x = S.make_nodes(c)
@@ -242,8 +243,11 @@ def main():
     plan.precompute("alg2")
     t_setup = time.perf_counter() - t0
     info = plan.info()
+    if ws > 1:  # every rank built its own replica of the plan: prove they agree bit for bit
+        D.check_same_bopt(plan.get_bopt(), dist, device=torch.device("cuda", dev))
+    r_start, _ = D.shard(R * ws, rank, ws)  # this rank's slice of the global batch (weak scaling)
 
-    g = torch.Generator(device=f"cuda:{dev}").manual_seed(1000 + rank)
+    g = torch.Generator(device=f"cuda:{dev}").manual_seed(1000 + r_start)
     f = torch.randn(R, N, dtype=cdt, device=f"cuda:{dev}", generator=g)
     h = torch.randn(R, M, dtype=cdt, device=f"cuda:{dev}", generator=g)
     fhat = torch.empty(R, M, dtype=cdt, device=f"cuda:{dev}")
@@ -282,10 +286,7 @@ def main():
     ms_total = ev0.elapsed_time(ev1)
     prof = plan.get_profile(reset=True)
     plan.set_profiling(False)
-    t_max = torch.tensor([ms_total], dtype=torch.float64, device=f"cuda:{dev}")
-    if ws > 1:
-        dist.all_reduce(t_max, op=dist.ReduceOp.MAX)
-    ms_total = float(t_max.item())
+    ms_total = D.max_over_ranks(ms_total, dist if ws > 1 else None, device=torch.device("cuda", dev))
     ms_step = ms_total / args.steps
     solves = 2 * R * ws * args.steps
     value = solves / (ms_total / 1e3)
