@@ -13,7 +13,7 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 HERE = os.path.join(ROOT, "paper_1811_05335_b200")
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libinft.so")
-SOURCES = ["plan.cu", "apply.cu", "stream1d.cu", "stream1d_ring.cu", "setup.cu"]
+SOURCES = ["plan.cu", "apply.cu", "stream1d.cu", "stream1d_ring.cu", "fft.cu", "setup.cu"]
 CUDA_HOME = os.environ.get("CUDA_HOME", "/usr/local/cuda")
 NVCC = os.path.join(CUDA_HOME, "bin", "nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]

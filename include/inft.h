@@ -93,6 +93,7 @@ typedef struct {
     double max_abs_w;          /* max |B_opt entry| */
     int32_t perm_identity;     /* 1 if the bin sort left the caller's node order unchanged */
     int32_t fast_path;         /* 1 if the register-window spread/gather kernels are used */
+    int32_t fused_fft;         /* 1 if the fused two-pass FFT (with deconvolution) replaces cuFFT */
     size_t workspace_bytes;    /* device bytes currently owned by the plan */
 } inft_info;
 

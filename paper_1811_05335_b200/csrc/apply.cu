@@ -355,6 +355,8 @@ struct StageTimer {
     }
 };
 
+static bool use_fused(const Plan& p) { return !p.no_fused_fft && fused_fft_available(p); }
+
 // One device-resident chunk (Rc <= grid capacity) of the inverse: a2 -> a3 -> a4.
 template <typename T>
 static void inverse_chunk(Plan& p, const void* f, void* fhat, int64_t Rc, cudaStream_t st) {
@@ -363,6 +365,11 @@ static void inverse_chunk(Plan& p, const void* f, void* fhat, int64_t Rc, cudaSt
     {
         StageTimer t(p, 0, st);
         spread<T>(p, static_cast<const C2<T>*>(f), g, Rc, st);
+    }
+    if (use_fused(p)) {  // a3 + a4 in two fused passes (fft.cu)
+        StageTimer t(p, 1, st);
+        fused_fft_inverse(p, g, fhat, Rc, st);
+        return;
     }
     {
         StageTimer t(p, 1, st);
@@ -383,6 +390,15 @@ static void adjoint_chunk(Plan& p, const void* h, void* f, int64_t Rc, cudaStrea
     ensure_grid(p, Rc);
     C2<T>* g = p.grid.as<C2<T>>();
     int64_t total = Rc * p.Mstot;
+    if (use_fused(p)) {  // a5 + a6 in two fused passes (fft.cu), grid written with its halo
+        {
+            StageTimer t(p, 4, st);
+            fused_fft_adjoint(p, h, g, Rc, st);
+        }
+        StageTimer t(p, 5, st);
+        gather<T>(p, g, static_cast<C2<T>*>(f), Rc, st);
+        return;
+    }
     {
         StageTimer t(p, 3, st);
         k_deconv_pad<T><<<gs_blocks(total, 256), 256, 0, st>>>(static_cast<const C2<T>*>(h), g, dtable<T>(p), p.M[0],

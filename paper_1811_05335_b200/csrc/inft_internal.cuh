@@ -76,6 +76,7 @@ struct Plan {
     bool perm_identity = true;
     int perm_shift = 0;  // c >= 0 if perm[i] = (i + c) mod N (caller order = cyclic shift of sorted), else -1
     bool fast1d = false;
+    bool no_fused_fft = false;  // INFT_NO_FUSED_FFT=1: cuFFT + separate deconvolution passes
     int64_t GS = 1;  // grid row stride in complex elements (1-D fast path: M_sigma + halo)
 
     // method state
@@ -160,6 +161,11 @@ bool ring_available(const Plan& p);
 bool ring_spread_available(const Plan& p);
 void spread_ring(Plan& p, const void* f, void* grid, int64_t R, cudaStream_t st);
 void gather_ring(Plan& p, const void* grid, void* f, int64_t R, cudaStream_t st);
+// fft.cu
+bool fused_fft_available(const Plan& p);
+void fused_fft_inverse(Plan& p, void* grid, void* fhat, int64_t R, cudaStream_t st);
+void fused_fft_adjoint(Plan& p, const void* h, void* grid, int64_t R, cudaStream_t st);
+void release_fft_state(const Plan* p);
 // setup.cu
 void precompute(Plan& p, inft_method method, inft_weights wt, double tau, cudaStream_t st);
 

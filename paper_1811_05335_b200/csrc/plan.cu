@@ -8,6 +8,7 @@
 #include <cub/cub.cuh>
 
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <limits>
 
@@ -75,6 +76,7 @@ void Plan::drain_profile() {
 
 Plan::~Plan() {
     DeviceGuard g(device);
+    release_fft_state(this);
     for (auto& r : recs) {
         cudaEventDestroy(r.a);
         cudaEventDestroy(r.b);
@@ -363,6 +365,10 @@ void plan_build(Plan& p, const double* nodes_any, cudaStream_t st) {
     int vec = p.prec == INFT_C128 ? 2 : 4;
     p.PP = (int)ceil_div(p.P + 1, vec) * vec;  // >= 1 padding slot (holds n0 for the streaming kernels)
     p.GS = p.fast1d ? p.Ms[0] + ceil_div(2 * p.m, 8) * 8 : p.Mstot;
+    {
+        const char* e = getenv("INFT_NO_FUSED_FFT");
+        p.no_fused_fft = e && atoi(e);
+    }
     compute_deconv(p, 1.0, st);
 }
 
@@ -688,6 +694,7 @@ inft_status inft_get_info(inft_plan_t plan, inft_info* info) {
     info->max_abs_w = p->max_abs_w;
     info->perm_identity = p->perm_identity ? 1 : 0;
     info->fast_path = p->fast1d ? 1 : 0;
+    info->fused_fft = (inft::fused_fft_available(*p) && !p->no_fused_fft) ? 1 : 0;
     info->workspace_bytes = p->workspace_bytes();
     return INFT_OK;
 }
