@@ -56,47 +56,78 @@ __device__ __forceinline__ C2<T> rot16(C2<T> a) {
     return mk<T>(fma(a.x, co, -a.y * si), fma(a.x, si, a.y * co));
 }
 
-// In-register DFT of size R (2, 4, 8, 16): a[k] <- sum_n a[n] e^{SIGN 2 pi i n k / R}.
-// Radix-2 decimation in time on a bit-reversed copy; every index and twiddle is static.
-template <int R>
-__device__ __forceinline__ constexpr int bitrev(int i) {
-    int r = 0;
-    for (int b = 1, k = R >> 1; b < R; b <<= 1, k >>= 1)
-        if (i & b) r |= k;
-    return r;
+// a * e^{SIGN 2 pi i e / 16} for an exponent e that is a constant after unrolling
+template <typename T, int SIGN>
+__device__ __forceinline__ C2<T> rot16rt(C2<T> v, int e) {
+    switch (e & 15) {
+        case 0: return v;
+        case 1: return rot16<T, SIGN, 1>(v);
+        case 2: return rot16<T, SIGN, 2>(v);
+        case 3: return rot16<T, SIGN, 3>(v);
+        case 4: return rot16<T, SIGN, 4>(v);
+        case 5: return rot16<T, SIGN, 5>(v);
+        case 6: return rot16<T, SIGN, 6>(v);
+        case 7: return rot16<T, SIGN, 7>(v);
+        case 8: return rot16<T, SIGN, 8>(v);
+        case 9: return rot16<T, SIGN, 9>(v);
+        case 10: return rot16<T, SIGN, 10>(v);
+        case 11: return rot16<T, SIGN, 11>(v);
+        case 12: return rot16<T, SIGN, 12>(v);
+        case 13: return rot16<T, SIGN, 13>(v);
+        case 14: return rot16<T, SIGN, 14>(v);
+        default: return rot16<T, SIGN, 15>(v);
+    }
 }
 
+// DFT4 in place: X_k = sum_n x_n (SIGN i)^{nk}
+template <typename T, int SIGN>
+__device__ __forceinline__ void dft4(C2<T>& x0, C2<T>& x1, C2<T>& x2, C2<T>& x3) {
+    const C2<T> u0 = cadd<T>(x0, x2), u1 = csub<T>(x0, x2), u2 = cadd<T>(x1, x3);
+    const C2<T> u3 = rot16<T, SIGN, 4>(csub<T>(x1, x3));
+    x0 = cadd<T>(u0, u2);
+    x2 = csub<T>(u0, u2);
+    x1 = cadd<T>(u1, u3);
+    x3 = csub<T>(u1, u3);
+}
+
+// In-register DFT of size R (2, 4, 8, 16): a[k] <- sum_n a[n] e^{SIGN 2 pi i n k / R}.
+// R = P*Q with n = n1 + P n2, k = Q k1 + k2:
+//   X[Q k1 + k2] = sum_{n1} w_P^{n1 k1} w_R^{n1 k2} sum_{n2} x[n1 + P n2] w_Q^{n2 k2}
+// (Q = 4 inner DFT4s, twiddles, P-point outer DFTs); every index is static.
 template <typename T, int SIGN, int R>
 __device__ __forceinline__ void dft_reg(C2<T> (&a)[R]) {
-    C2<T> b[R];
+    if constexpr (R == 2) {
+        const C2<T> t = a[0];
+        a[0] = cadd<T>(t, a[1]);
+        a[1] = csub<T>(t, a[1]);
+    } else if constexpr (R == 4) {
+        dft4<T, SIGN>(a[0], a[1], a[2], a[3]);
+    } else {
+        constexpr int P = R / 4;  // 2 or 4
+        C2<T> y[P][4];
 #pragma unroll
-    for (int i = 0; i < R; ++i) b[bitrev<R>(i)] = a[i];
+        for (int n1 = 0; n1 < P; ++n1) {
 #pragma unroll
-    for (int len = 2; len <= R; len <<= 1) {
+            for (int n2 = 0; n2 < 4; ++n2) y[n1][n2] = a[n1 + P * n2];
+            dft4<T, SIGN>(y[n1][0], y[n1][1], y[n1][2], y[n1][3]);
 #pragma unroll
-        for (int i = 0; i < R; i += len) {
+            for (int k2 = 1; k2 < 4; ++k2) y[n1][k2] = rot16rt<T, SIGN>(y[n1][k2], n1 * k2 * (16 / R));
+        }
 #pragma unroll
-            for (int k = 0; k < len / 2; ++k) {
-                // twiddle e^{SIGN 2 pi i k / len} = e^{SIGN 2 pi i (k * 16/len) / 16}
-                C2<T> v = b[i + k + len / 2];
-                switch (k * (16 / len)) {  // resolved at compile time after unrolling
-                    case 0: break;
-                    case 1: v = rot16<T, SIGN, 1>(v); break;
-                    case 2: v = rot16<T, SIGN, 2>(v); break;
-                    case 3: v = rot16<T, SIGN, 3>(v); break;
-                    case 4: v = rot16<T, SIGN, 4>(v); break;
-                    case 5: v = rot16<T, SIGN, 5>(v); break;
-                    case 6: v = rot16<T, SIGN, 6>(v); break;
-                    case 7: v = rot16<T, SIGN, 7>(v); break;
-                }
-                const C2<T> u = b[i + k];
-                b[i + k] = cadd<T>(u, v);
-                b[i + k + len / 2] = csub<T>(u, v);
+        for (int k2 = 0; k2 < 4; ++k2) {
+            if constexpr (P == 4) {
+                C2<T> z0 = y[0][k2], z1 = y[1][k2], z2 = y[2][k2], z3 = y[3][k2];
+                dft4<T, SIGN>(z0, z1, z2, z3);
+                a[k2] = z0;
+                a[4 + k2] = z1;
+                a[8 + k2] = z2;
+                a[12 + k2] = z3;
+            } else {
+                a[k2] = cadd<T>(y[0][k2], y[1][k2]);
+                a[4 + k2] = csub<T>(y[0][k2], y[1][k2]);
             }
         }
     }
-#pragma unroll
-    for (int i = 0; i < R; ++i) a[i] = b[i];
 }
 
 // padded shared-memory index: one complex of padding every 16 (breaks power-of-two strides)
@@ -188,28 +219,31 @@ __device__ __forceinline__ void run_stage(int si, int nst, int L, int TF, int Ns
     if (si < nst - 1) __syncthreads();  // writes visible to the next stage
 }
 
-template <typename T, int SIGN, typename Load, typename Store>
-__device__ __forceinline__ void cta_fft(int L, int TF, int nst, const int* rad, const C2<T>* tw, C2<T>* sm,
-                                        Load&& load, Store&& store) {
-    int Ns = 1;
-    for (int si = 0; si < nst; ++si) {
-        const int R = rad[si];
-        if (R == 16)
-            run_stage<T, SIGN, 16>(si, nst, L, TF, Ns, tw, sm, load, store);
-        else if (R == 8)
-            run_stage<T, SIGN, 8>(si, nst, L, TF, Ns, tw, sm, load, store);
-        else if (R == 4)
-            run_stage<T, SIGN, 4>(si, nst, L, TF, Ns, tw, sm, load, store);
-        else
-            run_stage<T, SIGN, 2>(si, nst, L, TF, Ns, tw, sm, load, store);
-        Ns *= R;
+// Static radix plan for L = 2^K: a first stage of radix 2^(K mod 4) (if any), then radix-16.
+template <typename T, int SIGN, int L, typename Load, typename Store>
+__device__ __forceinline__ void cta_fft(int TF, const C2<T>* tw, C2<T>* sm, Load&& load, Store&& store) {
+    constexpr int K = __builtin_ctz(L);
+    constexpr int R0 = 1 << (K % 4);
+    constexpr int N16 = K / 4;
+    constexpr int NST = N16 + (R0 > 1 ? 1 : 0);
+    int Ns = 1, si = 0;
+    if constexpr (R0 > 1) {
+        run_stage<T, SIGN, R0>(si, NST, L, TF, Ns, tw, sm, load, store);
+        Ns *= R0;
+        ++si;
+    }
+#pragma unroll 1
+    for (int s16 = 0; s16 < N16; ++s16) {
+        run_stage<T, SIGN, 16>(si, NST, L, TF, Ns, tw, sm, load, store);
+        Ns *= 16;
+        ++si;
     }
 }
 
 // ------------------------------------------------------------------ pass A (columns)
 // MODE 0: inverse, in place on the grid (x = grid[r][n]);  MODE 1: adjoint, x = d_k h_k in
 // the band (zero elsewhere), output to ybuf.
-template <typename T, int SIGN, int MODE>
+template <typename T, int SIGN, int MODE, int L>
 __global__ void __launch_bounds__(256) k_pass_a(Args<T> A, int TA) {
     extern __shared__ __align__(16) unsigned char smraw[];
     C2<T>* sm = reinterpret_cast<C2<T>*>(smraw);
@@ -246,13 +280,13 @@ __global__ void __launch_bounds__(256) k_pass_a(Args<T> A, int TA) {
         else
             yrow[o] = v;
     };
-    cta_fft<T, SIGN>(N1, TA, A.nst1, A.rad1, A.tw1, sm, load, store);
+    cta_fft<T, SIGN, L>(TA, A.tw1, sm, load, store);
 }
 
 // ------------------------------------------------------------------ pass B (rows)
 // MODE 0: inverse, input grid rows, output fhat (kept band times d_k);
 // MODE 1: adjoint, input ybuf rows, output grid (natural order) + halo.
-template <typename T, int SIGN, int MODE>
+template <typename T, int SIGN, int MODE, int L>
 __global__ void __launch_bounds__(256) k_pass_b(Args<T> A, int TB) {
     extern __shared__ __align__(16) unsigned char smraw[];
     C2<T>* sm = reinterpret_cast<C2<T>*>(smraw);
@@ -281,7 +315,7 @@ __global__ void __launch_bounds__(256) k_pass_b(Args<T> A, int TB) {
             if (k < A.H) grow[A.N + k] = v;
         }
     };
-    cta_fft<T, SIGN>(N2, TB, A.nst2, A.rad2, A.tw2, sm, load, store);
+    cta_fft<T, SIGN, L>(TB, A.tw2, sm, load, store);
 }
 
 }  // namespace fft
@@ -396,6 +430,29 @@ static int tile_for(int L, size_t cs) {
     return t;
 }
 
+template <typename T, int L>
+static void (*pick_L(int which, int mode))(fft::Args<T>, int) {
+    // mode 0 = inverse NFFT (forward sign), mode 1 = inverse adjoint (inverse sign)
+    if (which == 0) return mode == 0 ? fft::k_pass_a<T, -1, 0, L> : fft::k_pass_a<T, 1, 1, L>;
+    return mode == 0 ? fft::k_pass_b<T, -1, 0, L> : fft::k_pass_b<T, 1, 1, L>;
+}
+
+template <typename T>
+static void (*pick_kernel(int which, int mode, int L))(fft::Args<T>, int) {
+    switch (L) {
+        case 16: return pick_L<T, 16>(which, mode);
+        case 32: return pick_L<T, 32>(which, mode);
+        case 64: return pick_L<T, 64>(which, mode);
+        case 128: return pick_L<T, 128>(which, mode);
+        case 256: return pick_L<T, 256>(which, mode);
+        case 512: return pick_L<T, 512>(which, mode);
+        case 1024: return pick_L<T, 1024>(which, mode);
+        case 2048: return pick_L<T, 2048>(which, mode);
+        case 4096: return pick_L<T, 4096>(which, mode);
+    }
+    return nullptr;
+}
+
 template <typename T>
 static void launch_pass(Plan& p, fft::Args<T>& A, int which, int mode, int sign, int64_t R, cudaStream_t st) {
     const int L = which == 0 ? A.N1 : A.N2;
@@ -406,13 +463,10 @@ static void launch_pass(Plan& p, fft::Args<T>& A, int which, int mode, int sign,
     int threads = TF * (L / 16);
     threads = std::max(32, std::min(256, threads));
     dim3 g((unsigned)(other / TF), (unsigned)R);
-    void (*kern)(fft::Args<T>, int) = nullptr;
-    if (which == 0) {
-        if (mode == 0) kern = sign < 0 ? fft::k_pass_a<T, -1, 0> : fft::k_pass_a<T, 1, 0>;
-        else kern = sign < 0 ? fft::k_pass_a<T, -1, 1> : fft::k_pass_a<T, 1, 1>;
-    } else {
-        if (mode == 0) kern = sign < 0 ? fft::k_pass_b<T, -1, 0> : fft::k_pass_b<T, 1, 0>;
-        else kern = sign < 0 ? fft::k_pass_b<T, -1, 1> : fft::k_pass_b<T, 1, 1>;
+    void (*kern)(fft::Args<T>, int) = pick_kernel<T>(which, mode, L);
+    if (!kern) {
+        set_error("fused FFT: unsupported factor length");
+        throw Fail{INFT_ERR_UNSUPPORTED};
     }
     INFT_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     kern<<<g, threads, smem, st>>>(A, TF);
