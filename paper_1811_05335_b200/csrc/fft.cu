@@ -130,8 +130,9 @@ __device__ __forceinline__ void dft_reg(C2<T> (&a)[R]) {
     }
 }
 
-// padded shared-memory index: one complex of padding every 16 (breaks power-of-two strides)
-__device__ __forceinline__ int sp(int i) { return i + (i >> 4); }
+// shared-memory layout of TF transforms: [f][L + 2] (row stride = 2 mod 8 complex, so the
+// 8 lanes of a quarter warp -- 2 positions x 4 transforms -- fall on distinct banks)
+__device__ __forceinline__ int sidx(int f, int pos, int L) { return f * (L + 2) + pos; }
 
 // ------------------------------------------------------------------ kernel parameters
 template <typename T>
@@ -165,9 +166,20 @@ template <typename T, int SIGN, int R>
 __device__ __forceinline__ void stage_regs(C2<T> (&a)[R], int j, int Ns, int L, const C2<T>* __restrict__ tw) {
     if (Ns > 1) {
         const int k = j % Ns;
-        const int step = k * (L / (Ns * R));
+        // one table load, the other powers by multiplication (depth <= 4, a few ulps)
+        C2<T> w[R];
+        w[1] = twid<T, SIGN>(tw, k * (L / (Ns * R)));
 #pragma unroll
-        for (int m = 1; m < R; ++m) a[m] = cmul<T>(a[m], twid<T, SIGN>(tw, m * step));
+        for (int m = 2; m < R; ++m) {
+            if ((m & (m - 1)) == 0)
+                w[m] = cmul<T>(w[m / 2], w[m / 2]);
+            else {
+                const int hi = 1 << (31 - __clz(m));  // largest power of two below m
+                w[m] = cmul<T>(w[hi], w[m - hi]);
+            }
+        }
+#pragma unroll
+        for (int m = 1; m < R; ++m) a[m] = cmul<T>(a[m], w[m]);
     }
     dft_reg<T, SIGN, R>(a);
 }
@@ -195,7 +207,7 @@ __device__ __forceinline__ void run_stage(int si, int nst, int L, int TF, int Ns
 #pragma unroll
         for (int m = 0; m < R; ++m) {
             const int n = j + m * nbut;
-            a[p][m] = (si == 0) ? load(f, n) : sm[sp(n * TF + f)];
+            a[p][m] = (si == 0) ? load(f, n) : sm[sidx(f, n, L)];
         }
     }
     if (si > 0) __syncthreads();  // everyone has read the shared buffer
@@ -213,7 +225,7 @@ __device__ __forceinline__ void run_stage(int si, int nst, int L, int TF, int Ns
             if (si == nst - 1)
                 store(f, k, a[p][m]);
             else
-                sm[sp(k * TF + f)] = a[p][m];
+                sm[sidx(f, k, L)] = a[p][m];
         }
     }
     if (si < nst - 1) __syncthreads();  // writes visible to the next stage
@@ -459,7 +471,7 @@ static void launch_pass(Plan& p, fft::Args<T>& A, int which, int mode, int sign,
     const int other = which == 0 ? A.N2 : A.N1;
     // TF transforms per CTA: ~64 KB of shared memory, <= 256 threads (TF * L / 16)
     const int TF = std::max(1, std::min({tile_for(L, sizeof(C2<T>)), other, std::max(1, 4096 / L)}));
-    const size_t smem = sizeof(C2<T>) * (size_t)(L * TF + (L * TF) / 16 + 16);
+    const size_t smem = sizeof(C2<T>) * (size_t)((L + 2) * TF);
     int threads = TF * (L / 16);
     threads = std::max(32, std::min(256, threads));
     dim3 g((unsigned)(other / TF), (unsigned)R);
