@@ -390,7 +390,9 @@ static void adjoint_chunk(Plan& p, const void* h, void* f, int64_t Rc, cudaStrea
     ensure_grid(p, Rc);
     C2<T>* g = p.grid.as<C2<T>>();
     int64_t total = Rc * p.Mstot;
-    if (use_fused(p)) {  // a5 + a6 in two fused passes (fft.cu), grid written with its halo
+    // a5 + a6 in two fused passes (fft.cu), grid written with its halo; the TMA boxes over h
+    // need a 16-byte aligned base
+    if (use_fused(p) && (reinterpret_cast<uintptr_t>(h) & 15) == 0) {
         {
             StageTimer t(p, 4, st);
             fused_fft_adjoint(p, h, g, Rc, st);

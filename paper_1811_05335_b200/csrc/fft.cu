@@ -19,6 +19,7 @@
 
 #include "common.cuh"
 #include "inft_internal.cuh"
+#include "tma.cuh"
 
 namespace inft {
 namespace fft {
@@ -130,9 +131,6 @@ __device__ __forceinline__ void dft_reg(C2<T> (&a)[R]) {
     }
 }
 
-// shared-memory layout of TF transforms: [f][L + 2] (row stride = 2 mod 8 complex, so the
-// 8 lanes of a quarter warp -- 2 positions x 4 transforms -- fall on distinct banks)
-__device__ __forceinline__ int sidx(int f, int pos, int L) { return f * (L + 2) + pos; }
 
 // ------------------------------------------------------------------ kernel parameters
 template <typename T>
@@ -148,12 +146,18 @@ struct Args {
     const C2<T>* thi;     // [N >> LB]  e^{-2 pi i e 2^LB / N}
     int64_t N, GS, M;
     int N1, N2, LB, H;
-    int nst1, nst2;       // number of radix stages for N1 / N2
-    int rad1[8], rad2[8]; // radix per stage (first to last)
 };
 
+// table entry e of a forward-sign twiddle table, conjugated for SIGN > 0 (any state space)
 template <typename T, int SIGN>
-__device__ __forceinline__ C2<T> twid(const C2<T>* __restrict__ tab, int e) {
+__device__ __forceinline__ C2<T> twid(const C2<T>* tab, int e) {
+    C2<T> w = tab[e];
+    if (SIGN > 0) w.y = -w.y;
+    return w;
+}
+
+template <typename T, int SIGN>
+__device__ __forceinline__ C2<T> twid_g(const C2<T>* __restrict__ tab, int e) {
     C2<T> w = __ldg(tab + e);
     if (SIGN > 0) w.y = -w.y;
     return w;
@@ -162,13 +166,13 @@ __device__ __forceinline__ C2<T> twid(const C2<T>* __restrict__ tab, int e) {
 // One Stockham stage on registers: given a[m] = data[j + m L/R] (already loaded), multiply
 // by e^{SIGN 2 pi i m (j mod Ns) / (Ns R)} (table entry m (j mod Ns) L/(Ns R) of length L),
 // DFT_R; outputs a[m] belong at index (j / Ns) Ns R + (j mod Ns) + m Ns.
-template <typename T, int SIGN, int R>
-__device__ __forceinline__ void stage_regs(C2<T> (&a)[R], int j, int Ns, int L, const C2<T>* __restrict__ tw) {
-    if (Ns > 1) {
-        const int k = j % Ns;
+template <typename T, int SIGN, int R, int L, int NS>
+__device__ __forceinline__ void stage_regs(C2<T> (&a)[R], int j, const C2<T>* __restrict__ tw) {
+    if constexpr (NS > 1) {
+        const int k = j % NS;
         // one table load, the other powers by multiplication (depth <= 4, a few ulps)
         C2<T> w[R];
-        w[1] = twid<T, SIGN>(tw, k * (L / (Ns * R)));
+        w[1] = twid<T, SIGN>(tw, k * (L / (NS * R)));
 #pragma unroll
         for (int m = 2; m < R; ++m) {
             if ((m & (m - 1)) == 0)
@@ -184,167 +188,284 @@ __device__ __forceinline__ void stage_regs(C2<T> (&a)[R], int j, int Ns, int L, 
     dft_reg<T, SIGN, R>(a);
 }
 
-// ------------------------------------------------------------------ generic CTA transform
-// TF independent length-L transforms, thread t -> (f = t % TF, butterfly index b = t / TF).
-// LOAD(f, n) -> value of element n of transform f; STORE(f, k, v) writes output k.
-// sm: shared scratch of sp(L * TF) complex.  All threads of the CTA participate.
-template <typename T, int SIGN, int R, typename Load, typename Store>
-__device__ __forceinline__ void run_stage(int si, int nst, int L, int TF, int Ns, const C2<T>* tw, C2<T>* sm,
-                                          Load&& load, Store&& store) {
-    const int nbut = L / R;
-    const int total = nbut * TF;
-    // read phase (all butterflies of this thread) then write phase: each thread handles
-    // `per` butterflies; registers hold them all between the two phases.
-    constexpr int MAXPER = 16 / R;
-    C2<T> a[MAXPER][R];
-    const int per = (total + blockDim.x - 1) / blockDim.x;
+// ------------------------------------------------------------------ CTA transform geometry
+// TF independent length-L transforms per tile (compile-time: ~64 KB of shared memory, at
+// most 256 threads = TF L / 16, at most 8), thread t -> (f = t % TF, butterfly j = t / TF).
+// Static radix plan for L = 2^K: a first stage of radix 2^(K mod 4) (if any), then radix-16.
+template <typename T, int L>
+struct Geo {
+    static constexpr int TF = L >= 512 ? 4096 / L : 8;
+    static constexpr int NT = TF * L / 16 < 32 ? 32 : TF * L / 16;  // threads per CTA
+    // row padding of the [f][L + PAD] layout: the lanes of one 128-byte shared wavefront cover
+    // TF transforms x (wavefront / TF) consecutive positions
+    static constexpr int WAVE = (int)(128 / sizeof(C2<T>));
+    static constexpr int PAD = WAVE / TF > 1 ? WAVE / TF : 1;
+    static constexpr int S = L + PAD;
+    static constexpr int K = __builtin_ctz(L);
+    static constexpr int R0 = 1 << (K % 4);
+    static constexpr int RF = R0 > 1 ? R0 : 16;  // radix of the first stage
+    static constexpr int PER0 = 16 / RF;         // butterflies per thread in the first stage
+    static constexpr int NST = K / 4 + (R0 > 1 ? 1 : 0);
+};
+
+// shared-memory layout of the TF transforms: [f][S]
+template <typename G>
+__device__ __forceinline__ int sidx(int f, int pos) { return f * G::S + pos; }
+
+// One stage SI (radix R, span NS) of TF transforms.  LOAD(f, n, p, m) -> element n of
+// transform f (the first stage's butterfly p, leg m of this thread); STORE(f, k, v, m) writes
+// output k (leg m of the last stage's single butterfly of this thread, legs in increasing m).
+// sm: [TF][S] shared scratch;  tw: table e^{-2 pi i e / L}, e < L / 16 (the entries the
+// radix-16 stages use).
+template <typename T, int SIGN, typename G, int R, int NS, int SI, typename Load, typename Store>
+__device__ __forceinline__ void run_stage(const C2<T>* tw, C2<T>* sm, Load&& load, Store&& store) {
+    constexpr int L = G::S - G::PAD;
+    constexpr int TF = G::TF;
+    constexpr int nbut = L / R;
+    constexpr int total = nbut * TF;
+    constexpr int per = (total + G::NT - 1) / G::NT;
+    constexpr bool last = SI == G::NST - 1;
+    C2<T> a[per][R];
 #pragma unroll
-    for (int p = 0; p < MAXPER; ++p) {
-        if (p >= per) break;
-        const int t = threadIdx.x + p * blockDim.x;
-        if (t >= total) break;
+    for (int p = 0; p < per; ++p) {
+        const int t = threadIdx.x + p * G::NT;
+        if (total % G::NT != 0 && t >= total) break;
         const int f = t % TF, j = t / TF;
 #pragma unroll
         for (int m = 0; m < R; ++m) {
             const int n = j + m * nbut;
-            a[p][m] = (si == 0) ? load(f, n) : sm[sidx(f, n, L)];
+            if constexpr (SI == 0)
+                a[p][m] = load(f, n, p, m);
+            else
+                a[p][m] = sm[sidx<G>(f, n)];
         }
     }
-    if (si > 0) __syncthreads();  // everyone has read the shared buffer
+    if constexpr (SI > 0) __syncthreads();  // everyone has read the shared buffer
 #pragma unroll
-    for (int p = 0; p < MAXPER; ++p) {
-        if (p >= per) break;
-        const int t = threadIdx.x + p * blockDim.x;
-        if (t >= total) break;
+    for (int p = 0; p < per; ++p) {
+        const int t = threadIdx.x + p * G::NT;
+        if (total % G::NT != 0 && t >= total) break;
         const int f = t % TF, j = t / TF;
-        stage_regs<T, SIGN, R>(a[p], j, Ns, L, tw);
-        const int base = (j / Ns) * Ns * R + (j % Ns);
+        stage_regs<T, SIGN, R, L, NS>(a[p], j, tw);
+        const int base = (j / NS) * NS * R + (j % NS);
 #pragma unroll
         for (int m = 0; m < R; ++m) {
-            const int k = base + m * Ns;
-            if (si == nst - 1)
-                store(f, k, a[p][m]);
+            const int k = base + m * NS;
+            if constexpr (last)
+                store(f, k, a[p][m], m);
             else
-                sm[sidx(f, k, L)] = a[p][m];
+                sm[sidx<G>(f, k)] = a[p][m];
         }
     }
-    if (si < nst - 1) __syncthreads();  // writes visible to the next stage
+    if constexpr (!last) __syncthreads();  // writes visible to the next stage
 }
 
-// Static radix plan for L = 2^K: a first stage of radix 2^(K mod 4) (if any), then radix-16.
+template <typename T, int SIGN, typename G, int SI, int NS, typename Load, typename Store>
+__device__ __forceinline__ void fft_stages(const C2<T>* tw, C2<T>* sm, Load&& load, Store&& store) {
+    if constexpr (SI < G::NST) {
+        constexpr int R = (SI == 0) ? G::RF : 16;
+        run_stage<T, SIGN, G, R, NS, SI>(tw, sm, load, store);
+        fft_stages<T, SIGN, G, SI + 1, NS * R>(tw, sm, load, store);
+    }
+}
+
 template <typename T, int SIGN, int L, typename Load, typename Store>
-__device__ __forceinline__ void cta_fft(int TF, const C2<T>* tw, C2<T>* sm, Load&& load, Store&& store) {
-    constexpr int K = __builtin_ctz(L);
-    constexpr int R0 = 1 << (K % 4);
-    constexpr int N16 = K / 4;
-    constexpr int NST = N16 + (R0 > 1 ? 1 : 0);
-    int Ns = 1, si = 0;
-    if constexpr (R0 > 1) {
-        run_stage<T, SIGN, R0>(si, NST, L, TF, Ns, tw, sm, load, store);
-        Ns *= R0;
-        ++si;
-    }
-#pragma unroll 1
-    for (int s16 = 0; s16 < N16; ++s16) {
-        run_stage<T, SIGN, 16>(si, NST, L, TF, Ns, tw, sm, load, store);
-        Ns *= 16;
-        ++si;
-    }
+__device__ __forceinline__ void cta_fft(const C2<T>* tw, C2<T>* sm, Load&& load, Store&& store) {
+    fft_stages<T, SIGN, Geo<T, L>, 0, 1>(tw, sm, load, store);
 }
 
-// ------------------------------------------------------------------ pass A (columns)
-// MODE 0: inverse, in place on the grid (x = grid[r][n]);  MODE 1: adjoint, x = d_k h_k in
-// the band (zero elsewhere), output to ybuf.
+// ------------------------------------------------------------------ persistent tiled passes
+// Each pass is a persistent kernel (one CTA per SM) walking a list of tiles; the next tile
+// is copied into the other half of a double buffer by the Tensor Memory Accelerator (pass A:
+// 3-D tensor-map boxes of the strided columns; pass B: 1-D bulk copies of whole rows) while
+// the CTA transforms the current one, so HBM reads overlap the arithmetic.  The first
+// Stockham stage reads the landed tile, the stages in between use the work buffer, the last
+// stage applies the epilogue and writes global memory from registers.
+//
+// Shared memory: tile[2] | work | mbarrier[2].
+//
+// Pass A (columns, length L = N1, TF = TA columns per tile, tile layout [n1][TA]):
+//   MODE 0 (inverse): x = grid[r][N2 n1 + n2], output in place (twiddled);
+//   MODE 1 (adjoint): x = d_c h[r][c] on the band rows (the TMA boxes fetch only those rows,
+//                     the other rows are zero and never read), output to ybuf.
 template <typename T, int SIGN, int MODE, int L>
-__global__ void __launch_bounds__(256) k_pass_a(Args<T> A, int TA) {
-    extern __shared__ __align__(16) unsigned char smraw[];
-    C2<T>* sm = reinterpret_cast<C2<T>*>(smraw);
-    const int64_t r = blockIdx.y;
-    const int col0 = blockIdx.x * TA;
-    const int N1 = A.N1, N2 = A.N2;
-    C2<T>* grow = A.grid + r * A.GS;
-    C2<T>* yrow = A.ybuf + r * A.N;
-    const C2<T>* hrow = A.hin + r * A.M;
-    auto load = [&](int f, int n1) -> C2<T> {
-        const int64_t n = (int64_t)N2 * n1 + col0 + f;
-        if (MODE == 0) return grow[n];
-        // adjoint: ghat_q = d_k h_k for k = q (q < M/2) or q - N (q >= N - M/2)
-        const int64_t half = A.M / 2;
-        int64_t c;
-        if (n < half)
-            c = n + half;
-        else if (n >= A.N - half)
-            c = n - (A.N - half);
-        else
-            return mk<T>(T(0), T(0));
-        const C2<T> v = hrow[c];
-        const T d = A.dk[c];
-        return mk<T>(d * v.x, d * v.y);
-    };
-    auto store = [&](int f, int k1, C2<T> v) {
-        const int n2 = col0 + f;
-        const int e = n2 * k1;  // < N
-        const C2<T> w = cmul<T>(twid<T, SIGN>(A.tlo, e & ((1 << A.LB) - 1)), twid<T, SIGN>(A.thi, e >> A.LB));
-        v = cmul<T>(v, w);
-        const int64_t o = (int64_t)k1 * N2 + n2;
-        if (MODE == 0)
-            grow[o] = v;
-        else
-            yrow[o] = v;
-    };
-    cta_fft<T, SIGN, L>(TA, A.tw1, sm, load, store);
-}
-
-// ------------------------------------------------------------------ pass B (rows)
-// MODE 0: inverse, input grid rows, output fhat (kept band times d_k);
-// MODE 1: adjoint, input ybuf rows, output grid (natural order) + halo.
-template <typename T, int SIGN, int MODE, int L>
-__global__ void __launch_bounds__(256) k_pass_b(Args<T> A, int TB) {
-    extern __shared__ __align__(16) unsigned char smraw[];
-    C2<T>* sm = reinterpret_cast<C2<T>*>(smraw);
-    const int64_t r = blockIdx.y;
-    const int row0 = blockIdx.x * TB;
-    const int N1 = A.N1, N2 = A.N2;
-    const C2<T>* src = (MODE == 0) ? (A.grid + r * A.GS) : (A.ybuf + r * A.N);
-    C2<T>* grow = A.grid + r * A.GS;
-    C2<T>* frow = A.fhat + r * A.M;
-    auto load = [&](int f, int n2) -> C2<T> { return src[(int64_t)(row0 + f) * N2 + n2]; };
-    auto store = [&](int f, int k2, C2<T> v) {
-        const int64_t k = (int64_t)(row0 + f) + (int64_t)N1 * k2;
+__global__ void __launch_bounds__(Geo<T, L>::NT, 1)
+    k_pass_a(const __grid_constant__ CUtensorMap map, Args<T> A, int BR, int ntiles) {
+    extern __shared__ __align__(128) unsigned char smraw[];
+    constexpr int CE = (int)(sizeof(C2<T>) / 8);
+    using G = Geo<T, L>;
+    constexpr int TA = G::TF, S = G::S;
+    C2<T>* tile = reinterpret_cast<C2<T>*>(smraw);
+    C2<T>* work = tile + 2 * L * TA;
+    C2<T>* tws = work + S * TA;  // stage twiddles, L / 16 entries
+    uint64_t* bars = reinterpret_cast<uint64_t*>(tws + L / 16);
+    const int N2 = A.N2;
+    const int tiles_per_rhs = N2 / TA;
+    const int B = (int)(A.M / 2 / N2);  // band rows on each side (MODE 1)
+    const uint32_t tile_bytes = (uint32_t)(sizeof(C2<T>) * TA * (MODE == 0 ? L : 2 * B));
+    if (threadIdx.x == 0) {
+        prefetch_tmap(&map);
+        mbar_init(&bars[0], 1);
+        mbar_init(&bars[1], 1);
+        fence_barrier_init();
+    }
+    for (int i = threadIdx.x; i < L / 16; i += blockDim.x) tws[i] = A.tw1[i];
+    __syncthreads();
+    auto issue = [&](int id, int b) {
+        const int r = id / tiles_per_rhs, c0 = (id % tiles_per_rhs) * TA * CE;
+        C2<T>* dst = tile + b * L * TA;
+        mbar_arrive_expect_tx(&bars[b], tile_bytes);
         if (MODE == 0) {
-            const int64_t half = A.M / 2;
-            int64_t c;
-            if (k < half)
-                c = k + half;
-            else if (k >= A.N - half)
-                c = k - (A.N - half);
-            else
-                return;
-            const T d = A.dk[c];
-            frow[c] = mk<T>(d * v.x, d * v.y);
+            for (int q = 0; q < L; q += BR) tma_load_3d(dst + q * TA, &map, c0, q, r, &bars[b]);
         } else {
-            grow[k] = v;
-            if (k < A.H) grow[A.N + k] = v;
+            // tile rows [0, B) <- h rows [B, 2B);  tile rows [L - B, L) <- h rows [0, B)
+            for (int q = 0; q < B; q += BR) {
+                tma_load_3d(dst + q * TA, &map, c0, B + q, r, &bars[b]);
+                tma_load_3d(dst + (L - B + q) * TA, &map, c0, q, r, &bars[b]);
+            }
         }
     };
-    cta_fft<T, SIGN, L>(TB, A.tw2, sm, load, store);
+    // this thread's single butterfly of the last stage: transform fl, outputs k1 = jl + m L/16
+    const int fl = threadIdx.x % TA, jl = threadIdx.x < TA * (L / 16) ? threadIdx.x / TA : 0;
+    const int lmask = (1 << A.LB) - 1;
+    int it = 0;
+    if (threadIdx.x == 0 && (int)blockIdx.x < ntiles) issue(blockIdx.x, 0);
+    for (int id = blockIdx.x; id < ntiles; id += gridDim.x, ++it) {
+        const int b = it & 1;
+        if (threadIdx.x == 0 && id + (int)gridDim.x < ntiles) issue(id + gridDim.x, b ^ 1);
+        const int64_t r = id / tiles_per_rhs;
+        const int col0 = (id % tiles_per_rhs) * TA;
+        // loads independent of the tile data, issued before waiting for it:
+        // four-step twiddles w_N^{n2 k1} = w_N^{n2 jl} (w_N^{n2 L/16})^m ...
+        const int n2l = col0 + fl;
+        const int e0 = n2l * jl, eq = n2l * (L / 16);
+        const C2<T> t0a = twid_g<T, SIGN>(A.tlo, e0 & lmask), t0b = twid_g<T, SIGN>(A.thi, e0 >> A.LB);
+        const C2<T> tqa = twid_g<T, SIGN>(A.tlo, eq & lmask), tqb = twid_g<T, SIGN>(A.thi, eq >> A.LB);
+        // ... and (MODE 1) the deconvolution factors of this thread's first-stage legs
+        T dreg[G::PER0][G::RF];
+        if (MODE == 1) {
+#pragma unroll
+            for (int p = 0; p < G::PER0; ++p)
+#pragma unroll
+                for (int m = 0; m < G::RF; ++m) {
+                    const int t = threadIdx.x + p * G::NT;
+                    const int n1 = t / TA + m * (L / G::RF);
+                    const int n = n1 * N2 + col0 + t % TA;
+                    int c = -1;
+                    if (n1 < B)
+                        c = n + (int)(A.M / 2);
+                    else if (n1 >= L - B)
+                        c = n - (int)(A.N - A.M / 2);
+                    dreg[p][m] = (c >= 0 && t < TA * (L / G::RF)) ? __ldg(A.dk + c) : T(0);
+                }
+        }
+        mbar_wait(&bars[b], (it >> 1) & 1);
+        const C2<T>* tl = tile + b * L * TA;
+        auto load = [&](int f, int n1, int p, int m) -> C2<T> {
+            if (MODE == 0) return tl[n1 * TA + f];
+            if (n1 >= B && n1 < L - B) return mk<T>(T(0), T(0));
+            const C2<T> v = tl[n1 * TA + f];
+            const T d = dreg[p][m];
+            return mk<T>(d * v.x, d * v.y);
+        };
+        const C2<T> wq = cmul<T>(tqa, tqb);
+        C2<T> wcur = cmul<T>(t0a, t0b);
+        C2<T>* orow = (MODE == 0) ? A.grid + r * A.GS : A.ybuf + r * A.N;
+        auto store = [&](int f, int k1, C2<T> v, int m) {
+            if (m > 0) wcur = cmul<T>(wcur, wq);
+            orow[(int64_t)k1 * N2 + col0 + f] = cmul<T>(v, wcur);
+        };
+        cta_fft<T, SIGN, L>(tws, work, load, store);
+        fence_proxy_async();  // this thread's reads of tile[b] precede the next TMA into it
+        __syncthreads();      // tile[b] and work free for the next iteration
+    }
+}
+
+// Pass B (rows, length L = N2, TF = TB rows per tile, tile layout [f][S]):
+//   MODE 0 (inverse): input grid rows, output fhat (kept band times d_c);
+//   MODE 1 (adjoint): input ybuf rows, output grid (natural order) + halo.
+template <typename T, int SIGN, int MODE, int L>
+__global__ void __launch_bounds__(Geo<T, L>::NT, 1) k_pass_b(Args<T> A, int ntiles) {
+    extern __shared__ __align__(128) unsigned char smraw[];
+    using G = Geo<T, L>;
+    constexpr int TB = G::TF, S = G::S;
+    C2<T>* tile = reinterpret_cast<C2<T>*>(smraw);
+    C2<T>* work = tile + 2 * S * TB;
+    C2<T>* tws = work + S * TB;
+    uint64_t* bars = reinterpret_cast<uint64_t*>(tws + L / 16);
+    const int N1 = A.N1;
+    const int tiles_per_rhs = N1 / TB;
+    const C2<T>* src = (MODE == 0) ? A.grid : A.ybuf;
+    const int64_t src_stride = (MODE == 0) ? A.GS : A.N;
+    if (threadIdx.x == 0) {
+        mbar_init(&bars[0], 1);
+        mbar_init(&bars[1], 1);
+        fence_barrier_init();
+    }
+    for (int i = threadIdx.x; i < L / 16; i += blockDim.x) tws[i] = A.tw2[i];
+    __syncthreads();
+    auto issue = [&](int id, int b) {
+        const int64_t r = id / tiles_per_rhs;
+        const int row0 = (id % tiles_per_rhs) * TB;
+        mbar_arrive_expect_tx(&bars[b], (uint32_t)(sizeof(C2<T>) * L * TB));
+        for (int f = 0; f < TB; ++f)
+            bulk_g2s(tile + b * S * TB + f * S, src + r * src_stride + (int64_t)(row0 + f) * L,
+                     (uint32_t)(sizeof(C2<T>) * L), &bars[b]);
+    };
+    const int fl = threadIdx.x % TB, jl = threadIdx.x / TB;
+    const int64_t half = A.M / 2;
+    int it = 0;
+    if (threadIdx.x == 0 && (int)blockIdx.x < ntiles) issue(blockIdx.x, 0);
+    for (int id = blockIdx.x; id < ntiles; id += gridDim.x, ++it) {
+        const int b = it & 1;
+        if (threadIdx.x == 0 && id + (int)gridDim.x < ntiles) issue(id + gridDim.x, b ^ 1);
+        const int64_t r = id / tiles_per_rhs;
+        const int row0 = (id % tiles_per_rhs) * TB;
+        // MODE 0: deconvolution factors of this thread's last-stage outputs, before the wait
+        T dout[16];
+        if (MODE == 0) {
+#pragma unroll
+            for (int m = 0; m < 16; ++m) {
+                const int64_t k = (int64_t)(row0 + fl) + (int64_t)N1 * (jl + m * (L / 16));
+                int64_t c = -1;
+                if (k < half)
+                    c = k + half;
+                else if (k >= A.N - half)
+                    c = k - (A.N - half);
+                dout[m] = (c >= 0 && jl < L / 16) ? __ldg(A.dk + c) : T(0);
+            }
+        }
+        mbar_wait(&bars[b], (it >> 1) & 1);
+        const C2<T>* tl = tile + b * S * TB;
+        C2<T>* grow = A.grid + r * A.GS;
+        C2<T>* frow = A.fhat + r * A.M;
+        auto load = [&](int f, int n2, int, int) -> C2<T> { return tl[sidx<G>(f, n2)]; };
+        auto store = [&](int f, int k2, C2<T> v, int m) {
+            const int64_t k = (int64_t)(row0 + f) + (int64_t)N1 * k2;
+            if (MODE == 0) {
+                int64_t c;
+                if (k < half)
+                    c = k + half;
+                else if (k >= A.N - half)
+                    c = k - (A.N - half);
+                else
+                    return;
+                const T d = dout[m];
+                frow[c] = mk<T>(d * v.x, d * v.y);
+            } else {
+                grow[k] = v;
+                if (k < A.H) grow[A.N + k] = v;
+            }
+        };
+        cta_fft<T, SIGN, L>(tws, work, load, store);
+        fence_proxy_async();
+        __syncthreads();
+    }
 }
 
 }  // namespace fft
 
 // =========================================================================== host
-static void radix_plan(int L, int* rad, int& nst) {
-    nst = 0;
-    int rem = L;
-    while (rem > 1) {
-        int R = rem >= 16 ? 16 : rem;
-        rad[nst++] = R;
-        rem /= R;
-    }
-    // put the smallest radix first (its stage reads global memory)
-    std::reverse(rad, rad + nst);
-}
-
 template <typename T>
 __global__ void k_twiddle_table(C2<T>* out, int64_t count, int64_t denom, int64_t mult) {
     int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
@@ -369,11 +490,25 @@ static std::map<const Plan*, FftState*>& fft_states() {
     return m;
 }
 
+static int split_n1(int64_t N) {
+    int lg = 0;
+    while ((int64_t(1) << lg) < N) lg++;
+    return 1 << (lg / 2);
+}
+
 bool fused_fft_available(const Plan& p) {
     if (p.d != 1) return false;
     const int64_t N = p.Ms[0];
     if (N < 256 || (N & (N - 1)) || N > (int64_t(1) << 24)) return false;
-    if (p.GS < N) return false;
+    if (p.GS < N || (p.GS & 1)) return false;
+    // pass A of the adjoint fetches whole band rows of h: M/2 must be a multiple of N2
+    const int64_t N2 = N / split_n1(N);
+    const int64_t half = p.M[0] / 2;
+    if (p.M[0] % 2 || half % N2) return false;
+    const int64_t B = half / N2;
+    if (B > 256 && B % 256) return false;
+    // pass A's TMA box is TF columns wide and must span >= 16 bytes (TF = 1 only for N1 = 4096)
+    if (p.prec == INFT_C64 && split_n1(N) >= 4096) return false;
     return true;
 }
 
@@ -386,7 +521,7 @@ static FftState& fft_state(Plan& p, cudaStream_t st) {
     const int64_t N = p.Ms[0];
     int lg = 0;
     while ((int64_t(1) << lg) < N) lg++;
-    s->N1 = 1 << (lg / 2);       // strided pass (columns)
+    s->N1 = split_n1(N);         // strided pass (columns)
     s->N2 = (int)(N / s->N1);    // contiguous pass (rows), N2 >= N1
     s->LB = (lg + 1) / 2;
     const size_t cs = sizeof(C2<T>);
@@ -425,8 +560,6 @@ static fft::Args<T> make_args(Plan& p, FftState& s) {
     A.N2 = s.N2;
     A.LB = s.LB;
     A.H = (int)(p.GS - p.Ms[0]);
-    radix_plan(s.N1, A.rad1, A.nst1);
-    radix_plan(s.N2, A.rad2, A.nst2);
     A.tw1 = s.tw1.as<C2<T>>();
     A.tw2 = s.tw2.as<C2<T>>();
     A.tlo = s.tlo.as<C2<T>>();
@@ -434,54 +567,100 @@ static fft::Args<T> make_args(Plan& p, FftState& s) {
     return A;
 }
 
-static int tile_for(int L, size_t cs) {
-    // ~64 KB of shared memory per CTA (3 CTAs per SM), at least one transform
-    int t = (int)std::max<size_t>(1, (size_t)(64 * 1024) / ((size_t)L * cs));
-    t = std::min(t, 8);
-    while (t > 1 && (t & (t - 1))) t--;
-    return t;
-}
+template <typename T>
+using PassAFn = void (*)(const CUtensorMap, fft::Args<T>, int, int);
+template <typename T>
+using PassBFn = void (*)(fft::Args<T>, int);
 
 template <typename T, int L>
-static void (*pick_L(int which, int mode))(fft::Args<T>, int) {
+static void pick_L(int mode, PassAFn<T>& a, PassBFn<T>& b) {
     // mode 0 = inverse NFFT (forward sign), mode 1 = inverse adjoint (inverse sign)
-    if (which == 0) return mode == 0 ? fft::k_pass_a<T, -1, 0, L> : fft::k_pass_a<T, 1, 1, L>;
-    return mode == 0 ? fft::k_pass_b<T, -1, 0, L> : fft::k_pass_b<T, 1, 1, L>;
+    a = mode == 0 ? fft::k_pass_a<T, -1, 0, L> : fft::k_pass_a<T, 1, 1, L>;
+    b = mode == 0 ? fft::k_pass_b<T, -1, 0, L> : fft::k_pass_b<T, 1, 1, L>;
 }
 
 template <typename T>
-static void (*pick_kernel(int which, int mode, int L))(fft::Args<T>, int) {
+static bool pick_kernels(int mode, int L, PassAFn<T>& a, PassBFn<T>& b, int& TF, int& S, int& NT) {
+#define INFT_GEO(LL) TF = fft::Geo<T, LL>::TF, S = fft::Geo<T, LL>::S, NT = fft::Geo<T, LL>::NT
     switch (L) {
-        case 16: return pick_L<T, 16>(which, mode);
-        case 32: return pick_L<T, 32>(which, mode);
-        case 64: return pick_L<T, 64>(which, mode);
-        case 128: return pick_L<T, 128>(which, mode);
-        case 256: return pick_L<T, 256>(which, mode);
-        case 512: return pick_L<T, 512>(which, mode);
-        case 1024: return pick_L<T, 1024>(which, mode);
-        case 2048: return pick_L<T, 2048>(which, mode);
-        case 4096: return pick_L<T, 4096>(which, mode);
+        case 16: pick_L<T, 16>(mode, a, b); INFT_GEO(16); return true;
+        case 32: pick_L<T, 32>(mode, a, b); INFT_GEO(32); return true;
+        case 64: pick_L<T, 64>(mode, a, b); INFT_GEO(64); return true;
+        case 128: pick_L<T, 128>(mode, a, b); INFT_GEO(128); return true;
+        case 256: pick_L<T, 256>(mode, a, b); INFT_GEO(256); return true;
+        case 512: pick_L<T, 512>(mode, a, b); INFT_GEO(512); return true;
+        case 1024: pick_L<T, 1024>(mode, a, b); INFT_GEO(1024); return true;
+        case 2048: pick_L<T, 2048>(mode, a, b); INFT_GEO(2048); return true;
+        case 4096: pick_L<T, 4096>(mode, a, b); INFT_GEO(4096); return true;
     }
-    return nullptr;
+#undef INFT_GEO
+    return false;
 }
 
+static int num_sms() {
+    static int n = 0;
+    if (!n) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+        if (n <= 0) n = 148;
+    }
+    return n;
+}
+
+// pass A over `src` (MODE 0: the grid, rows GS; MODE 1: h, rows M)
 template <typename T>
-static void launch_pass(Plan& p, fft::Args<T>& A, int which, int mode, int sign, int64_t R, cudaStream_t st) {
-    const int L = which == 0 ? A.N1 : A.N2;
-    const int other = which == 0 ? A.N2 : A.N1;
-    // TF transforms per CTA: ~64 KB of shared memory, <= 256 threads (TF * L / 16)
-    const int TF = std::max(1, std::min({tile_for(L, sizeof(C2<T>)), other, std::max(1, 4096 / L)}));
-    const size_t smem = sizeof(C2<T>) * (size_t)((L + 2) * TF);
-    int threads = TF * (L / 16);
-    threads = std::max(32, std::min(256, threads));
-    dim3 g((unsigned)(other / TF), (unsigned)R);
-    void (*kern)(fft::Args<T>, int) = pick_kernel<T>(which, mode, L);
-    if (!kern) {
+static void launch_pass_a(Plan& p, fft::Args<T>& A, int mode, const void* src, int64_t R, cudaStream_t st) {
+    const size_t cs = sizeof(C2<T>);
+    constexpr int CE = (int)(sizeof(C2<T>) / 8);
+    const int L = A.N1;
+    PassAFn<T> ka = nullptr;
+    PassBFn<T> kb = nullptr;
+    int TA, S, threads;
+    if (!pick_kernels<T>(mode, L, ka, kb, TA, S, threads)) {
         set_error("fused FFT: unsupported factor length");
         throw Fail{INFT_ERR_UNSUPPORTED};
     }
-    INFT_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    kern<<<g, threads, smem, st>>>(A, TF);
+    CUtensorMap map;
+    int BR;
+    bool ok;
+    if (mode == 0) {
+        BR = std::min(L, 256);
+        ok = make_tmap_3d(&map, src, (uint64_t)A.N2 * CE, (uint64_t)A.N1, (uint64_t)R, cs * (uint64_t)A.N2,
+                          cs * (uint64_t)A.GS, (uint32_t)(TA * CE), (uint32_t)BR);
+    } else {
+        const int B = (int)(A.M / 2 / A.N2);
+        BR = std::min(B, 256);
+        ok = make_tmap_3d(&map, src, (uint64_t)A.N2 * CE, (uint64_t)(A.M / A.N2), (uint64_t)R, cs * (uint64_t)A.N2,
+                          cs * (uint64_t)A.M, (uint32_t)(TA * CE), (uint32_t)BR);
+    }
+    if (!ok) {
+        set_error("cuTensorMapEncodeTiled failed (fused FFT pass A)");
+        throw Fail{INFT_ERR_CUDA};
+    }
+    const size_t smem = cs * (size_t)(2 * L * TA + S * TA + L / 16) + 16;
+    const int ntiles = (int)(R * (A.N2 / TA));
+    INFT_CUDA(cudaFuncSetAttribute(ka, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    ka<<<(unsigned)std::min(ntiles, num_sms()), threads, smem, st>>>(map, A, BR, ntiles);
+    INFT_CHECK_LAUNCH();
+    p.launches++;
+}
+
+template <typename T>
+static void launch_pass_b(Plan& p, fft::Args<T>& A, int mode, int64_t R, cudaStream_t st) {
+    const size_t cs = sizeof(C2<T>);
+    const int L = A.N2;
+    PassAFn<T> ka = nullptr;
+    PassBFn<T> kb = nullptr;
+    int TB, S, threads;
+    if (!pick_kernels<T>(mode, L, ka, kb, TB, S, threads)) {
+        set_error("fused FFT: unsupported factor length");
+        throw Fail{INFT_ERR_UNSUPPORTED};
+    }
+    const size_t smem = cs * (size_t)(3 * S * TB + L / 16) + 16;
+    const int ntiles = (int)(R * (A.N1 / TB));
+    INFT_CUDA(cudaFuncSetAttribute(kb, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    kb<<<(unsigned)std::min(ntiles, num_sms()), threads, smem, st>>>(A, ntiles);
     INFT_CHECK_LAUNCH();
     p.launches++;
 }
@@ -501,8 +680,8 @@ static void fused_inverse_t(Plan& p, void* grid, void* fhat, int64_t R, cudaStre
     A.grid = static_cast<C2<T>*>(grid);
     A.fhat = static_cast<C2<T>*>(fhat);
     A.dk = dtab_for<T>(p);
-    launch_pass<T>(p, A, 0, 0, -1, R, st);
-    launch_pass<T>(p, A, 1, 0, -1, R, st);
+    launch_pass_a<T>(p, A, 0, grid, R, st);
+    launch_pass_b<T>(p, A, 0, R, st);
 }
 
 // adjoint: h -> grid (D, zero pad, F), natural order with halo
@@ -518,8 +697,8 @@ static void fused_adjoint_t(Plan& p, const void* h, void* grid, int64_t R, cudaS
     A.ybuf = s.ybuf.as<C2<T>>();
     A.hin = static_cast<const C2<T>*>(h);
     A.dk = dtab_for<T>(p);
-    launch_pass<T>(p, A, 0, 1, +1, R, st);
-    launch_pass<T>(p, A, 1, 1, +1, R, st);
+    launch_pass_a<T>(p, A, 1, h, R, st);
+    launch_pass_b<T>(p, A, 1, R, st);
 }
 
 void fused_fft_inverse(Plan& p, void* grid, void* fhat, int64_t R, cudaStream_t st) {

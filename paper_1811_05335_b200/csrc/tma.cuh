@@ -67,6 +67,16 @@ __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, i
         : "memory");
 }
 
+// 3-D tiled tensor copy global -> shared (coordinates in elements, innermost first).
+__device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, int c0, int c1, int c2,
+                                            uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, "
+        "%4}], [%5];" ::"r"(smem_addr(dst)),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(smem_addr(bar))
+        : "memory");
+}
+
 // Order this thread's prior generic-proxy shared-memory accesses before later
 // async-proxy (TMA / bulk copy) accesses: required before releasing a stage
 // buffer that the next TMA will overwrite (cross-proxy WAR hazard).
@@ -109,5 +119,11 @@ __device__ __forceinline__ uint32_t swz128(int row, int c) { return (uint32_t)ro
 // (SWIZZLE_128B); out-of-bounds elements read as zero.
 bool make_tmap_2d(CUtensorMap* out, const void* base, uint64_t inner, uint64_t rows, uint64_t row_stride_bytes,
                   uint32_t box_rows);
+
+// Host: 3-D tensor map over [d2][d1][d0] 8-byte elements (strides s1, s2 in bytes, multiples
+// of 16), box {b0, b1, 1}, no swizzle: a box lands in shared memory as a row-major
+// [b1][b0] array.
+bool make_tmap_3d(CUtensorMap* out, const void* base, uint64_t d0, uint64_t d1, uint64_t d2, uint64_t s1,
+                  uint64_t s2, uint32_t b0, uint32_t b1);
 
 }  // namespace inft
