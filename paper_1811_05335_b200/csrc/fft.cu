@@ -15,6 +15,8 @@
 //                 elsewhere -- no padded grid is materialised), pass B writes the natural-
 //                 order grid and its 2m halo for the gather.
 #include <algorithm>
+#include <cstdio>
+#include <cstring>
 #include <vector>
 
 #include "common.cuh"
@@ -274,6 +276,12 @@ __device__ __forceinline__ void cta_fft(const C2<T>* tw, C2<T>* sm, Load&& load,
     fft_stages<T, SIGN, Geo<T, L>, 0, 1>(tw, sm, load, store);
 }
 
+// byte offset of pass B's deconvolution tile: after tile[2] | work | twiddles, 128-aligned
+template <typename T>
+__host__ __device__ constexpr size_t d_offset(int L, int S, int TB) {
+    return ((sizeof(C2<T>) * (size_t)(3 * S * TB + L / 16)) + 127) / 128 * 128;
+}
+
 // ------------------------------------------------------------------ persistent tiled passes
 // Each pass is a persistent kernel (one CTA per SM) walking a list of tiles; the next tile
 // is copied into the other half of a double buffer by the Tensor Memory Accelerator (pass A:
@@ -290,7 +298,8 @@ __device__ __forceinline__ void cta_fft(const C2<T>* tw, C2<T>* sm, Load&& load,
 //                     the other rows are zero and never read), output to ybuf.
 template <typename T, int SIGN, int MODE, int L>
 __global__ void __launch_bounds__(Geo<T, L>::NT, 1)
-    k_pass_a(const __grid_constant__ CUtensorMap map, Args<T> A, int BR, int ntiles) {
+    k_pass_a(const __grid_constant__ CUtensorMap map, const __grid_constant__ CUtensorMap dmap, Args<T> A, int BR,
+             int ntiles) {
     extern __shared__ __align__(128) unsigned char smraw[];
     constexpr int CE = (int)(sizeof(C2<T>) / 8);
     using G = Geo<T, L>;
@@ -302,9 +311,14 @@ __global__ void __launch_bounds__(Geo<T, L>::NT, 1)
     const int N2 = A.N2;
     const int tiles_per_rhs = N2 / TA;
     const int B = (int)(A.M / 2 / N2);  // band rows on each side (MODE 1)
-    const uint32_t tile_bytes = (uint32_t)(sizeof(C2<T>) * TA * (MODE == 0 ? L : 2 * B));
+    // MODE 1: the deconvolution factors of the band rows land in the unused middle rows of the
+    // tile buffer, as [2B][DW] (rows: d rows [B, 2B) then [0, B); DW >= TA columns)
+    constexpr int DW = (int)(16 / sizeof(T)) > TA ? (int)(16 / sizeof(T)) : TA;
+    const uint32_t tile_bytes = (uint32_t)(MODE == 0 ? sizeof(C2<T>) * TA * L
+                                                     : sizeof(C2<T>) * TA * 2 * B + sizeof(T) * DW * 2 * B);
     if (threadIdx.x == 0) {
         prefetch_tmap(&map);
+        if (MODE == 1) prefetch_tmap(&dmap);
         mbar_init(&bars[0], 1);
         mbar_init(&bars[1], 1);
         fence_barrier_init();
@@ -319,9 +333,13 @@ __global__ void __launch_bounds__(Geo<T, L>::NT, 1)
             for (int q = 0; q < L; q += BR) tma_load_3d(dst + q * TA, &map, c0, q, r, &bars[b]);
         } else {
             // tile rows [0, B) <- h rows [B, 2B);  tile rows [L - B, L) <- h rows [0, B)
+            T* dsm = reinterpret_cast<T*>(dst + B * TA);
+            const int dc0 = ((id % tiles_per_rhs) * TA) & ~(DW - 1);  // 16-byte aligned box start
             for (int q = 0; q < B; q += BR) {
                 tma_load_3d(dst + q * TA, &map, c0, B + q, r, &bars[b]);
                 tma_load_3d(dst + (L - B + q) * TA, &map, c0, q, r, &bars[b]);
+                tma_load_3d(dsm + q * DW, &dmap, dc0, B + q, 0, &bars[b]);
+                tma_load_3d(dsm + (B + q) * DW, &dmap, dc0, q, 0, &bars[b]);
             }
         }
     };
@@ -341,31 +359,14 @@ __global__ void __launch_bounds__(Geo<T, L>::NT, 1)
         const int e0 = n2l * jl, eq = n2l * (L / 16);
         const C2<T> t0a = twid_g<T, SIGN>(A.tlo, e0 & lmask), t0b = twid_g<T, SIGN>(A.thi, e0 >> A.LB);
         const C2<T> tqa = twid_g<T, SIGN>(A.tlo, eq & lmask), tqb = twid_g<T, SIGN>(A.thi, eq >> A.LB);
-        // ... and (MODE 1) the deconvolution factors of this thread's first-stage legs
-        T dreg[G::PER0][G::RF];
-        if (MODE == 1) {
-#pragma unroll
-            for (int p = 0; p < G::PER0; ++p)
-#pragma unroll
-                for (int m = 0; m < G::RF; ++m) {
-                    const int t = threadIdx.x + p * G::NT;
-                    const int n1 = t / TA + m * (L / G::RF);
-                    const int n = n1 * N2 + col0 + t % TA;
-                    int c = -1;
-                    if (n1 < B)
-                        c = n + (int)(A.M / 2);
-                    else if (n1 >= L - B)
-                        c = n - (int)(A.N - A.M / 2);
-                    dreg[p][m] = (c >= 0 && t < TA * (L / G::RF)) ? __ldg(A.dk + c) : T(0);
-                }
-        }
         mbar_wait(&bars[b], (it >> 1) & 1);
         const C2<T>* tl = tile + b * L * TA;
-        auto load = [&](int f, int n1, int p, int m) -> C2<T> {
+        const T* dsm = reinterpret_cast<const T*>(tl + B * TA);
+        auto load = [&](int f, int n1, int, int) -> C2<T> {
             if (MODE == 0) return tl[n1 * TA + f];
             if (n1 >= B && n1 < L - B) return mk<T>(T(0), T(0));
             const C2<T> v = tl[n1 * TA + f];
-            const T d = dreg[p][m];
+            const T d = dsm[(n1 < B ? n1 : n1 - (L - 2 * B)) * DW + (col0 & (DW - 1)) + f];
             return mk<T>(d * v.x, d * v.y);
         };
         const C2<T> wq = cmul<T>(tqa, tqb);
@@ -385,21 +386,30 @@ __global__ void __launch_bounds__(Geo<T, L>::NT, 1)
 //   MODE 0 (inverse): input grid rows, output fhat (kept band times d_c);
 //   MODE 1 (adjoint): input ybuf rows, output grid (natural order) + halo.
 template <typename T, int SIGN, int MODE, int L>
-__global__ void __launch_bounds__(Geo<T, L>::NT, 1) k_pass_b(Args<T> A, int ntiles) {
+__global__ void __launch_bounds__(Geo<T, L>::NT, 1)
+    k_pass_b(const __grid_constant__ CUtensorMap dmap, Args<T> A, int BRd, int ntiles) {
     extern __shared__ __align__(128) unsigned char smraw[];
     using G = Geo<T, L>;
     constexpr int TB = G::TF, S = G::S;
+    // MODE 0: the deconvolution factors of the tile's kept outputs, [2 B2][DW] (rows: k2 in
+    // [0, B2), then k2 in [N2 - B2, N2)), fetched by TMA while the first stages run
+    constexpr int DW = (int)(16 / sizeof(T)) > TB ? (int)(16 / sizeof(T)) : TB;
+    const int N1 = A.N1;
+    const int64_t half = A.M / 2;
+    const int B2 = (int)(half / N1);  // kept k2 rows: [0, B2) and [N2 - B2, N2)
     C2<T>* tile = reinterpret_cast<C2<T>*>(smraw);
     C2<T>* work = tile + 2 * S * TB;
     C2<T>* tws = work + S * TB;
-    uint64_t* bars = reinterpret_cast<uint64_t*>(tws + L / 16);
-    const int N1 = A.N1;
+    T* dsm = reinterpret_cast<T*>(smraw + d_offset<T>(L, S, TB));
+    uint64_t* bars = reinterpret_cast<uint64_t*>(dsm + (MODE == 0 ? 2 * B2 * DW : 0));
     const int tiles_per_rhs = N1 / TB;
     const C2<T>* src = (MODE == 0) ? A.grid : A.ybuf;
     const int64_t src_stride = (MODE == 0) ? A.GS : A.N;
     if (threadIdx.x == 0) {
+        if (MODE == 0) prefetch_tmap(&dmap);
         mbar_init(&bars[0], 1);
         mbar_init(&bars[1], 1);
+        mbar_init(&bars[2], 1);
         fence_barrier_init();
     }
     for (int i = threadIdx.x; i < L / 16; i += blockDim.x) tws[i] = A.tw2[i];
@@ -412,27 +422,24 @@ __global__ void __launch_bounds__(Geo<T, L>::NT, 1) k_pass_b(Args<T> A, int ntil
             bulk_g2s(tile + b * S * TB + f * S, src + r * src_stride + (int64_t)(row0 + f) * L,
                      (uint32_t)(sizeof(C2<T>) * L), &bars[b]);
     };
-    const int fl = threadIdx.x % TB, jl = threadIdx.x / TB;
-    const int64_t half = A.M / 2;
     int it = 0;
     if (threadIdx.x == 0 && (int)blockIdx.x < ntiles) issue(blockIdx.x, 0);
     for (int id = blockIdx.x; id < ntiles; id += gridDim.x, ++it) {
         const int b = it & 1;
-        if (threadIdx.x == 0 && id + (int)gridDim.x < ntiles) issue(id + gridDim.x, b ^ 1);
         const int64_t r = id / tiles_per_rhs;
         const int row0 = (id % tiles_per_rhs) * TB;
-        // MODE 0: deconvolution factors of this thread's last-stage outputs, before the wait
-        T dout[16];
-        if (MODE == 0) {
-#pragma unroll
-            for (int m = 0; m < 16; ++m) {
-                const int64_t k = (int64_t)(row0 + fl) + (int64_t)N1 * (jl + m * (L / 16));
-                int64_t c = -1;
-                if (k < half)
-                    c = k + half;
-                else if (k >= A.N - half)
-                    c = k - (A.N - half);
-                dout[m] = (c >= 0 && jl < L / 16) ? __ldg(A.dk + c) : T(0);
+        if (threadIdx.x == 0) {
+            if (id + (int)gridDim.x < ntiles) issue(id + gridDim.x, b ^ 1);
+            if (MODE == 0) {
+                // d rows [B2, 2 B2) (k2 < B2) and [0, B2) (k2 >= N2 - B2), columns row0 ..
+                // the box's inner start must be 16-byte aligned (an unaligned start coordinate
+                // faults with "illegal instruction"): start at row0 rounded down to DW
+                const int dc0 = row0 & ~(DW - 1);
+                mbar_arrive_expect_tx(&bars[2], (uint32_t)(sizeof(T) * DW * 2 * B2));
+                for (int q = 0; q < B2; q += BRd) {
+                    tma_load_3d(dsm + q * DW, &dmap, dc0, B2 + q, 0, &bars[2]);
+                    tma_load_3d(dsm + (B2 + q) * DW, &dmap, dc0, q, 0, &bars[2]);
+                }
             }
         }
         mbar_wait(&bars[b], (it >> 1) & 1);
@@ -443,14 +450,19 @@ __global__ void __launch_bounds__(Geo<T, L>::NT, 1) k_pass_b(Args<T> A, int ntil
         auto store = [&](int f, int k2, C2<T> v, int m) {
             const int64_t k = (int64_t)(row0 + f) + (int64_t)N1 * k2;
             if (MODE == 0) {
+                if (m == 0) mbar_wait(&bars[2], it & 1);
                 int64_t c;
-                if (k < half)
+                int sr;
+                if (k2 < B2) {
                     c = k + half;
-                else if (k >= A.N - half)
+                    sr = k2;
+                } else if (k2 >= L - B2) {
                     c = k - (A.N - half);
-                else
+                    sr = k2 - (L - 2 * B2);
+                } else {
                     return;
-                const T d = dout[m];
+                }
+                const T d = dsm[sr * DW + (row0 & (DW - 1)) + f];
                 frow[c] = mk<T>(d * v.x, d * v.y);
             } else {
                 grow[k] = v;
@@ -507,6 +519,29 @@ bool fused_fft_available(const Plan& p) {
     if (p.M[0] % 2 || half % N2) return false;
     const int64_t B = half / N2;
     if (B > 256 && B % 256) return false;
+    // pass A of the adjoint stages d (2B rows x >= 16 bytes) in the tile's unused middle rows
+    {
+        const int N1 = split_n1(N);
+        const int TF = N1 >= 512 ? 4096 / N1 : 8;
+        const size_t cs = p.prec == INFT_C128 ? 16 : 8, ds = cs / 2;
+        const size_t dw = std::max<size_t>((size_t)TF, 16 / ds);
+        if ((size_t)(N1 - 2 * B) * TF * cs < (size_t)2 * B * dw * ds) return false;
+        // TMA destinations 128-byte aligned
+        if (((size_t)B * TF * cs) % 128 || ((size_t)B * dw * ds) % 128) return false;
+    }
+    // pass B of the inverse stages the tile's d factors: shared memory must fit
+    {
+        const int N2i = (int)N2;
+        const int TF = N2i >= 512 ? 4096 / N2i : 8;
+        const size_t cs = p.prec == INFT_C128 ? 16 : 8, ds = cs / 2;
+        const int pad = std::max(1, (int)(128 / cs) / TF);
+        const size_t dw = std::max<size_t>((size_t)TF, 16 / ds);
+        const size_t B2 = (size_t)(half / split_n1(N));
+        const size_t smem = ((cs * (size_t)(3 * (N2i + pad) * TF + N2i / 16)) + 127) / 128 * 128 + ds * 2 * B2 * dw + 32;
+        if (smem > 227 * 1024) return false;
+        if (B2 > 256 && B2 % 256) return false;
+        if ((B2 * dw * ds) % 128) return false;
+    }
     // pass A's TMA box is TF columns wide and must span >= 16 bytes (TF = 1 only for N1 = 4096)
     if (p.prec == INFT_C64 && split_n1(N) >= 4096) return false;
     return true;
@@ -568,9 +603,9 @@ static fft::Args<T> make_args(Plan& p, FftState& s) {
 }
 
 template <typename T>
-using PassAFn = void (*)(const CUtensorMap, fft::Args<T>, int, int);
+using PassAFn = void (*)(const CUtensorMap, const CUtensorMap, fft::Args<T>, int, int);
 template <typename T>
-using PassBFn = void (*)(fft::Args<T>, int);
+using PassBFn = void (*)(const CUtensorMap, fft::Args<T>, int, int);
 
 template <typename T, int L>
 static void pick_L(int mode, PassAFn<T>& a, PassBFn<T>& b) {
@@ -621,7 +656,7 @@ static void launch_pass_a(Plan& p, fft::Args<T>& A, int mode, const void* src, i
         set_error("fused FFT: unsupported factor length");
         throw Fail{INFT_ERR_UNSUPPORTED};
     }
-    CUtensorMap map;
+    CUtensorMap map, dmap;
     int BR;
     bool ok;
     if (mode == 0) {
@@ -633,7 +668,12 @@ static void launch_pass_a(Plan& p, fft::Args<T>& A, int mode, const void* src, i
         BR = std::min(B, 256);
         ok = make_tmap_3d(&map, src, (uint64_t)A.N2 * CE, (uint64_t)(A.M / A.N2), (uint64_t)R, cs * (uint64_t)A.N2,
                           cs * (uint64_t)A.M, (uint32_t)(TA * CE), (uint32_t)BR);
+        // deconvolution table d as [M / N2][N2], boxes DW columns wide (>= 16 bytes)
+        const int DW = std::max<int>(TA, (int)(16 / sizeof(T)));
+        ok = ok && make_tmap_3d(&dmap, A.dk, (uint64_t)A.N2, (uint64_t)(A.M / A.N2), 1, sizeof(T) * (uint64_t)A.N2,
+                                sizeof(T) * (uint64_t)A.M, (uint32_t)DW, (uint32_t)BR, (int)sizeof(T));
     }
+    if (mode == 0) dmap = map;
     if (!ok) {
         set_error("cuTensorMapEncodeTiled failed (fused FFT pass A)");
         throw Fail{INFT_ERR_CUDA};
@@ -641,7 +681,7 @@ static void launch_pass_a(Plan& p, fft::Args<T>& A, int mode, const void* src, i
     const size_t smem = cs * (size_t)(2 * L * TA + S * TA + L / 16) + 16;
     const int ntiles = (int)(R * (A.N2 / TA));
     INFT_CUDA(cudaFuncSetAttribute(ka, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    ka<<<(unsigned)std::min(ntiles, num_sms()), threads, smem, st>>>(map, A, BR, ntiles);
+    ka<<<(unsigned)std::min(ntiles, num_sms()), threads, smem, st>>>(map, dmap, A, BR, ntiles);
     INFT_CHECK_LAUNCH();
     p.launches++;
 }
@@ -657,10 +697,24 @@ static void launch_pass_b(Plan& p, fft::Args<T>& A, int mode, int64_t R, cudaStr
         set_error("fused FFT: unsupported factor length");
         throw Fail{INFT_ERR_UNSUPPORTED};
     }
-    const size_t smem = cs * (size_t)(3 * S * TB + L / 16) + 16;
+    const int B2 = (int)(A.M / 2 / A.N1);
+    const int DW = std::max<int>(TB, (int)(16 / sizeof(T)));
+    const size_t smem = fft::d_offset<T>(L, S, TB) + (mode == 0 ? sizeof(T) * (size_t)(2 * B2 * DW) : 0) + 32;
+    CUtensorMap dmap;
+    const int BRd = std::min(B2, 256);
+    if (mode == 0) {
+        // deconvolution table d as [M / N1][N1]: row k2', column k1
+        if (!make_tmap_3d(&dmap, A.dk, (uint64_t)A.N1, (uint64_t)(A.M / A.N1), 1, sizeof(T) * (uint64_t)A.N1,
+                          sizeof(T) * (uint64_t)A.M, (uint32_t)DW, (uint32_t)BRd, (int)sizeof(T))) {
+            set_error("cuTensorMapEncodeTiled failed (fused FFT pass B)");
+            throw Fail{INFT_ERR_CUDA};
+        }
+    } else {
+        memset(&dmap, 0, sizeof(dmap));
+    }
     const int ntiles = (int)(R * (A.N1 / TB));
     INFT_CUDA(cudaFuncSetAttribute(kb, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    kb<<<(unsigned)std::min(ntiles, num_sms()), threads, smem, st>>>(A, ntiles);
+    kb<<<(unsigned)std::min(ntiles, num_sms()), threads, smem, st>>>(dmap, A, BRd, ntiles);
     INFT_CHECK_LAUNCH();
     p.launches++;
 }

@@ -38,7 +38,20 @@ struct Fail {
         }                                                                                \
     } while (0)
 
-#define INFT_CHECK_LAUNCH() INFT_CUDA(cudaGetLastError())
+#define INFT_STR2_(x) #x
+#define INFT_STR_(x) INFT_STR2_(x)
+// INFT_SYNC_CHECK=1: synchronize after every launch so a fault names its kernel's call site
+bool sync_check_enabled();
+#define INFT_CHECK_LAUNCH()                                                              \
+    do {                                                                                 \
+        cudaError_t e_ = cudaGetLastError();                                             \
+        if (e_ == cudaSuccess && ::inft::sync_check_enabled()) e_ = cudaDeviceSynchronize(); \
+        if (e_ != cudaSuccess) {                                                         \
+            ::inft::set_error(std::string("kernel launch at " __FILE__ ":" INFT_STR_(__LINE__) ": ") + \
+                              cudaGetErrorString(e_));                                   \
+            throw ::inft::Fail{INFT_ERR_CUDA};                                           \
+        }                                                                                \
+    } while (0)
 
 // ------------------------------------------------------------ device buffer
 struct DevBuf {

@@ -18,6 +18,14 @@
 namespace inft {
 
 static thread_local std::string g_last_error;
+bool sync_check_enabled() {
+    static const bool on = [] {
+        const char* e = getenv("INFT_SYNC_CHECK");
+        return e && atoi(e) != 0;
+    }();
+    return on;
+}
+
 void set_error(const std::string& msg) { g_last_error = msg; }
 
 void DevBuf::alloc(size_t b) {

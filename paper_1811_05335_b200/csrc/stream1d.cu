@@ -668,14 +668,15 @@ static PFN_cuTensorMapEncodeTiled_v12000 tmap_encoder() {
 }
 
 bool make_tmap_3d(CUtensorMap* out, const void* base, uint64_t d0, uint64_t d1, uint64_t d2, uint64_t s1,
-                  uint64_t s2, uint32_t b0, uint32_t b1) {
+                  uint64_t s2, uint32_t b0, uint32_t b1, int esize) {
     PFN_cuTensorMapEncodeTiled_v12000 encode = tmap_encoder();
     if (!encode) return false;
     cuuint64_t dims[3] = {d0, d1, d2};
     cuuint64_t strides[2] = {s1, s2};
     cuuint32_t box[3] = {b0, b1, 1u};
     cuuint32_t estr[3] = {1, 1, 1};
-    CUresult r = encode(out, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, const_cast<void*>(base), dims, strides, box, estr,
+    CUresult r = encode(out, esize == 4 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3,
+                        const_cast<void*>(base), dims, strides, box, estr,
                         CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                         CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     return r == CUDA_SUCCESS;

@@ -120,10 +120,10 @@ __device__ __forceinline__ uint32_t swz128(int row, int c) { return (uint32_t)ro
 bool make_tmap_2d(CUtensorMap* out, const void* base, uint64_t inner, uint64_t rows, uint64_t row_stride_bytes,
                   uint32_t box_rows);
 
-// Host: 3-D tensor map over [d2][d1][d0] 8-byte elements (strides s1, s2 in bytes, multiples
-// of 16), box {b0, b1, 1}, no swizzle: a box lands in shared memory as a row-major
-// [b1][b0] array.
+// Host: 3-D tensor map over [d2][d1][d0] elements of `esize` bytes (8: FLOAT64, 4: FLOAT32;
+// strides s1, s2 in bytes, multiples of 16), box {b0, b1, 1} (b0 * esize a multiple of 16),
+// no swizzle: a box lands in shared memory as a row-major [b1][b0] array.
 bool make_tmap_3d(CUtensorMap* out, const void* base, uint64_t d0, uint64_t d1, uint64_t d2, uint64_t s1,
-                  uint64_t s2, uint32_t b0, uint32_t b1);
+                  uint64_t s2, uint32_t b0, uint32_t b1, int esize = 8);
 
 }  // namespace inft
