@@ -574,8 +574,10 @@ static void spread_t(Plan& p, const void* f, void* grid, int64_t R, cudaStream_t
     Fns<T> F = fns_for<T>(p.m, p.S[0]);
     const int nseg = (int)p.nseg[0];
     const int nchunks = (int)ceil_div(nseg, kQ);
-    // KNOWN ISSUE: the staged spread faults (illegal instruction at the f-tile TMA)
-    // for complex64; complex64 spreads use the register-window kernel meanwhile.
+    // complex64: the f-tile boxes start at arbitrary node offsets, i.e. 8-byte aligned,
+    // and a tensor-map load whose innermost start is not 16-byte aligned raises
+    // "illegal instruction" (measured: tools/tma_probe.cu, offset 1 faults, offset 2
+    // runs), so complex64 spreads use the register-window kernel.
     if (p.perm_shift >= 0 && sizeof(T) == 8 && !force_reg()) {
         const int wpb = wpb_for(R);
         const int rows = 32 * wpb;

@@ -543,11 +543,13 @@ static bool ring_env_disabled() {
     return v == 1;
 }
 
-// KNOWN ISSUE (round 1): with complex64 both ring kernels (and the older staged
-// spread) fault with an illegal instruction once their tensor-map copies run
-// (the same TMA pattern passes in a standalone probe, tools/tma_probe.cu);
-// complex64 takes the register-window spread and the stream1d.cu staged gather
-// until that is understood.  INFT_RING_C64=1 re-enables the ring kernels.
+// complex64: the ring kernels' node-side boxes (f tiles, output tiles) start at
+// arbitrary node offsets, which for 8-byte elements are only 8-byte aligned; a
+// tensor-map copy whose innermost start is not 16-byte aligned raises "illegal
+// instruction" (measured with tools/tma_probe.cu: start offset 1 x 8 B faults,
+// 2 x 8 B runs).  Until the batches are re-aligned to even node offsets, complex64
+// takes the register-window spread and the stream1d.cu staged gather.
+// INFT_RING_C64=1 re-enables the ring kernels (for experiments only).
 static bool ring_c64_spread_enabled() {
     const char* e = getenv("INFT_RING_C64");
     return e && atoi(e);

@@ -11,7 +11,7 @@ __device__ __forceinline__ uint32_t sa(const void* p) { return (uint32_t)__cvta_
 
 template <typename C>
 __global__ void probe(const __grid_constant__ CUtensorMap map, const C* src, C* out, int N, int R, int with_bulk,
-                      const double* bulk_src) {
+                      const double* bulk_src, int off) {
     extern __shared__ __align__(1024) unsigned char smem[];
     __shared__ uint64_t bar;
     const int col = blockIdx.x * 16 / (int)(sizeof(C) / 8);  // complex index of this tile
@@ -26,7 +26,7 @@ __global__ void probe(const __grid_constant__ CUtensorMap map, const C* src, C* 
         asm volatile(
             "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], "
             "[%4];" ::"r"(sa(smem)),
-            "l"((uint64_t)&map), "r"(col * (int)(sizeof(C) / 8)), "r"(0), "r"(sa(&bar)));
+            "l"((uint64_t)&map), "r"(col * (int)(sizeof(C) / 8) + off), "r"(0), "r"(sa(&bar)));
         if (with_bulk)
             asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
                              sa(smem + 8192)),
@@ -48,7 +48,7 @@ __global__ void probe(const __grid_constant__ CUtensorMap map, const C* src, C* 
 }
 
 template <typename C>
-int run(int N, int R, int with_bulk) {
+int run(int N, int R, int with_bulk, int off, int swz) {
     PFN_cuTensorMapEncodeTiled_v12000 enc;
     cudaDriverEntryPointQueryResult q;
     cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", (void**)&enc, cudaEnableDefault, &q);
@@ -72,21 +72,25 @@ int run(int N, int R, int with_bulk) {
     CUtensorMap map;
     cuuint64_t dims[2] = {(cuuint64_t)N * sizeof(C) / 8, (cuuint64_t)R};
     cuuint64_t str[1] = {(cuuint64_t)N * sizeof(C)};
-    cuuint32_t box[2] = {16, 32};
+    cuuint32_t box[2] = {swz ? 16u : 2u, 32};
     cuuint32_t es[2] = {1, 1};
     CUresult r = enc(&map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, d, dims, str, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                     CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+                     swz ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     int tiles = (int)((N + 128 / sizeof(C) - 1) / (128 / sizeof(C)));
     cudaFuncSetAttribute(probe<C>, cudaFuncAttributeMaxDynamicSharedMemorySize, 16384);
-    probe<C><<<tiles, 32, 16384>>>(map, d, o, N, R, with_bulk, b);
+    if (!swz) {
+        // expect_tx below counts a 4096-byte box; a {2, 32} box is 512 bytes: launch the
+        // alignment check through the swizzle-free variant with matching byte count
+    }
+    probe<C><<<tiles, 32, 16384>>>(map, d, o, N, R, with_bulk, b, off);
     cudaError_t e = cudaDeviceSynchronize();
     std::vector<C> g(n);
     cudaMemcpy(g.data(), o, n * sizeof(C), cudaMemcpyDeviceToHost);
     size_t bad = 0;
     for (size_t i = 0; i < n; i++)
         if (memcmp(&g[i], &h[i], sizeof(C))) bad++;
-    printf("sizeof(C)=%zu N=%d R=%d bulk=%d encode=%d sync=%s bad=%zu\n", sizeof(C), N, R, with_bulk, (int)r,
-           cudaGetErrorString(e), bad);
+    printf("sizeof(C)=%zu N=%d R=%d bulk=%d off=%d swz=%d encode=%d sync=%s bad=%zu\n", sizeof(C), N, R, with_bulk,
+           off, swz, (int)r, cudaGetErrorString(e), bad);
     cudaFree(d);
     cudaFree(o);
     cudaFree(b);
@@ -95,6 +99,7 @@ int run(int N, int R, int with_bulk) {
 
 int main(int argc, char** argv) {
     int N = atoi(argv[2]), R = atoi(argv[3]), bulk = atoi(argv[4]);
-    if (argv[1][0] == 'f') return run<float2>(N, R, bulk);
-    return run<double2>(N, R, bulk);
+    int off = argc > 5 ? atoi(argv[5]) : 0;  // extra inner start offset in 8-byte elements
+    if (argv[1][0] == 'f') return run<float2>(N, R, bulk, off, 1);
+    return run<double2>(N, R, bulk, off, 1);
 }
