@@ -3,6 +3,9 @@
 the binding (which refuses to load without the library).
 
     python build_native.py [--force] [--verbose]
+
+Experiments: INFT_NVCC_EXTRA="-DNAME=VALUE ..." adds nvcc flags and INFT_LIB_OUT
+names another output file (load it with INFT_LIB=...).
 """
 import os
 import subprocess
@@ -12,7 +15,8 @@ import time
 ROOT = os.path.dirname(os.path.abspath(__file__))
 HERE = os.path.join(ROOT, "paper_1811_05335_b200")
 CSRC = os.path.join(HERE, "csrc")
-LIB = os.path.join(HERE, "libinft.so")
+LIB = os.environ.get("INFT_LIB_OUT") or os.path.join(HERE, "libinft.so")
+EXTRA = os.environ.get("INFT_NVCC_EXTRA", "").split()
 SOURCES = ["plan.cu", "apply.cu", "stream1d.cu", "stream1d_ring.cu", "fft.cu", "setup.cu"]
 CUDA_HOME = os.environ.get("CUDA_HOME", "/usr/local/cuda")
 NVCC = os.path.join(CUDA_HOME, "bin", "nvcc")
@@ -38,7 +42,7 @@ def up_to_date():
 def build(force=False, verbose=False):
     if not force and up_to_date():
         return LIB
-    objdir = os.path.join(HERE, "build")
+    objdir = os.path.join(HERE, "build" if not EXTRA else "build_" + os.path.basename(LIB).replace(".so", ""))
     os.makedirs(objdir, exist_ok=True)
     objs = []
     procs = []
@@ -46,7 +50,7 @@ def build(force=False, verbose=False):
     for s in SOURCES:
         obj = os.path.join(objdir, s.replace(".cu", ".o"))
         objs.append(obj)
-        cmd = [NVCC, *ARCH, *FLAGS, "-c", os.path.join(CSRC, s), "-o", obj]
+        cmd = [NVCC, *ARCH, *FLAGS, *EXTRA, "-c", os.path.join(CSRC, s), "-o", obj]
         if verbose:
             cmd.insert(1, "-Xptxas=-v")
             print(" ".join(cmd), flush=True)

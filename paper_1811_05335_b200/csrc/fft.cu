@@ -191,28 +191,43 @@ __device__ __forceinline__ void stage_regs(C2<T> (&a)[R], int j, const C2<T>* __
 }
 
 // ------------------------------------------------------------------ CTA transform geometry
+// kRB: radix of the bulk Stockham stages (16: 16 elements per thread, 8: twice the threads
+// per tile at half the registers per thread)
+#ifndef INFT_FFT_RADIX
+#define INFT_FFT_RADIX 16
+#endif
+constexpr int kRB = INFT_FFT_RADIX;
+constexpr int kLgRB = kRB == 16 ? 4 : (kRB == 8 ? 3 : 2);
 // TF independent length-L transforms per tile (compile-time: ~64 KB of shared memory, at
 // most 256 threads = TF L / 16, at most 8), thread t -> (f = t % TF, butterfly j = t / TF).
 // Static radix plan for L = 2^K: a first stage of radix 2^(K mod 4) (if any), then radix-16.
 template <typename T, int L>
 struct Geo {
     static constexpr int TF = L >= 512 ? 4096 / L : 8;
-    static constexpr int NT = TF * L / 16 < 32 ? 32 : TF * L / 16;  // threads per CTA
+    static constexpr int NT = TF * L / kRB < 32 ? 32 : TF * L / kRB;  // threads per CTA
     // row padding of the [f][L + PAD] layout: the lanes of one 128-byte shared wavefront cover
     // TF transforms x (wavefront / TF) consecutive positions
     static constexpr int WAVE = (int)(128 / sizeof(C2<T>));
     static constexpr int PAD = WAVE / TF > 1 ? WAVE / TF : 1;
-    static constexpr int S = L + PAD;
+    static constexpr int ST = L + PAD;  // row stride of pass B's bulk-copied tile rows
     static constexpr int K = __builtin_ctz(L);
-    static constexpr int R0 = 1 << (K % 4);
-    static constexpr int RF = R0 > 1 ? R0 : 16;  // radix of the first stage
-    static constexpr int PER0 = 16 / RF;         // butterflies per thread in the first stage
-    static constexpr int NST = K / 4 + (R0 > 1 ? 1 : 0);
+    static constexpr int R0 = 1 << (K % kLgRB);
+    static constexpr int RF = R0 > 1 ? R0 : kRB;  // radix of the first stage
+    static constexpr int PER0 = kRB / RF;         // butterflies per thread in the first stage
+    static constexpr int NST = K / kLgRB + (R0 > 1 ? 1 : 0);
+    static constexpr int LR = L / kRB;            // span of the last stage = twiddle table size
+    // work buffer rows: position p lives at p + p / SKD with SKD = RF (one skew slot per
+    // first-stage butterfly, so the first stage's strided writes RF j + m spread over the
+    // banks) when one wavefront spans several butterflies of a transform (PAD > 1); row
+    // stride SW = PAD (mod WAVE) like ST
+    static constexpr int SKD = (PAD > 1 && RF >= 4) ? RF : L;  // skew divisor (L: none)
+    static constexpr int SW0 = L + L / SKD;
+    static constexpr int SW = SW0 + ((PAD - SW0 % WAVE) % WAVE + WAVE) % WAVE;
 };
 
 // shared-memory layout of the TF transforms: [f][S]
 template <typename G>
-__device__ __forceinline__ int sidx(int f, int pos) { return f * G::S + pos; }
+__device__ __forceinline__ int sidx(int f, int pos) { return f * G::SW + pos + pos / G::SKD; }
 
 // One stage SI (radix R, span NS) of TF transforms.  LOAD(f, n, p, m) -> element n of
 // transform f (the first stage's butterfly p, leg m of this thread); STORE(f, k, v, m) writes
@@ -221,7 +236,7 @@ __device__ __forceinline__ int sidx(int f, int pos) { return f * G::S + pos; }
 // radix-16 stages use).
 template <typename T, int SIGN, typename G, int R, int NS, int SI, typename Load, typename Store>
 __device__ __forceinline__ void run_stage(const C2<T>* tw, C2<T>* sm, Load&& load, Store&& store) {
-    constexpr int L = G::S - G::PAD;
+    constexpr int L = G::ST - G::PAD;
     constexpr int TF = G::TF;
     constexpr int nbut = L / R;
     constexpr int total = nbut * TF;
@@ -265,7 +280,7 @@ __device__ __forceinline__ void run_stage(const C2<T>* tw, C2<T>* sm, Load&& loa
 template <typename T, int SIGN, typename G, int SI, int NS, typename Load, typename Store>
 __device__ __forceinline__ void fft_stages(const C2<T>* tw, C2<T>* sm, Load&& load, Store&& store) {
     if constexpr (SI < G::NST) {
-        constexpr int R = (SI == 0) ? G::RF : 16;
+        constexpr int R = (SI == 0) ? G::RF : kRB;
         run_stage<T, SIGN, G, R, NS, SI>(tw, sm, load, store);
         fft_stages<T, SIGN, G, SI + 1, NS * R>(tw, sm, load, store);
     }
@@ -278,8 +293,8 @@ __device__ __forceinline__ void cta_fft(const C2<T>* tw, C2<T>* sm, Load&& load,
 
 // byte offset of pass B's deconvolution tile: after tile[2] | work | twiddles, 128-aligned
 template <typename T>
-__host__ __device__ constexpr size_t d_offset(int L, int S, int TB) {
-    return ((sizeof(C2<T>) * (size_t)(3 * S * TB + L / 16)) + 127) / 128 * 128;
+__host__ __device__ constexpr size_t d_offset(int L, int ST, int SW, int TB) {
+    return ((sizeof(C2<T>) * (size_t)(2 * ST * TB + SW * TB + L / kRB)) + 127) / 128 * 128;
 }
 
 // ------------------------------------------------------------------ persistent tiled passes
@@ -303,11 +318,11 @@ __global__ void __launch_bounds__(Geo<T, L>::NT, 1)
     extern __shared__ __align__(128) unsigned char smraw[];
     constexpr int CE = (int)(sizeof(C2<T>) / 8);
     using G = Geo<T, L>;
-    constexpr int TA = G::TF, S = G::S;
+    constexpr int TA = G::TF, S = G::SW;
     C2<T>* tile = reinterpret_cast<C2<T>*>(smraw);
     C2<T>* work = tile + 2 * L * TA;
     C2<T>* tws = work + S * TA;  // stage twiddles, L / 16 entries
-    uint64_t* bars = reinterpret_cast<uint64_t*>(tws + L / 16);
+    uint64_t* bars = reinterpret_cast<uint64_t*>(tws + L / kRB);
     const int N2 = A.N2;
     const int tiles_per_rhs = N2 / TA;
     const int B = (int)(A.M / 2 / N2);  // band rows on each side (MODE 1)
@@ -323,7 +338,7 @@ __global__ void __launch_bounds__(Geo<T, L>::NT, 1)
         mbar_init(&bars[1], 1);
         fence_barrier_init();
     }
-    for (int i = threadIdx.x; i < L / 16; i += blockDim.x) tws[i] = A.tw1[i];
+    for (int i = threadIdx.x; i < L / kRB; i += blockDim.x) tws[i] = A.tw1[i];
     __syncthreads();
     auto issue = [&](int id, int b) {
         const int r = id / tiles_per_rhs, c0 = (id % tiles_per_rhs) * TA * CE;
@@ -344,7 +359,7 @@ __global__ void __launch_bounds__(Geo<T, L>::NT, 1)
         }
     };
     // this thread's single butterfly of the last stage: transform fl, outputs k1 = jl + m L/16
-    const int fl = threadIdx.x % TA, jl = threadIdx.x < TA * (L / 16) ? threadIdx.x / TA : 0;
+    const int fl = threadIdx.x % TA, jl = threadIdx.x < TA * (L / kRB) ? threadIdx.x / TA : 0;
     const int lmask = (1 << A.LB) - 1;
     int it = 0;
     if (threadIdx.x == 0 && (int)blockIdx.x < ntiles) issue(blockIdx.x, 0);
@@ -356,7 +371,7 @@ __global__ void __launch_bounds__(Geo<T, L>::NT, 1)
         // loads independent of the tile data, issued before waiting for it:
         // four-step twiddles w_N^{n2 k1} = w_N^{n2 jl} (w_N^{n2 L/16})^m ...
         const int n2l = col0 + fl;
-        const int e0 = n2l * jl, eq = n2l * (L / 16);
+        const int e0 = n2l * jl, eq = n2l * (L / kRB);
         const C2<T> t0a = twid_g<T, SIGN>(A.tlo, e0 & lmask), t0b = twid_g<T, SIGN>(A.thi, e0 >> A.LB);
         const C2<T> tqa = twid_g<T, SIGN>(A.tlo, eq & lmask), tqb = twid_g<T, SIGN>(A.thi, eq >> A.LB);
         mbar_wait(&bars[b], (it >> 1) & 1);
@@ -390,7 +405,7 @@ __global__ void __launch_bounds__(Geo<T, L>::NT, 1)
     k_pass_b(const __grid_constant__ CUtensorMap dmap, Args<T> A, int BRd, int ntiles) {
     extern __shared__ __align__(128) unsigned char smraw[];
     using G = Geo<T, L>;
-    constexpr int TB = G::TF, S = G::S;
+    constexpr int TB = G::TF, S = G::ST, SW = G::SW;
     // MODE 0: the deconvolution factors of the tile's kept outputs, [2 B2][DW] (rows: k2 in
     // [0, B2), then k2 in [N2 - B2, N2)), fetched by TMA while the first stages run
     constexpr int DW = (int)(16 / sizeof(T)) > TB ? (int)(16 / sizeof(T)) : TB;
@@ -399,8 +414,8 @@ __global__ void __launch_bounds__(Geo<T, L>::NT, 1)
     const int B2 = (int)(half / N1);  // kept k2 rows: [0, B2) and [N2 - B2, N2)
     C2<T>* tile = reinterpret_cast<C2<T>*>(smraw);
     C2<T>* work = tile + 2 * S * TB;
-    C2<T>* tws = work + S * TB;
-    T* dsm = reinterpret_cast<T*>(smraw + d_offset<T>(L, S, TB));
+    C2<T>* tws = work + SW * TB;
+    T* dsm = reinterpret_cast<T*>(smraw + d_offset<T>(L, S, SW, TB));
     uint64_t* bars = reinterpret_cast<uint64_t*>(dsm + (MODE == 0 ? 2 * B2 * DW : 0));
     const int tiles_per_rhs = N1 / TB;
     const C2<T>* src = (MODE == 0) ? A.grid : A.ybuf;
@@ -412,7 +427,7 @@ __global__ void __launch_bounds__(Geo<T, L>::NT, 1)
         mbar_init(&bars[2], 1);
         fence_barrier_init();
     }
-    for (int i = threadIdx.x; i < L / 16; i += blockDim.x) tws[i] = A.tw2[i];
+    for (int i = threadIdx.x; i < L / kRB; i += blockDim.x) tws[i] = A.tw2[i];
     __syncthreads();
     auto issue = [&](int id, int b) {
         const int64_t r = id / tiles_per_rhs;
@@ -446,7 +461,7 @@ __global__ void __launch_bounds__(Geo<T, L>::NT, 1)
         const C2<T>* tl = tile + b * S * TB;
         C2<T>* grow = A.grid + r * A.GS;
         C2<T>* frow = A.fhat + r * A.M;
-        auto load = [&](int f, int n2, int, int) -> C2<T> { return tl[sidx<G>(f, n2)]; };
+        auto load = [&](int f, int n2, int, int) -> C2<T> { return tl[f * S + n2]; };
         auto store = [&](int f, int k2, C2<T> v, int m) {
             const int64_t k = (int64_t)(row0 + f) + (int64_t)N1 * k2;
             if (MODE == 0) {
@@ -502,6 +517,9 @@ static std::map<const Plan*, FftState*>& fft_states() {
     return m;
 }
 
+template <typename T>
+static size_t pass_b_smem(int L, int N1, int64_t M, int mode);
+
 static int split_n1(int64_t N) {
     int lg = 0;
     while ((int64_t(1) << lg) < N) lg++;
@@ -531,14 +549,13 @@ bool fused_fft_available(const Plan& p) {
     }
     // pass B of the inverse stages the tile's d factors: shared memory must fit
     {
-        const int N2i = (int)N2;
-        const int TF = N2i >= 512 ? 4096 / N2i : 8;
-        const size_t cs = p.prec == INFT_C128 ? 16 : 8, ds = cs / 2;
-        const int pad = std::max(1, (int)(128 / cs) / TF);
+        const int64_t B2 = half / split_n1(N);
+        const size_t ds = p.prec == INFT_C128 ? 8 : 4;
+        const int TF = N2 >= 512 ? (int)(4096 / N2) : 8;
         const size_t dw = std::max<size_t>((size_t)TF, 16 / ds);
-        const size_t B2 = (size_t)(half / split_n1(N));
-        const size_t smem = ((cs * (size_t)(3 * (N2i + pad) * TF + N2i / 16)) + 127) / 128 * 128 + ds * 2 * B2 * dw + 32;
-        if (smem > 227 * 1024) return false;
+        const size_t smem = p.prec == INFT_C128 ? pass_b_smem<double>((int)N2, split_n1(N), p.M[0], 0)
+                                                : pass_b_smem<float>((int)N2, split_n1(N), p.M[0], 0);
+        if (smem == 0 || smem > 227 * 1024) return false;
         if (B2 > 256 && B2 % 256) return false;
         if ((B2 * dw * ds) % 128) return false;
     }
@@ -615,8 +632,8 @@ static void pick_L(int mode, PassAFn<T>& a, PassBFn<T>& b) {
 }
 
 template <typename T>
-static bool pick_kernels(int mode, int L, PassAFn<T>& a, PassBFn<T>& b, int& TF, int& S, int& NT) {
-#define INFT_GEO(LL) TF = fft::Geo<T, LL>::TF, S = fft::Geo<T, LL>::S, NT = fft::Geo<T, LL>::NT
+static bool pick_kernels(int mode, int L, PassAFn<T>& a, PassBFn<T>& b, int& TF, int& ST, int& SW, int& NT) {
+#define INFT_GEO(LL) TF = fft::Geo<T, LL>::TF, ST = fft::Geo<T, LL>::ST, SW = fft::Geo<T, LL>::SW, NT = fft::Geo<T, LL>::NT
     switch (L) {
         case 16: pick_L<T, 16>(mode, a, b); INFT_GEO(16); return true;
         case 32: pick_L<T, 32>(mode, a, b); INFT_GEO(32); return true;
@@ -643,6 +660,18 @@ static int num_sms() {
     return n;
 }
 
+// dynamic shared memory of pass B (0: unsupported length)
+template <typename T>
+static size_t pass_b_smem(int L, int N1, int64_t M, int mode) {
+    PassAFn<T> ka = nullptr;
+    PassBFn<T> kb = nullptr;
+    int TB, ST, SW, threads;
+    if (!pick_kernels<T>(mode, L, ka, kb, TB, ST, SW, threads)) return 0;
+    const int B2 = (int)(M / 2 / N1);
+    const int DW = std::max<int>(TB, (int)(16 / sizeof(T)));
+    return fft::d_offset<T>(L, ST, SW, TB) + (mode == 0 ? sizeof(T) * (size_t)(2 * B2 * DW) : 0) + 32;
+}
+
 // pass A over `src` (MODE 0: the grid, rows GS; MODE 1: h, rows M)
 template <typename T>
 static void launch_pass_a(Plan& p, fft::Args<T>& A, int mode, const void* src, int64_t R, cudaStream_t st) {
@@ -651,8 +680,8 @@ static void launch_pass_a(Plan& p, fft::Args<T>& A, int mode, const void* src, i
     const int L = A.N1;
     PassAFn<T> ka = nullptr;
     PassBFn<T> kb = nullptr;
-    int TA, S, threads;
-    if (!pick_kernels<T>(mode, L, ka, kb, TA, S, threads)) {
+    int TA, ST, SW, threads;
+    if (!pick_kernels<T>(mode, L, ka, kb, TA, ST, SW, threads)) {
         set_error("fused FFT: unsupported factor length");
         throw Fail{INFT_ERR_UNSUPPORTED};
     }
@@ -678,7 +707,7 @@ static void launch_pass_a(Plan& p, fft::Args<T>& A, int mode, const void* src, i
         set_error("cuTensorMapEncodeTiled failed (fused FFT pass A)");
         throw Fail{INFT_ERR_CUDA};
     }
-    const size_t smem = cs * (size_t)(2 * L * TA + S * TA + L / 16) + 16;
+    const size_t smem = cs * (size_t)(2 * L * TA + SW * TA + L / fft::kRB) + 16;
     const int ntiles = (int)(R * (A.N2 / TA));
     INFT_CUDA(cudaFuncSetAttribute(ka, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     ka<<<(unsigned)std::min(ntiles, num_sms()), threads, smem, st>>>(map, dmap, A, BR, ntiles);
@@ -692,14 +721,14 @@ static void launch_pass_b(Plan& p, fft::Args<T>& A, int mode, int64_t R, cudaStr
     const int L = A.N2;
     PassAFn<T> ka = nullptr;
     PassBFn<T> kb = nullptr;
-    int TB, S, threads;
-    if (!pick_kernels<T>(mode, L, ka, kb, TB, S, threads)) {
+    int TB, ST, SW, threads;
+    if (!pick_kernels<T>(mode, L, ka, kb, TB, ST, SW, threads)) {
         set_error("fused FFT: unsupported factor length");
         throw Fail{INFT_ERR_UNSUPPORTED};
     }
     const int B2 = (int)(A.M / 2 / A.N1);
     const int DW = std::max<int>(TB, (int)(16 / sizeof(T)));
-    const size_t smem = fft::d_offset<T>(L, S, TB) + (mode == 0 ? sizeof(T) * (size_t)(2 * B2 * DW) : 0) + 32;
+    const size_t smem = pass_b_smem<T>(L, A.N1, A.M, mode);
     CUtensorMap dmap;
     const int BRd = std::min(B2, 256);
     if (mode == 0) {
