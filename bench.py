@@ -62,6 +62,22 @@ def model_bytes_per_rhs(N, M, Ms, P, e, ew, R):
     return inv, adj, spread, gather
 
 
+def ncu_traffic(stage, prec, R):
+    """dram__bytes_read.sum + dram__bytes_write.sum per launch of the stage's kernel, from the
+    committed `ncu --set full` summary of this workload (profiles/ncu_traffic.json, written by
+    tools/ncu_traffic.py); None when the capture does not cover this stage/precision/batch."""
+    path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "ncu_traffic.json")
+    try:
+        with open(path) as fh:
+            t = json.load(fh)
+    except (OSError, ValueError):
+        return None, None
+    if t.get("prec") != prec or int(t.get("rhs", -1)) != int(R):
+        return None, None
+    k = t.get("stages", {}).get(stage)
+    return (k["dram_bytes"], t.get("source")) if k else (None, None)
+
+
 class ClockSampler:
     """nvidia-smi clocks / throttle reasons sampled DURING the timed region."""
 
@@ -293,17 +309,23 @@ def main():
 
     # ---------------------------------------------------------------- roofline of the dominant kernel
     inv_b, adj_b, spread_b, gather_b = model_bytes_per_rhs(N, M, Ms, info["P"], e, ew, R)
+    # per-kernel algorithmic bytes: each kernel reads its input and
+    # writes its output once; on the fused path pass B of the inverse reads the whole grid
+    # (e Ms) and writes the kept band (e M), pass A of the adjoint reads h and writes the grid
+    fused = bool(info.get("fused_fft"))
     stage_bytes = {"spread": spread_b * R, "gather": gather_b * R,
                    "fft_forward": 2 * e * Ms * R, "fft_inverse": 2 * e * Ms * R,
-                   "trunc_deconv": 2 * e * M * R, "deconv_pad": e * (M + Ms) * R}
+                   "trunc_deconv": (e * (Ms + M) if fused else 2 * e * M) * R, "deconv_pad": e * (M + Ms) * R}
     stage_ms = {k: (v[0] / v[1] if v[1] else None) for k, v in prof.items()}
     dom = max((k for k in stage_ms if stage_ms[k]), key=lambda k: prof[k][0])
     peak, peak_kind = measured_peak_hbm()
     achieved = stage_bytes[dom] / (stage_ms[dom] / 1e3) / 1e9
     apply_gbs = (inv_b + adj_b) * R / (ms_step / 1e3) / 1e9
+    traffic, traffic_src = ncu_traffic(dom, args.prec, R)
     roofline = {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak, "unit": "GB/s",
-                "frac": achieved / peak, "traffic": None, "peak_source": peak_kind + " (MEASURED_PEAKS.json hbm_gbs)",
-                "bytes_per_launch": stage_bytes[dom], "ms_per_launch": stage_ms[dom]}
+                "frac": achieved / peak, "traffic": traffic, "peak_source": peak_kind + " (MEASURED_PEAKS.json hbm_gbs)",
+                "bytes_per_launch": stage_bytes[dom], "ms_per_launch": stage_ms[dom],
+                "traffic_source": traffic_src, "fused_fft": fused}
     stages = {k: {"ms_per_launch": stage_ms[k], "launches": prof[k][1],
                   "gbs": (stage_bytes[k] / (stage_ms[k] / 1e3) / 1e9) if stage_ms[k] else None,
                   "share_of_step": (prof[k][0] / ms_total) if ms_total else None} for k in stage_ms}

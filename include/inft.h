@@ -162,9 +162,15 @@ inft_status inft_get_info(inft_plan_t plan, inft_info* info);
 
 /* Per-stage device time of the apply, measured with CUDA events recorded on
  * the launching stream around every stage of every apply while profiling is
- * enabled (stages: 0 spread a2, 1 FFT a3, 2 truncate+deconvolve a4,
- * 3 deconvolve+pad a5, 4 FFT a6, 5 gather a7).  inft_get_profile synchronises
- * with the recorded events; reset != 0 clears the accumulators. */
+ * enabled.  Stages (one kernel each on the fused 1-D path, info.fused_fft = 1):
+ *   0 spread a2;
+ *   1 FFT a3 (unfused: cuFFT; fused: pass A, column FFTs + four-step twiddles);
+ *   2 truncate+deconvolve a4 (fused: pass B, row FFTs + a4);
+ *   3 deconvolve+pad a5 (fused: pass A, a5 + column FFTs);
+ *   4 FFT a6 (unfused: cuFFT; fused: pass B, row FFTs + grid halo);
+ *   5 gather a7.
+ * inft_get_profile synchronises with the recorded events; reset != 0 clears
+ * the accumulators. */
 typedef struct {
     double ms[6];
     int64_t count[6];

@@ -367,8 +367,12 @@ static void inverse_chunk(Plan& p, const void* f, void* fhat, int64_t Rc, cudaSt
         spread<T>(p, static_cast<const C2<T>*>(f), g, Rc, st);
     }
     if (use_fused(p)) {  // a3 + a4 in two fused passes (fft.cu)
-        StageTimer t(p, 1, st);
-        fused_fft_inverse(p, g, fhat, Rc, st);
+        {
+            StageTimer t(p, 1, st);  // pass A: column FFTs + four-step twiddles (in place)
+            fused_fft_inverse(p, g, fhat, Rc, st, 1);
+        }
+        StageTimer t(p, 2, st);  // pass B: row FFTs + truncation + deconvolution
+        fused_fft_inverse(p, g, fhat, Rc, st, 2);
         return;
     }
     {
@@ -394,8 +398,12 @@ static void adjoint_chunk(Plan& p, const void* h, void* f, int64_t Rc, cudaStrea
     // need a 16-byte aligned base
     if (use_fused(p) && (reinterpret_cast<uintptr_t>(h) & 15) == 0) {
         {
-            StageTimer t(p, 4, st);
-            fused_fft_adjoint(p, h, g, Rc, st);
+            StageTimer t(p, 3, st);  // pass A: deconvolution + zero pad + column FFTs
+            fused_fft_adjoint(p, h, g, Rc, st, 1);
+        }
+        {
+            StageTimer t(p, 4, st);  // pass B: row FFTs, natural-order grid + halo
+            fused_fft_adjoint(p, h, g, Rc, st, 2);
         }
         StageTimer t(p, 5, st);
         gather<T>(p, g, static_cast<C2<T>*>(f), Rc, st);

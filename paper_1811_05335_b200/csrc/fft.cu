@@ -757,19 +757,19 @@ const float* dtab_for<float>(const Plan& p) { return p.dkf.as<float>(); }
 
 // inverse: grid (spread output, rows GS) -> fhat  (F^* then truncate, times d)
 template <typename T>
-static void fused_inverse_t(Plan& p, void* grid, void* fhat, int64_t R, cudaStream_t st) {
+static void fused_inverse_t(Plan& p, void* grid, void* fhat, int64_t R, cudaStream_t st, int part) {
     FftState& s = fft_state<T>(p, st);
     fft::Args<T> A = make_args<T>(p, s);
     A.grid = static_cast<C2<T>*>(grid);
     A.fhat = static_cast<C2<T>*>(fhat);
     A.dk = dtab_for<T>(p);
-    launch_pass_a<T>(p, A, 0, grid, R, st);
-    launch_pass_b<T>(p, A, 0, R, st);
+    if (part & 1) launch_pass_a<T>(p, A, 0, grid, R, st);
+    if (part & 2) launch_pass_b<T>(p, A, 0, R, st);
 }
 
 // adjoint: h -> grid (D, zero pad, F), natural order with halo
 template <typename T>
-static void fused_adjoint_t(Plan& p, const void* h, void* grid, int64_t R, cudaStream_t st) {
+static void fused_adjoint_t(Plan& p, const void* h, void* grid, int64_t R, cudaStream_t st, int part) {
     FftState& s = fft_state<T>(p, st);
     if (s.y_rhs < R) {
         s.ybuf.alloc(sizeof(C2<T>) * (size_t)p.Ms[0] * R);
@@ -780,22 +780,22 @@ static void fused_adjoint_t(Plan& p, const void* h, void* grid, int64_t R, cudaS
     A.ybuf = s.ybuf.as<C2<T>>();
     A.hin = static_cast<const C2<T>*>(h);
     A.dk = dtab_for<T>(p);
-    launch_pass_a<T>(p, A, 1, h, R, st);
-    launch_pass_b<T>(p, A, 1, R, st);
+    if (part & 1) launch_pass_a<T>(p, A, 1, h, R, st);
+    if (part & 2) launch_pass_b<T>(p, A, 1, R, st);
 }
 
-void fused_fft_inverse(Plan& p, void* grid, void* fhat, int64_t R, cudaStream_t st) {
+void fused_fft_inverse(Plan& p, void* grid, void* fhat, int64_t R, cudaStream_t st, int part) {
     if (p.prec == INFT_C128)
-        fused_inverse_t<double>(p, grid, fhat, R, st);
+        fused_inverse_t<double>(p, grid, fhat, R, st, part);
     else
-        fused_inverse_t<float>(p, grid, fhat, R, st);
+        fused_inverse_t<float>(p, grid, fhat, R, st, part);
 }
 
-void fused_fft_adjoint(Plan& p, const void* h, void* grid, int64_t R, cudaStream_t st) {
+void fused_fft_adjoint(Plan& p, const void* h, void* grid, int64_t R, cudaStream_t st, int part) {
     if (p.prec == INFT_C128)
-        fused_adjoint_t<double>(p, h, grid, R, st);
+        fused_adjoint_t<double>(p, h, grid, R, st, part);
     else
-        fused_adjoint_t<float>(p, h, grid, R, st);
+        fused_adjoint_t<float>(p, h, grid, R, st, part);
 }
 
 }  // namespace inft

@@ -176,8 +176,9 @@ void spread_ring(Plan& p, const void* f, void* grid, int64_t R, cudaStream_t st)
 void gather_ring(Plan& p, const void* grid, void* f, int64_t R, cudaStream_t st);
 // fft.cu
 bool fused_fft_available(const Plan& p);
-void fused_fft_inverse(Plan& p, void* grid, void* fhat, int64_t R, cudaStream_t st);
-void fused_fft_adjoint(Plan& p, const void* h, void* grid, int64_t R, cudaStream_t st);
+// part: 1 = pass A (columns), 2 = pass B (rows), 3 = both
+void fused_fft_inverse(Plan& p, void* grid, void* fhat, int64_t R, cudaStream_t st, int part = 3);
+void fused_fft_adjoint(Plan& p, const void* h, void* grid, int64_t R, cudaStream_t st, int part = 3);
 void release_fft_state(const Plan* p);
 // setup.cu
 void precompute(Plan& p, inft_method method, inft_weights wt, double tau, cudaStream_t st);
