@@ -459,7 +459,14 @@ static void run(Plan& p, const void* in, size_t in_rhs_bytes, void* out, size_t 
     }
     ensure_streams(p);
     size_t per = std::max(in_dev ? 0 : in_rhs_bytes, out_dev ? 0 : out_rhs_bytes);
-    int64_t Rh = std::max<int64_t>(1, std::min<int64_t>(R, (int64_t)(((size_t)256 << 20) / std::max<size_t>(per, 1))));
+    // chunks of ~stage_mb MB (INFT_STAGE_MB, default 256; e2e step on config 5: 256 MB 80.7 ms,
+    // 64 MB 82.0 ms, 32 MB 87.6 ms -- per-chunk costs outweigh the shorter pipeline fill/drain)
+    static const size_t stage_mb = [] {
+        const char* e = getenv("INFT_STAGE_MB");
+        const long v = e ? atol(e) : 256;
+        return (size_t)(v > 0 ? v : 256);
+    }();
+    int64_t Rh = std::max<int64_t>(1, std::min<int64_t>(R, (int64_t)((stage_mb << 20) / std::max<size_t>(per, 1))));
     Rh = grid_capacity(p, Rh);
     if (!in_dev && p.stage_in_bytes < in_rhs_bytes * Rh) {
         for (int i = 0; i < 2; i++) p.stage_in[i].alloc(in_rhs_bytes * Rh);
