@@ -94,6 +94,7 @@ typedef struct {
     int32_t perm_identity;     /* 1 if the bin sort left the caller's node order unchanged */
     int32_t fast_path;         /* 1 if the register-window spread/gather kernels are used */
     int32_t fused_fft;         /* 1 if the fused two-pass FFT (with deconvolution) replaces cuFFT */
+    int32_t max_lowrank_rank;  /* Alg. 2: largest pivoted-Cholesky rank among columns with |I(l)| > 64 */
     size_t workspace_bytes;    /* device bytes currently owned by the plan */
 } inft_info;
 

@@ -42,7 +42,7 @@ class InftInfo(ctypes.Structure):
                 ("scale", ctypes.c_double), ("tau", ctypes.c_double), ("n_rank_deficient", ctypes.c_int64),
                 ("n_empty_cols", ctypes.c_int64), ("max_col_size", ctypes.c_int64), ("max_abs_w", ctypes.c_double),
                 ("perm_identity", ctypes.c_int32), ("fast_path", ctypes.c_int32), ("fused_fft", ctypes.c_int32),
-                ("workspace_bytes", ctypes.c_size_t)]
+                ("max_lowrank_rank", ctypes.c_int32), ("workspace_bytes", ctypes.c_size_t)]
 
 
 class InftProfile(ctypes.Structure):

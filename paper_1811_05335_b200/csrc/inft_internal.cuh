@@ -97,7 +97,7 @@ struct Plan {
     inft_weights wt = INFT_WEIGHTS_REAL;
     double scale = 1.0;
     double tau = 1e-6;
-    int64_t n_rank_deficient = 0, n_empty_cols = 0, max_col_size = 0;
+    int64_t n_rank_deficient = 0, n_empty_cols = 0, max_col_size = 0, max_lowrank_rank = 0;
     double max_abs_w = 0.0;
 
     // device arrays (plan-owned)

@@ -21,6 +21,7 @@
 // eigenvalues below tau^2 lambda_max are dropped (tau on singular values).
 // INFT_PLAIN_NFFT -- the window matrix B (eq. matrix_B), KB window (reading A7).
 #include <algorithm>
+#include <cstdio>
 #include <cmath>
 #include <vector>
 
@@ -231,6 +232,12 @@ __device__ __forceinline__ double rhs_entry(const GramCtx& g, int64_t a, int64_t
 // by the eigenvectors (columns).  Rotation (Golub-Van Loan, symmetric Schur):
 // tau = (a_qq - a_pp)/(2 a_pq), t = sign(tau)/(|tau| + sqrt(1 + tau^2)),
 // c = 1/sqrt(1 + t^2), s = t c; A <- J^T A J with J_pp = J_qq = c, J_pq = s, J_qp = -s.
+// sweep statistics (INFT_SETUP_DEBUG=1 prints them after Alg. 2): total sweeps, calls, max
+__device__ unsigned long long g_jac_stats[3];
+// large-column solver phase cycles (thread 0 of each CTA): collect+sort, diag, pivoted
+// Cholesky, C = L^T L, Jacobi, back-substitution
+__device__ unsigned long long g_lr_cycles[6];
+
 __device__ void jacobi_eig(double* A, double* V, int n, int ld, double* cs, int* pq, int* flag) {
     const int tid = threadIdx.x, nt = blockDim.x;
     const int np = (n + 1) & ~1;
@@ -243,7 +250,11 @@ __device__ void jacobi_eig(double* A, double* V, int n, int ld, double* cs, int*
     if (tid == 0) {
         double mx = 0.0;
         for (int i = 0; i < n; i++) mx = fmax(mx, fabs(A[i * ld + i]));
-        s_tol = 1e-17 * mx;
+        // off-diagonal entries below 1e-15 of the largest diagonal entry are rounding noise
+        // (two-sided rotations cannot push the entries next to a large diagonal entry lower);
+        // they move eigenvalues by at most that much (Weyl), i.e. within the min-norm cutoff's
+        // tau^2 lambda_max = 1e-12 lambda_max by a factor 1e-3
+        s_tol = 1e-15 * mx;
     }
     __syncthreads();
     const double tol = s_tol;
@@ -302,7 +313,160 @@ __device__ void jacobi_eig(double* A, double* V, int n, int ld, double* cs, int*
             }
             __syncthreads();
         }
+        if (*flag == 0) {
+            if (tid == 0) {
+                atomicAdd(&g_jac_stats[0], (unsigned long long)(sweep + 1));
+                atomicAdd(&g_jac_stats[1], 1ull);
+                atomicMax(&g_jac_stats[2], (unsigned long long)(sweep + 1));
+            }
+            break;
+        }
+        __syncthreads();
+        if (sweep == 59 && tid == 0) {
+            atomicAdd(&g_jac_stats[0], 60ull);
+            atomicAdd(&g_jac_stats[1], 1ull);
+            atomicMax(&g_jac_stats[2], 60ull);
+        }
+    }
+}
+
+// Jacobi for the large-column solver, without eigenvectors: the rotations are (a) applied to the
+// vector t on the fly (t <- J^T t, so t ends as V^T t) and (b) logged per round in `log`
+// ([round][np] (c, s) pairs, at most max_rounds rounds) so that V u can be formed afterwards
+// (jacobi_apply_v).  Returns the number of logged rounds.
+// Storage: A holds the upper triangle of an
+// np x np symmetric matrix (np = n rounded up to even; the pad row/column is zero), element
+// (i, j), i <= j, at pidx(i, j).  One round applies all disjoint rotations of the round-robin
+// ordering at once, A <- J^T A J, as independent 2 x 2 block updates: for rotation pairs
+// (p, q) and (p', q') the block A[{p, q}][{p', q'}] becomes R^T B R' with R = [[c, s], [-s, c]]
+// (the same rotation as jacobi_eig).  One read and one write per element and one barrier per
+// round, so the k x k problem of a big column fits shared memory in packed form (k <= 230).
+__device__ __forceinline__ int pidx(int i, int j, int np) {
+    if (i > j) {
+        const int t = i;
+        i = j;
+        j = t;
+    }
+    return i * np - (i * (i - 1)) / 2 + (j - i);
+}
+
+__host__ __device__ inline size_t packed_doubles(int n) {
+    const size_t np = (size_t)((n + 1) & ~1);
+    return np * (np + 1) / 2;
+}
+
+__device__ int jacobi_packed_log(double* A, int n, double* t, double* log, int max_rounds, double* cs, int* pq,
+                                 int* flag) {
+    const int tid = threadIdx.x, nt = blockDim.x;
+    const int lane = tid & 31, warp = tid >> 5, nw = nt >> 5;
+    const int np = (n + 1) & ~1;
+    const int half = np / 2;
+    __shared__ double s_tol;
+    if (tid == 0) {
+        double mx = 0.0;
+        for (int i = 0; i < n; i++) mx = fmax(mx, fabs(A[pidx(i, i, np)]));
+        s_tol = 1e-15 * mx;  // as jacobi_eig
+    }
+    __syncthreads();
+    const double tol = s_tol;
+    int g = 0, sweeps = 0;
+    for (int sweep = 0; g + np - 1 <= max_rounds; sweep++) {
+        if (tid == 0) *flag = 0;
+        __syncthreads();
+        for (int r = 0; r < np - 1; r++, g++) {
+            for (int k = tid; k < half; k += nt) {
+                int pa = k == 0 ? 0 : ((k - 1 + r) % (np - 1)) + 1;
+                int kb = np - 1 - k;
+                int pb = ((kb - 1 + r) % (np - 1)) + 1;
+                int p = min(pa, pb), q = max(pa, pb);
+                double c = 1.0, s = 0.0;
+                if (q < n) {
+                    double apq = A[pidx(p, q, np)];
+                    if (fabs(apq) > tol) {
+                        double app = A[pidx(p, p, np)], aqq = A[pidx(q, q, np)];
+                        double tau = (aqq - app) / (2.0 * apq);
+                        double tt = (tau >= 0 ? 1.0 : -1.0) / (fabs(tau) + sqrt(1.0 + tau * tau));
+                        c = 1.0 / sqrt(1.0 + tt * tt);
+                        s = tt * c;
+                        *flag = 1;
+                        const double a = t[p], b = t[q];
+                        t[p] = c * a - s * b;
+                        t[q] = s * a + c * b;
+                    }
+                }
+                cs[2 * k] = c;
+                cs[2 * k + 1] = s;
+                pq[2 * k] = p;
+                pq[2 * k + 1] = q;
+                log[(size_t)g * np + 2 * k] = c;
+                log[(size_t)g * np + 2 * k + 1] = s;
+            }
+            __syncthreads();
+            for (int a = warp; a < half; a += nw) {
+                const double ca = cs[2 * a], sa = cs[2 * a + 1];
+                const int p = pq[2 * a], q = pq[2 * a + 1];
+                for (int b = a + lane; b < half; b += 32) {
+                    const double cb = cs[2 * b], sb = cs[2 * b + 1];
+                    if (sa == 0.0 && sb == 0.0) continue;
+                    const int p2 = pq[2 * b], q2 = pq[2 * b + 1];
+                    if (b == a) {  // diagonal block [[app, apq], [apq, aqq]]
+                        const int ipp = pidx(p, p, np), ipq = pidx(p, q, np), iqq = pidx(q, q, np);
+                        const double app = A[ipp], apq = A[ipq], aqq = A[iqq];
+                        // R^T M R with R = [[c, s], [-s, c]]
+                        const double m00 = ca * app - sa * apq, m01 = ca * apq - sa * aqq;
+                        const double m10 = sa * app + ca * apq, m11 = sa * apq + ca * aqq;
+                        A[ipp] = ca * m00 - sa * m01;
+                        A[ipq] = sa * m00 + ca * m01;
+                        A[iqq] = sa * m10 + ca * m11;
+                    } else {
+                        const int i00 = pidx(p, p2, np), i01 = pidx(p, q2, np), i10 = pidx(q, p2, np),
+                                  i11 = pidx(q, q2, np);
+                        const double x00 = A[i00], x01 = A[i01], x10 = A[i10], x11 = A[i11];
+                        // rows: R_a^T; columns: R_b
+                        const double y00 = ca * x00 - sa * x10, y01 = ca * x01 - sa * x11;
+                        const double y10 = sa * x00 + ca * x10, y11 = sa * x01 + ca * x11;
+                        A[i00] = cb * y00 - sb * y01;
+                        A[i01] = sb * y00 + cb * y01;
+                        A[i10] = cb * y10 - sb * y11;
+                        A[i11] = sb * y10 + cb * y11;
+                    }
+                }
+            }
+            __syncthreads();
+        }
+        sweeps = sweep + 1;
         if (*flag == 0) break;
+        __syncthreads();
+    }
+    if (tid == 0) {
+        atomicAdd(&g_jac_stats[0], (unsigned long long)sweeps);
+        atomicAdd(&g_jac_stats[1], 1ull);
+        atomicMax(&g_jac_stats[2], (unsigned long long)sweeps);
+    }
+    __syncthreads();
+    return g;
+}
+
+// v <- V v for the V of jacobi_packed_log (V = J_1 J_2 ... J_G, the rounds' rotations in
+// order): rounds applied in reverse order.
+__device__ void jacobi_apply_v(double* v, int n, const double* log, int rounds) {
+    const int tid = threadIdx.x, nt = blockDim.x;
+    const int np = (n + 1) & ~1;
+    const int half = np / 2;
+    for (int g = rounds - 1; g >= 0; g--) {
+        const int r = g % (np - 1);
+        for (int k = tid; k < half; k += nt) {
+            const double s = log[(size_t)g * np + 2 * k + 1];
+            if (s == 0.0) continue;
+            const double c = log[(size_t)g * np + 2 * k];
+            int pa = k == 0 ? 0 : ((k - 1 + r) % (np - 1)) + 1;
+            int kb = np - 1 - k;
+            int pb = ((kb - 1 + r) % (np - 1)) + 1;
+            int p = min(pa, pb), q = max(pa, pb);
+            const double a = v[p], b = v[q];
+            v[p] = c * a + s * b;
+            v[q] = -s * a + c * b;
+        }
         __syncthreads();
     }
 }
@@ -407,6 +571,241 @@ __global__ void k_alg2_solve(ColCtx cc, GramCtx gc, const int64_t* __restrict__ 
         for (int a = threadIdx.x; a < nc; a += blockDim.x) w64[li[a] * P + lt[a]] = b[a];
         if (threadIdx.x == 0 && dropped > 0) atomicAdd(ndrop, 1ull);
         __syncthreads();
+    }
+}
+
+// ------------------------------------------------------------------ Alg. 2, large columns
+// Block-wide argmax over v[0, n) (ties -> smallest index); every thread gets the result.
+__device__ void block_argmax(const double* v, int n, double& vmax, int& imax, double* rv, int* ri) {
+    double bv = -1.0;
+    int bi = 0x7fffffff;
+    for (int i = threadIdx.x; i < n; i += blockDim.x) {
+        const double x = v[i];
+        if (x > bv) {
+            bv = x;
+            bi = i;
+        }
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+        const double ov = __shfl_down_sync(0xffffffffu, bv, o);
+        const int oi = __shfl_down_sync(0xffffffffu, bi, o);
+        if (ov > bv || (ov == bv && oi < bi)) {
+            bv = ov;
+            bi = oi;
+        }
+    }
+    const int warp = threadIdx.x >> 5, nw = (blockDim.x + 31) >> 5;
+    __syncthreads();
+    if ((threadIdx.x & 31) == 0) {
+        rv[warp] = bv;
+        ri[warp] = bi;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        for (int w = 1; w < nw; w++)
+            if (rv[w] > rv[0] || (rv[w] == rv[0] && ri[w] < ri[0])) {
+                rv[0] = rv[w];
+                ri[0] = ri[w];
+            }
+    }
+    __syncthreads();
+    vmax = rv[0];
+    imax = ri[0];
+    __syncthreads();
+}
+
+// Large columns (|I(l)| > 64).  The Gram matrix G of a big column has a small numerical rank
+// (config 4: n = 3528 unknowns, rank ~180-250 above 1e-15 of its diagonal), so instead of an
+// O(n^3) eigensolve per column:
+//   1. pivoted Cholesky G ~ L L^T (L: n x r, greedy largest-residual-diagonal pivots, columns of G
+//      evaluated on demand, stop when every residual diagonal <= rel * max diag(G): far below the
+//      tau^2 lambda_max cutoff since lambda_max >= max diag);
+//   2. the r x r eigenproblem C = L^T L = W Lambda W^T (Jacobi; its nonzero eigenvalues are those of
+//      L L^T), then the same min-norm cut as the small columns:
+//      b = L W Lambda^{-2} W^T L^T y over lambda > tau^2 lambda_max  (= V Lambda^{-1} V^T y).
+// Unknowns are put in canonical (i, t) order by rank counting (deterministic result).
+struct LrScratch {
+    double *L, *dg, *y, *C, *log, *z, *u;
+    int64_t* li;
+    int* lt;
+    int64_t* li0;
+    int* lt0;
+};
+
+constexpr int kLrSweeps = 24;  // rotation-log capacity in sweeps (config 4: <= 15 needed)
+
+__host__ __device__ inline size_t lr_log_doubles(int rmax) { return (size_t)kLrSweeps * (rmax + 1) * (rmax + 2); }
+
+__device__ LrScratch lr_slices(double* base, int nmax, int rmax) {
+    LrScratch S;
+    S.L = base;
+    S.dg = S.L + (size_t)rmax * nmax;
+    S.y = S.dg + nmax;
+    S.C = S.y + nmax;
+    S.log = S.C + (size_t)rmax * (rmax + 1);
+    S.z = S.log + lr_log_doubles(rmax);
+    S.u = S.z + rmax;
+    S.li = reinterpret_cast<int64_t*>(S.u + rmax);
+    S.li0 = S.li + nmax;
+    S.lt = reinterpret_cast<int*>(S.li0 + nmax);
+    S.lt0 = S.lt + nmax;
+    return S;
+}
+
+__host__ __device__ inline size_t lr_scratch_doubles(int nmax, int rmax) {
+    return (size_t)rmax * nmax + 2 * (size_t)nmax + (size_t)rmax * (rmax + 1) + lr_log_doubles(rmax) +
+           2 * (size_t)rmax + 2 * (size_t)nmax /* li, li0 */ + (size_t)nmax /* lt, lt0 */ + 8;
+}
+
+__global__ void __launch_bounds__(256) k_alg2_solve_lr(ColCtx cc, GramCtx gc, const int64_t* __restrict__ cols,
+                                                       int64_t ncols, const int32_t* __restrict__ cnt, int nmax,
+                                                       int rmax, int ksm, double* __restrict__ scratch, double tau2,
+                                                       double rel, int P, double* __restrict__ w64,
+                                                       unsigned long long* __restrict__ ndrop,
+                                                       int* __restrict__ rank_max) {
+    __shared__ double rv[32];
+    __shared__ int ri[32];
+    __shared__ int cntr;
+    // dynamic: packed C for k <= ksm, then the rotation lists cs[rmax + 2], pq[rmax + 2]
+    extern __shared__ double smx[];
+    double* Csm = smx;
+    double* cs = Csm + packed_doubles(ksm);
+    int* pq = reinterpret_cast<int*>(cs + rmax + 2);
+    LrScratch S = lr_slices(scratch + (size_t)blockIdx.x * lr_scratch_doubles(nmax, rmax), nmax, rmax);
+    const int tid = threadIdx.x, nt = blockDim.x;
+    const int lane = tid & 31, warp = tid >> 5, nw = nt >> 5;
+    for (int64_t ci = blockIdx.x; ci < ncols; ci += gridDim.x) {
+        const int64_t n = cols[ci];
+        const int nc = min(cnt[n], nmax);
+        long long tph = clock64();
+        auto phase = [&](int w) {
+            if (tid == 0) {
+                const long long now = clock64();
+                atomicAdd(&g_lr_cycles[w], (unsigned long long)(now - tph));
+                tph = now;
+            }
+        };
+        if (tid == 0) cntr = 0;
+        __syncthreads();
+        for_column(cc, n, tid, nt, [&](int64_t i, int64_t t) {
+            const int k = atomicAdd(&cntr, 1);
+            if (k < nmax) {
+                S.li0[k] = i;
+                S.lt0[k] = (int)t;
+            }
+        });
+        __syncthreads();
+        // canonical order: position = number of smaller (i, t) keys (keys are distinct)
+        for (int a = tid; a < nc; a += nt) {
+            const int64_t ia = S.li0[a];
+            const int ta = S.lt0[a];
+            int r = 0;
+            for (int c = 0; c < nc; c++) {
+                const int64_t ic = S.li0[c];
+                r += (ic < ia) || (ic == ia && S.lt0[c] < ta);
+            }
+            S.li[r] = ia;
+            S.lt[r] = ta;
+        }
+        __syncthreads();
+        phase(0);
+        for (int a = tid; a < nc; a += nt) {
+            S.dg[a] = gram_entry(gc, S.li[a], S.li[a]);
+            S.y[a] = rhs_entry(gc, S.li[a], n);
+        }
+        __syncthreads();
+        double c0;
+        int ignore;
+        block_argmax(S.dg, nc, c0, ignore, rv, ri);
+        phase(1);
+        // 1. pivoted Cholesky
+        int k = 0;
+        while (k < rmax) {
+            double v;
+            int piv;
+            block_argmax(S.dg, nc, v, piv, rv, ri);
+            if (!(v > rel * c0)) break;
+            const double sq = sqrt(v);
+            const int64_t lp = S.li[piv];
+            double* Lk = S.L + (size_t)k * nmax;
+            for (int i = tid; i < nc; i += nt) {
+                double acc = 0.0;
+                for (int j = 0; j < k; j++) acc = fma(S.L[(size_t)j * nmax + i], S.L[(size_t)j * nmax + piv], acc);
+                Lk[i] = (gram_entry(gc, S.li[i], lp) - acc) / sq;
+            }
+            __syncthreads();
+            for (int i = tid; i < nc; i += nt) S.dg[i] = (i == piv) ? 0.0 : S.dg[i] - Lk[i] * Lk[i];
+            __syncthreads();
+            k++;
+        }
+        phase(2);
+        // 2. C = L^T L (k x k, packed upper triangle; shared memory when it fits) and z = L^T y:
+        //    one warp per entry, lanes over the unknowns
+        double* C = k <= ksm ? Csm : S.C;
+        const int npk = (k + 1) & ~1;
+        for (size_t e = tid; e < packed_doubles(k); e += nt) C[e] = 0.0;
+        __syncthreads();
+        for (int e = warp; e < k * (k + 1) / 2 + k; e += nw) {
+            int a, c;
+            const double* vb;
+            if (e < k * (k + 1) / 2) {
+                a = (int)((sqrt(8.0 * e + 1.0) - 1.0) * 0.5);
+                while ((a + 1) * (a + 2) / 2 <= e) a++;
+                while (a * (a + 1) / 2 > e) a--;
+                c = e - a * (a + 1) / 2;  // c <= a
+                vb = S.L + (size_t)c * nmax;
+            } else {
+                a = e - k * (k + 1) / 2;
+                c = -1;
+                vb = S.y;
+            }
+            const double* va = S.L + (size_t)a * nmax;
+            double acc = 0.0;
+            for (int i = lane; i < nc; i += 32) acc = fma(va[i], vb[i], acc);
+            for (int o = 16; o > 0; o >>= 1) acc += __shfl_down_sync(0xffffffffu, acc, o);
+            if (lane == 0) {
+                if (c >= 0)
+                    C[pidx(c, a, npk)] = acc;
+                else
+                    S.z[a] = acc;
+            }
+        }
+        __syncthreads();
+        int dropped = nc - k;
+        phase(3);
+        if (k > 0) {
+            // 3. eigenvalues of C; z <- W^T z on the fly, rotations logged for W u
+            const int rounds = jacobi_packed_log(C, k, S.z, S.log, kLrSweeps * (k + 1), cs, pq, &cntr);
+            if (tid == 0) {
+                double mx = 0.0;
+                int dr = 0;
+                for (int a = 0; a < k; a++) mx = fmax(mx, C[pidx(a, a, npk)]);
+                for (int a = 0; a < k; a++) dr += !(C[pidx(a, a, npk)] > tau2 * mx && mx > 0.0);
+                rv[0] = mx;
+                cntr = dr;
+            }
+            __syncthreads();
+            const double cut = tau2 * rv[0];
+            for (int a = tid; a < k; a += nt) {
+                const double lam = C[pidx(a, a, npk)];
+                S.u[a] = (lam > cut && rv[0] > 0.0) ? S.z[a] / (lam * lam) : 0.0;
+            }
+            dropped += cntr;
+            __syncthreads();
+            jacobi_apply_v(S.u, k, S.log, rounds);  // u <- W u
+        }
+        phase(4);
+        for (int i = tid; i < nc; i += nt) {
+            double b = 0.0;
+            for (int a = 0; a < k; a++) b = fma(S.L[(size_t)a * nmax + i], S.u[a], b);
+            w64[S.li[i] * P + S.lt[i]] = b;
+        }
+        if (tid == 0) {
+            if (dropped > 0) atomicAdd(ndrop, 1ull);
+            atomicMax(rank_max, k);
+        }
+        __syncthreads();
+        phase(5);
     }
 }
 
@@ -647,8 +1046,36 @@ static void alg2(Plan& p, double tau, DevBuf& w64, cudaStream_t st) {
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
     const int limits[3] = {32, 64, (int)mx};
     const int threads[3] = {32, 128, 256};
+    DevBuf rank_max;
+    rank_max.alloc(sizeof(int));
+    INFT_CUDA(cudaMemsetAsync(rank_max.p, 0, sizeof(int), st));
     for (int k = 0; k < 3; k++) {
         if (cls[k].empty()) continue;
+        if (k == 2) {  // large columns: pivoted Cholesky + small eigenproblem (k_alg2_solve_lr)
+            const int nmax = (int)mx;
+            const int rmax = std::min(nmax, 384);
+            const int ksm = std::min(rmax, 231);  // packed C in shared memory up to k = 231 (216 KB)
+            DevBuf cols;
+            cols.alloc(sizeof(int64_t) * cls[k].size());
+            INFT_CUDA(cudaMemcpyAsync(cols.p, cls[k].data(), sizeof(int64_t) * cls[k].size(), cudaMemcpyHostToDevice,
+                                      st));
+            const size_t per = sizeof(double) * lr_scratch_doubles(nmax, rmax);
+            const size_t budget = (size_t)8 << 30;
+            const unsigned grid = (unsigned)std::max<int64_t>(
+                1, std::min<int64_t>((int64_t)cls[k].size(), std::min<int64_t>((int64_t)nsm, budget / per)));
+            DevBuf scratch;
+            scratch.alloc(per * grid);
+            const size_t smem = sizeof(double) * (packed_doubles(ksm) + rmax + 2) + sizeof(int) * (rmax + 2) + 16;
+            INFT_CUDA(cudaFuncSetAttribute(k_alg2_solve_lr, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+            k_alg2_solve_lr<<<grid, 256, smem, st>>>(cc, gc, cols.as<int64_t>(), (int64_t)cls[k].size(),
+                                                     cnt.as<int32_t>(), nmax, rmax, ksm, scratch.as<double>(), tau * tau,
+                                                     1e-15, p.P, w64.as<double>(), ndrop.as<unsigned long long>(),
+                                                     rank_max.as<int>());
+            INFT_CHECK_LAUNCH();
+            p.launches++;
+            INFT_CUDA(cudaStreamSynchronize(st));
+            continue;
+        }
         int nmax = limits[k];
         DevBuf cols;
         cols.alloc(sizeof(int64_t) * cls[k].size());
@@ -677,9 +1104,23 @@ static void alg2(Plan& p, double tau, DevBuf& w64, cudaStream_t st) {
         INFT_CUDA(cudaStreamSynchronize(st));
     }
     unsigned long long nd = 0;
+    int rk = 0;
     INFT_CUDA(cudaMemcpyAsync(&nd, ndrop.p, sizeof(nd), cudaMemcpyDeviceToHost, st));
+    INFT_CUDA(cudaMemcpyAsync(&rk, rank_max.p, sizeof(rk), cudaMemcpyDeviceToHost, st));
     INFT_CUDA(cudaStreamSynchronize(st));
     p.n_rank_deficient = (int64_t)nd;
+    p.max_lowrank_rank = rk;
+    if (getenv("INFT_SETUP_DEBUG")) {
+        unsigned long long js[3];
+        INFT_CUDA(cudaMemcpyFromSymbol(js, g_jac_stats, sizeof(js)));
+        unsigned long long lc[6];
+        INFT_CUDA(cudaMemcpyFromSymbol(lc, g_lr_cycles, sizeof(lc)));
+        fprintf(stderr, "alg2: classes %zu/%zu/%zu cols, jacobi calls %llu mean sweeps %.2f max %llu\n",
+                cls[0].size(), cls[1].size(), cls[2].size(), js[1], js[1] ? (double)js[0] / js[1] : 0.0, js[2]);
+        fprintf(stderr, "alg2 large columns, Gcycles per phase: collect %.2f diag %.2f pchol %.2f gram %.2f "
+                "jacobi %.2f back %.2f\n", lc[0] * 1e-9, lc[1] * 1e-9, lc[2] * 1e-9, lc[3] * 1e-9, lc[4] * 1e-9,
+                lc[5] * 1e-9);
+    }
 }
 
 static void alg1(Plan& p, double tau, DevBuf& w64, cudaStream_t st) {
@@ -730,6 +1171,7 @@ static void alg1(Plan& p, double tau, DevBuf& w64, cudaStream_t st) {
     INFT_CUDA(cudaMemcpyAsync(&nd, ndrop.p, sizeof(nd), cudaMemcpyDeviceToHost, st));
     INFT_CUDA(cudaStreamSynchronize(st));
     p.n_rank_deficient = (int64_t)nd;
+    p.max_lowrank_rank = 0;
     p.n_empty_cols = 0;
     p.max_col_size = p.P;
 }
