@@ -18,6 +18,7 @@
 
 #include "common.cuh"
 #include "inft_internal.cuh"
+#include "tma.cuh"
 
 namespace inft {
 
@@ -103,6 +104,258 @@ __global__ void k_spread_generic_2d(const int32_t* __restrict__ seg_start, const
         });
         grid[idx] = mk<T>(sx, sy);
     }
+}
+
+// 2-D spread, output-stationary, one warp per (grid cell n, 32 RHS): the warp walks the
+// candidate nodes of the (up to 2 x 2) tiles whose nodes can reach n -- a warp-uniform loop,
+// so the slot test, the weight and the node record are shared by the 32 lanes -- and lane r
+// accumulates w_{j,t} f_r(x_j) for its RHS from the node-major copy fT[i][r] (one coalesced
+// 32-lane read per node).  Every grid value is written once: no atomics, deterministic.
+template <typename T>
+__global__ void k_transpose_f(const C2<T>* __restrict__ f, const int32_t* __restrict__ perm, C2<T>* __restrict__ fT,
+                              int64_t N, int R) {
+    const int64_t total = (int64_t)N * R;
+    for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
+         idx += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t i = idx / R;
+        const int r = (int)(idx - i * R);
+        fT[idx] = f[(int64_t)r * N + perm[i]];
+    }
+}
+
+template <typename T, bool WC>
+__global__ void k_spread_2d_warp(const int32_t* __restrict__ seg_start, const int32_t* __restrict__ n0s,
+                                 const T* __restrict__ w, int PP, int P1, const C2<T>* __restrict__ fT,
+                                 C2<T>* __restrict__ grid, int64_t Ms1, int64_t Ms2, int S1, int S2, int64_t nseg2,
+                                 int R, int64_t GS) {
+    const int lane = threadIdx.x & 31;
+    const int64_t wid0 = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    const int nrc = (R + 31) >> 5;
+    const int64_t Mst = Ms1 * Ms2;
+    const int64_t nseg1 = (Ms1 + S1 - 1) / S1;
+    for (int64_t wid = wid0; wid < Mst * nrc; wid += nwarps) {
+        const int64_t n = wid / nrc;
+        const int r = (int)(wid - n * nrc) * 32 + lane;
+        const bool active = r < R;
+        const int64_t n1 = n / Ms2, n2 = n - (n / Ms2) * Ms2;
+        T sx = 0, sy = 0;
+        for_segments(n1, std::min<int64_t>(P1, Ms1), Ms1, S1, nseg1, [&](int64_t s1) {
+            for_segments(n2, std::min<int64_t>(P1, Ms2), Ms2, S2, nseg2, [&](int64_t s2) {
+                const int64_t tile = s1 * nseg2 + s2;
+                const int i1 = __ldg(seg_start + tile + 1);
+                for (int i = __ldg(seg_start + tile); i < i1; ++i) {
+                    int64_t t1 = mod64(n1 - __ldg(n0s + 2 * i), Ms1);
+                    const int64_t t2b = mod64(n2 - __ldg(n0s + 2 * i + 1), Ms2);
+                    if (t1 >= P1 || t2b >= P1) continue;
+                    const C2<T> fv = active ? fT[(int64_t)i * R + r] : mk<T>(T(0), T(0));
+                    for (; t1 < P1; t1 += Ms1)
+                        for (int64_t t2 = t2b; t2 < P1; t2 += Ms2) {
+                            const int64_t t = t1 * P1 + t2;
+                            if (WC) {
+                                const T wr = __ldg(w + ((int64_t)i * PP + t) * 2), wi = __ldg(w + ((int64_t)i * PP + t) * 2 + 1);
+                                sx += wr * fv.x + wi * fv.y;
+                                sy += wr * fv.y - wi * fv.x;
+                            } else {
+                                const T wr = __ldg(w + (int64_t)i * PP + t);
+                                sx = fma(wr, fv.x, sx);
+                                sy = fma(wr, fv.y, sy);
+                            }
+                        }
+                }
+            });
+        });
+        if (active) grid[(int64_t)r * GS + n] = mk<T>(sx, sy);
+    }
+}
+
+// 2-D spread, tile-stationary (16 x 16 cells, P1 = 2m+1 <= 16): CTA = one output tile x 32
+// RHS, 8 warps; warp w owns cell rows w and w + 8 of the tile, lane = RHS, and keeps those
+// 2 x 16 accumulators in registers.  The warps walk the nodes of the 2 x 2 tiles whose nodes can reach
+// the tile (warp-uniform loop: node record, row test and weights shared by the lanes); a node
+// adds its row slice w[t1][0..P1) f_r to the row, the column offset dispatched by a
+// warp-uniform switch so that every register index is static.  Each grid value is written
+// once: no atomics, deterministic.  f is read from the node-major copy fT[i][r].
+template <typename T, int P1, int C>
+__device__ __forceinline__ void row_add(T (&ax)[16], T (&ay)[16], const T* wr, C2<T> fv) {
+#pragma unroll
+    for (int t2 = 0; t2 < P1; ++t2) {
+        constexpr int lo = C < 0 ? -C : 0;  // first tap inside the tile
+        if (t2 >= lo && C + t2 < 16) {
+            const int col = (C + t2) < 0 ? 0 : ((C + t2) > 15 ? 15 : (C + t2));
+            const T wv = wr[t2];
+            ax[col] = fma(wv, fv.x, ax[col]);
+            ay[col] = fma(wv, fv.y, ay[col]);
+        }
+    }
+}
+
+// warp-uniform column-offset dispatch c in [-(P1-1), 15] -> static register indices
+template <typename T, int P1>
+__device__ __forceinline__ void row_dispatch(int c, T (&ax)[16], T (&ay)[16], const T* wr, C2<T> fv) {
+#define INFT_ROW_CASE(CC)                                   \
+    case CC:                                                \
+        if constexpr ((CC) > -P1) row_add<T, P1, CC>(ax, ay, wr, fv); \
+        break;
+    switch (c) {
+        INFT_ROW_CASE(-15) INFT_ROW_CASE(-14) INFT_ROW_CASE(-13) INFT_ROW_CASE(-12) INFT_ROW_CASE(-11)
+        INFT_ROW_CASE(-10) INFT_ROW_CASE(-9) INFT_ROW_CASE(-8) INFT_ROW_CASE(-7) INFT_ROW_CASE(-6)
+        INFT_ROW_CASE(-5) INFT_ROW_CASE(-4) INFT_ROW_CASE(-3) INFT_ROW_CASE(-2) INFT_ROW_CASE(-1)
+        INFT_ROW_CASE(0) INFT_ROW_CASE(1) INFT_ROW_CASE(2) INFT_ROW_CASE(3) INFT_ROW_CASE(4) INFT_ROW_CASE(5)
+        INFT_ROW_CASE(6) INFT_ROW_CASE(7) INFT_ROW_CASE(8) INFT_ROW_CASE(9) INFT_ROW_CASE(10) INFT_ROW_CASE(11)
+        INFT_ROW_CASE(12) INFT_ROW_CASE(13) INFT_ROW_CASE(14) INFT_ROW_CASE(15)
+        default: break;
+    }
+#undef INFT_ROW_CASE
+}
+
+// Node batches of kB2 records are staged in shared memory, double-buffered: the batch's
+// weights (one contiguous run of kB2 * PP values) by one 1-D bulk copy, its f values (kB2 x 32
+// RHS) and slot bases by per-thread cp.async, all issued one batch ahead so that the warps
+// only ever read shared memory in the node loop.
+constexpr int kB2 = 48;
+
+template <typename T>
+__host__ __device__ constexpr size_t tile2d_stage_bytes(int PP) {
+    return ((sizeof(C2<T>) * kB2 * 32 + sizeof(int2) * kB2 + sizeof(T) * (size_t)kB2 * PP) + 127) / 128 * 128;
+}
+
+template <typename T, int MC>
+__global__ void __launch_bounds__(256) k_spread_2d_tile(const int32_t* __restrict__ seg_start,
+                                                        const int32_t* __restrict__ n0s, const T* __restrict__ w,
+                                                        int PP, const C2<T>* __restrict__ fT, C2<T>* __restrict__ grid,
+                                                        int Ms1, int Ms2, int nseg1, int nseg2, int R, int64_t GS) {
+    constexpr int P1 = 2 * MC + 1;
+    extern __shared__ __align__(128) unsigned char sm2[];
+    __shared__ uint64_t full[2];
+    __shared__ int tlo[4], thi[4], tnb[5];  // candidate tile ranges, batch prefix counts
+    const size_t stage_bytes = tile2d_stage_bytes<T>(PP);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int s1 = blockIdx.x / nseg2, s2 = blockIdx.x - (blockIdx.x / nseg2) * nseg2;
+    const int row0 = s1 * 16, col0 = s2 * 16;
+    const int rbase = blockIdx.y * 32;
+    const int r = rbase + lane;
+    const bool active = r < R;
+    if (threadIdx.x == 0) {
+        tnb[0] = 0;
+        for (int tq = 0; tq < 4; ++tq) {
+            const int d1 = (tq >> 1) - 1, d2 = (tq & 1) - 1;
+            const int t1s = s1 + d1 < 0 ? s1 + d1 + nseg1 : s1 + d1;
+            const int t2s = s2 + d2 < 0 ? s2 + d2 + nseg2 : s2 + d2;
+            const int tile = t1s * nseg2 + t2s;
+            tlo[tq] = __ldg(seg_start + tile);
+            thi[tq] = __ldg(seg_start + tile + 1);
+            tnb[tq + 1] = tnb[tq] + (thi[tq] - tlo[tq] + kB2 - 1) / kB2;
+        }
+        mbar_init(&full[0], 1);
+        mbar_init(&full[1], 1);
+        fence_barrier_init();
+    }
+    __syncthreads();
+    const int nbat = tnb[4];
+    auto batch = [&](int b, int& base, int& nb) {
+        int tq = 0;
+        while (b >= tnb[tq + 1]) ++tq;
+        base = tlo[tq] + (b - tnb[tq]) * kB2;
+        nb = min(kB2, thi[tq] - base);
+    };
+    auto issue = [&](int b) {
+        int base, nb;
+        batch(b, base, nb);
+        unsigned char* sb = sm2 + (size_t)(b & 1) * stage_bytes;
+        C2<T>* fsm = reinterpret_cast<C2<T>*>(sb);
+        int2* rec = reinterpret_cast<int2*>(fsm + kB2 * 32);
+        T* wsm = reinterpret_cast<T*>(rec + kB2);
+        if (threadIdx.x == 0) {
+            const uint32_t wb = (uint32_t)(sizeof(T) * (size_t)nb * PP);
+            mbar_arrive_expect_tx(&full[b & 1], wb);
+            bulk_g2s(wsm, w + (int64_t)base * PP, wb, &full[b & 1]);
+        }
+        for (int e = threadIdx.x; e < nb * 32; e += blockDim.x) {
+            const int j = e >> 5, l = e & 31;
+            const bool ok = rbase + l < R;
+            cp_async<(int)sizeof(C2<T>)>(fsm + e, fT + (int64_t)(base + j) * R + (ok ? rbase + l : 0),
+                                         ok ? (int)sizeof(C2<T>) : 0);
+        }
+        for (int j = threadIdx.x; j < nb; j += blockDim.x) cp_async<8>(rec + j, n0s + 2 * (base + j), 8);
+        cp_async_commit();
+    };
+    T ax[2][16], ay[2][16];
+#pragma unroll
+    for (int q = 0; q < 2; ++q)
+#pragma unroll
+        for (int c = 0; c < 16; ++c) ax[q][c] = ay[q][c] = T(0);
+    // rows warp and warp + 8 of the tile: a node's 13-row footprint then spreads its work over
+    // all warps (balanced batches between the barriers)
+    const int myrow = row0 + warp;
+    if (nbat > 0) issue(0);
+#pragma unroll 1
+    for (int b = 0; b < nbat; ++b) {
+        if (b + 1 < nbat) {
+            issue(b + 1);
+            cp_async_wait<1>();
+        } else {
+            cp_async_wait<0>();
+        }
+        mbar_wait(&full[b & 1], (b >> 1) & 1);
+        __syncthreads();  // every thread's cp.async data of batch b visible
+        int base, nb;
+        batch(b, base, nb);
+        const unsigned char* sb = sm2 + (size_t)(b & 1) * stage_bytes;
+        const C2<T>* fsm = reinterpret_cast<const C2<T>*>(sb);
+        const int2* rec = reinterpret_cast<const int2*>(fsm + kB2 * 32);
+        const T* wsm = reinterpret_cast<const T*>(rec + kB2);
+#pragma unroll 1
+        for (int j = 0; j < nb; ++j) {
+            const int2 a = rec[j];
+            int dr = myrow - a.x;  // t1 of my first row (mod Ms1)
+            if (dr < 0) dr += Ms1;
+            if (dr >= Ms1) dr -= Ms1;
+            int dr2 = dr + 8;
+            if (dr2 >= Ms1) dr2 -= Ms1;
+            if (dr >= P1 && dr2 >= P1) continue;
+            int c = a.y - col0;  // column of tap 0 relative to the tile, in [-(P1-1), 15]
+            if (c > 15) c -= Ms2;
+            if (c < -(P1 - 1)) c += Ms2;
+            const C2<T> fv = fsm[j * 32 + lane];
+            const T* wj = wsm + j * PP;
+            if (dr < P1) row_dispatch<T, P1>(c, ax[0], ay[0], wj + dr * P1, fv);
+            if (dr2 < P1) row_dispatch<T, P1>(c, ax[1], ay[1], wj + dr2 * P1, fv);
+        }
+        fence_proxy_async();  // reads of this stage precede the bulk copy that reuses it
+        __syncthreads();
+    }
+    if (active) {
+        C2<T>* g = grid + (int64_t)r * GS + (int64_t)myrow * Ms2 + col0;
+#pragma unroll
+        for (int q = 0; q < 2; ++q)
+#pragma unroll
+            for (int c = 0; c < 16; ++c) g[(int64_t)q * 8 * Ms2 + c] = mk<T>(ax[q][c], ay[q][c]);
+    }
+}
+
+template <typename T>
+using Tile2dFn = void (*)(const int32_t*, const int32_t*, const T*, int, const C2<T>*, C2<T>*, int, int, int, int,
+                          int, int64_t);
+
+template <typename T>
+static Tile2dFn<T> tile2d_fn(int m) {
+    switch (m) {
+        case 1: return k_spread_2d_tile<T, 1>;
+        case 2: return k_spread_2d_tile<T, 2>;
+        case 3: return k_spread_2d_tile<T, 3>;
+        case 4: return k_spread_2d_tile<T, 4>;
+        case 5: return k_spread_2d_tile<T, 5>;
+        case 6: return k_spread_2d_tile<T, 6>;
+        case 7: return k_spread_2d_tile<T, 7>;
+    }
+    return nullptr;
+}
+
+static bool tile2d_available(const Plan& p) {
+    return p.d == 2 && p.wt == INFT_WEIGHTS_REAL && p.m >= 1 && p.m <= 7 && p.S[0] == 16 && p.S[1] == 16 &&
+           p.Ms[0] % 16 == 0 && p.Ms[1] % 16 == 0 && p.nseg[0] >= 2 && p.nseg[1] >= 2 &&
+           !getenv_flag("INFT_SPREAD2D_WARP");
 }
 
 // Generic gather: one thread per (sorted node i, RHS r).
@@ -244,6 +497,37 @@ static void spread(Plan& p, const C2<T>* f, C2<T>* grid, int64_t R, cudaStream_t
             k_spread_generic_1d<T, false><<<gs_blocks(total, 256), 256, 0, st>>>(
                 p.seg_start.as<int32_t>(), p.n0s.as<int32_t>(), p.perm.as<int32_t>(), w, p.PP, p.P, f, grid, p.N,
                 p.Ms[0], p.GS, p.S[0], (int)R);
+    } else if (!getenv_flag("INFT_SPREAD2D_GENERIC")) {
+        // node-major copy of f (sorted node order), then the tile kernel (or one warp per cell)
+        if (p.fT_rhs < R) {
+            p.fT.alloc(sizeof(C2<T>) * (size_t)p.N * R);
+            p.fT_rhs = R;
+        }
+        C2<T>* fT = p.fT.as<C2<T>>();
+        k_transpose_f<T><<<gs_blocks(R * p.N, 256), 256, 0, st>>>(f, p.perm.as<int32_t>(), fT, p.N, (int)R);
+        INFT_CHECK_LAUNCH();
+        p.launches++;
+        if (tile2d_available(p)) {
+            dim3 g((unsigned)(p.nseg[0] * p.nseg[1]), (unsigned)ceil_div(R, 32));
+            const size_t smem = 2 * tile2d_stage_bytes<T>(p.PP);
+            INFT_CUDA(cudaFuncSetAttribute(tile2d_fn<T>(p.m), cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+            tile2d_fn<T>(p.m)<<<g, 256, smem, st>>>(p.seg_start.as<int32_t>(), p.n0s.as<int32_t>(), w, p.PP, fT, grid,
+                                                 (int)p.Ms[0], (int)p.Ms[1], (int)p.nseg[0], (int)p.nseg[1], (int)R,
+                                                 p.GS);
+            INFT_CHECK_LAUNCH();
+            p.launches++;
+            return;
+        }
+        const int64_t warps = p.Mstot * ceil_div(R, 32);
+        const unsigned blocks = (unsigned)std::min<int64_t>(ceil_div(warps * 32, 256), (int64_t)148 * 64);
+        if (p.wt == INFT_WEIGHTS_COMPLEX)
+            k_spread_2d_warp<T, true><<<blocks, 256, 0, st>>>(p.seg_start.as<int32_t>(), p.n0s.as<int32_t>(), w, p.PP,
+                                                              p.P1, fT, grid, p.Ms[0], p.Ms[1], p.S[0], p.S[1],
+                                                              p.nseg[1], (int)R, p.GS);
+        else
+            k_spread_2d_warp<T, false><<<blocks, 256, 0, st>>>(p.seg_start.as<int32_t>(), p.n0s.as<int32_t>(), w,
+                                                               p.PP, p.P1, fT, grid, p.Ms[0], p.Ms[1], p.S[0],
+                                                               p.S[1], p.nseg[1], (int)R, p.GS);
     } else {
         int64_t total = R * p.Mstot;
         if (p.wt == INFT_WEIGHTS_COMPLEX)

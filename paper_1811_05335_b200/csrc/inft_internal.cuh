@@ -42,6 +42,7 @@ struct Fail {
 #define INFT_STR_(x) INFT_STR2_(x)
 // INFT_SYNC_CHECK=1: synchronize after every launch so a fault names its kernel's call site
 bool sync_check_enabled();
+bool getenv_flag(const char* name);  // name set to a nonzero integer
 #define INFT_CHECK_LAUNCH()                                                              \
     do {                                                                                 \
         cudaError_t e_ = cudaGetLastError();                                             \
@@ -115,6 +116,8 @@ struct Plan {
 
     // workspace
     DevBuf grid;          // [Rt][Mstot] complex (plan precision)
+    DevBuf fT;            // 2-D spread: node-major copy of f, [N][R] (sorted node order)
+    int64_t fT_rhs = 0;
     int64_t grid_rhs = 0; // capacity in RHS
     DevBuf stage_in[2], stage_out[2];
     size_t stage_in_bytes = 0, stage_out_bytes = 0;

@@ -18,6 +18,11 @@
 namespace inft {
 
 static thread_local std::string g_last_error;
+bool getenv_flag(const char* name) {
+    const char* e = getenv(name);
+    return e && atoi(e) != 0;
+}
+
 bool sync_check_enabled() {
     static const bool on = [] {
         const char* e = getenv("INFT_SYNC_CHECK");
@@ -49,7 +54,7 @@ void DevBuf::free_() {
 
 size_t Plan::workspace_bytes() const {
     size_t t = nodes.bytes + l0.bytes + bin.bytes + perm.bytes + seg_start.bytes + n0s.bytes +
-               delta.bytes + dk.bytes + dkf.bytes + w.bytes + w64.bytes + grid.bytes;
+               delta.bytes + dk.bytes + dkf.bytes + w.bytes + w64.bytes + grid.bytes + fT.bytes;
     for (int i = 0; i < 2; i++) t += stage_in[i].bytes + stage_out[i].bytes;
     for (auto& kv : fft) {
         size_t ws = 0;
@@ -280,7 +285,8 @@ void plan_build(Plan& p, const double* nodes_any, cudaStream_t st) {
         p.nseg[0] = ceil_div(p.Ms[0], p.S[0]);
         p.nseg[1] = 1;
     } else {
-        p.S[0] = p.S[1] = choose_segment(p.m);
+        // 2-D tiles: 16 x 16 cells for m <= 7 (the tile spread k_spread_2d_tile needs P1 <= 16)
+        p.S[0] = p.S[1] = (2 * p.m + 1 <= 16) ? 16 : choose_segment(p.m);
         p.nseg[0] = ceil_div(p.Ms[0], p.S[0]);
         p.nseg[1] = ceil_div(p.Ms[1], p.S[1]);
     }

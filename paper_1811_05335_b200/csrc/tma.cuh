@@ -77,6 +77,24 @@ __device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, i
         : "memory");
 }
 
+// Per-thread asynchronous copy global -> shared of BYTES (4, 8 or 16) with zero fill when
+// src_bytes = 0 (LDGSTS); completion by cp_async_commit / cp_async_wait<N>.
+template <int BYTES>
+__device__ __forceinline__ void cp_async(void* dst, const void* src, int src_bytes) {
+    if constexpr (BYTES == 16)
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(smem_addr(dst)), "l"(src), "r"(src_bytes)
+                     : "memory");
+    else
+        asm volatile("cp.async.ca.shared.global [%0], [%1], %2, %3;" ::"r"(smem_addr(dst)), "l"(src), "n"(BYTES),
+                     "r"(src_bytes)
+                     : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+    asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+
 // Order this thread's prior generic-proxy shared-memory accesses before later
 // async-proxy (TMA / bulk copy) accesses: required before releasing a stage
 // buffer that the next TMA will overwrite (cross-proxy WAR hazard).
