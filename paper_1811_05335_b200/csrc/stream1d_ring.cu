@@ -80,6 +80,10 @@ __global__ void __launch_bounds__(128, INFT_RING_MINB) k_spread_ring(const __gri
     constexpr int EB = 128 / (int)sizeof(C2<T>);
     constexpr int CE = (int)sizeof(C2<T>) / 8;
     constexpr int NBOX = kNB / EB;   // f boxes per batch
+    // complex64: a box may only start at an even node (16-byte aligned innermost start; an
+    // 8-byte aligned start faults), so the batch's f tile is fetched from the even node at or
+    // before it with one extra box and read at offset (col & 1)
+    constexpr int NBF = NBOX + (CE == 1 ? 1 : 0);
     constexpr int SBOX = SEG / EB;   // store boxes per segment
     static_assert(SEG % EB == 0 && kNB % EB == 0, "tile shapes");
     const int WPB = blockDim.x >> 5;
@@ -87,7 +91,7 @@ __global__ void __launch_bounds__(128, INFT_RING_MINB) k_spread_ring(const __gri
     const uint32_t sw = ((uint32_t)lane << 7) | ((uint32_t)(lane & 7) << 4);
 
     extern __shared__ __align__(1024) unsigned char smem[];
-    const uint32_t fstage = (uint32_t)NBOX * WPB * 4096u;  // [NBOX][rows][128]
+    const uint32_t fstage = (uint32_t)NBF * WPB * 4096u;  // [NBF][rows][128]
     const uint32_t rstage = (uint32_t)((kNB * PP * (int)sizeof(T) + 127) & ~127);
     unsigned char* fbuf = smem;
     unsigned char* stg = smem + kStages * fstage;                 // [WPB][SBOX][32][128]
@@ -125,11 +129,12 @@ __global__ void __launch_bounds__(128, INFT_RING_MINB) k_spread_ring(const __gri
         const uint32_t rbytes = (uint32_t)(cnt * PP * (int)sizeof(T));
         int col = pos + cshift;
         if (col >= N) col -= N;
+        if (CE == 1) col &= ~1;
         mbar_arrive_expect_tx(&full[stage], fstage + rbytes);
         for (int wi = 0; wi < WPB; ++wi)
 #pragma unroll
-            for (int bx = 0; bx < NBOX; ++bx)
-                tma_load_2d(fbuf + stage * fstage + (wi * NBOX + bx) * 4096u, &fmap, tcoord<CE>(col + bx * EB),
+            for (int bx = 0; bx < NBF; ++bx)
+                tma_load_2d(fbuf + stage * fstage + (wi * NBF + bx) * 4096u, &fmap, tcoord<CE>(col + bx * EB),
                             row0 + wi * 32, &full[stage]);
         bulk_g2s(rbuf + stage * rstage, w + (int64_t)pos * PP, rbytes, &full[stage]);
     };
@@ -188,7 +193,7 @@ __global__ void __launch_bounds__(128, INFT_RING_MINB) k_spread_ring(const __gri
         ++cur_k;
     };
 
-    const uint32_t frow = (uint32_t)warp * NBOX * 4096u;  // this warp's boxes inside a stage
+    const uint32_t frow = (uint32_t)warp * NBF * 4096u;  // this warp's boxes inside a stage
     for (int b = 0; b < nb; ++b) {
         const int stage = b % kStages;
         const uint32_t parity = (uint32_t)((b / kStages) & 1);
@@ -198,6 +203,12 @@ __global__ void __launch_bounds__(128, INFT_RING_MINB) k_spread_ring(const __gri
         mbar_wait(&full[stage], parity);
         const unsigned char* fb = fbuf + stage * fstage + frow;
         const T* rec = reinterpret_cast<const T*>(rbuf + stage * rstage);
+        int fo = 0;  // complex64: offset of the batch's first node inside the fetched tile
+        if (CE == 1) {
+            int col = pos + cshift;
+            if (col >= N) col -= N;
+            fo = col & 1;
+        }
         // Dense batch: the kNB nodes are exactly one segment with slot offsets
         // 0..SEG-1 (jittered nodes with N = M_sigma).  Straight-line code, no
         // per-node dispatch: node q adds into window registers q .. q+2m.
@@ -214,7 +225,7 @@ __global__ void __launch_bounds__(128, INFT_RING_MINB) k_spread_ring(const __gri
             while (cur_k < kq) flush();
 #pragma unroll
             for (int q = 0; q < kNB; ++q) {
-                const C2<T> fv = *reinterpret_cast<const C2<T>*>(fb + cofs<T>(q, sw));
+                const C2<T> fv = *reinterpret_cast<const C2<T>*>(fb + cofs<T>(q + fo, sw));
                 T wv[P];
                 WeightLoader<T, P>::load_smem(rec + q * PP, wv);
 #pragma unroll
@@ -235,7 +246,7 @@ __global__ void __launch_bounds__(128, INFT_RING_MINB) k_spread_ring(const __gri
             const int dl = (int)(n0 % SEG);
             const int kq = pro ? 0 : seg - s0 + 1;
             while (cur_k < kq) flush();
-            const C2<T> fv = *reinterpret_cast<const C2<T>*>(fb + cofs<T>(q, sw));
+            const C2<T> fv = *reinterpret_cast<const C2<T>*>(fb + cofs<T>(q + fo, sw));
             T wv[P];
             WeightLoader<T, P>::load_smem(rec, wv);
             switch (dl) {
@@ -482,14 +493,31 @@ __global__ void __launch_bounds__(128, INFT_RING_MINB) k_gather_ring(const __gri
             }
         }
         if (full_tile) {
-            fence_proxy_async();
-            __syncwarp();
-            if (lane == 0) {
-                int col = pos + cshift;
-                if (col >= N) col -= N;
+            int col = pos + cshift;
+            if (col >= N) col -= N;
+            if (CE == 2 || (col & 1) == 0) {
+                fence_proxy_async();
+                __syncwarp();
+                if (lane == 0) {
 #pragma unroll
-                for (int bx = 0; bx < OBOX; ++bx) tma_store_2d(&omap, tcoord<CE>(col + bx * EB), rstore, my_stg + bx * 4096u);
-                bulk_commit();
+                    for (int bx = 0; bx < OBOX; ++bx)
+                        tma_store_2d(&omap, tcoord<CE>(col + bx * EB), rstore, my_stg + bx * 4096u);
+                    bulk_commit();
+                }
+            } else {
+                // complex64 batch starting on an odd node: a TMA store box may not start there
+                // (16-byte aligned innermost start).  Plain stores, two staged rows per
+                // instruction (16 consecutive nodes each) so that they stay coalesced.
+                static_assert(kNB == 16, "two 16-node rows per warp store");
+                __syncwarp();
+#pragma unroll
+                for (int i = 0; i < 16; ++i) {
+                    const int rho = 2 * i + (lane >> 4), q = lane & 15;
+                    const uint32_t swr = ((uint32_t)rho << 7) | ((uint32_t)(rho & 7) << 4);
+                    if (rstore + rho < R)
+                        f[(int64_t)(rstore + rho) * N + col + q] =
+                            *reinterpret_cast<const C2<T>*>(my_stg + cofs<T>(q, swr));
+                }
             }
         }
         fence_proxy_async();
@@ -543,16 +571,15 @@ static bool ring_env_disabled() {
     return v == 1;
 }
 
-// complex64: the ring kernels' node-side boxes (f tiles, output tiles) start at
-// arbitrary node offsets, which for 8-byte elements are only 8-byte aligned; a
-// tensor-map copy whose innermost start is not 16-byte aligned raises "illegal
-// instruction" (measured with tools/tma_probe.cu: start offset 1 x 8 B faults,
-// 2 x 8 B runs).  Until the batches are re-aligned to even node offsets, complex64
-// takes the register-window spread and the stream1d.cu staged gather.
-// INFT_RING_C64=1 re-enables the ring kernels (for experiments only).
+// complex64: a tensor-map copy whose innermost start is not 16-byte aligned raises "illegal
+// instruction" (measured with tools/tma_probe.cu: start offset 1 x 8 B faults, 2 x 8 B runs),
+// and node-side boxes start at arbitrary nodes; k_spread_ring therefore fetches each batch's
+// f tile from the even node at or before it (one extra box) and k_gather_ring stores a batch
+// that starts on an odd node with plain stores.  INFT_RING_C64=0 routes complex64 to the
+// register-window / stream1d kernels instead.
 static bool ring_c64_spread_enabled() {
     const char* e = getenv("INFT_RING_C64");
-    return e && atoi(e);
+    return !(e && atoi(e) == 0);
 }
 
 bool ring_spread_available(const Plan& p) { return ring_available(p); }
@@ -573,7 +600,8 @@ static int ring_wpb(int64_t R) {
 template <typename T>
 static size_t ring_spread_smem(int wpb, int PP, int SEG) {
     const int EB = 128 / (int)sizeof(C2<T>);
-    size_t f = (size_t)ring::kStages * (ring::kNB / EB) * wpb * 4096;
+    const int nbf = ring::kNB / EB + (sizeof(C2<T>) == 8 ? 1 : 0);  // k_spread_ring's NBF
+    size_t f = (size_t)ring::kStages * nbf * wpb * 4096;
     size_t st = (size_t)wpb * (SEG / EB) * 4096;
     size_t r = (size_t)ring::kStages * ((ring::kNB * PP * (int)sizeof(T) + 127) & ~127);
     return f + st + r + 2 * ring::kStages * sizeof(uint64_t);
