@@ -15,6 +15,7 @@
 // spectra are centered (c = k + M/2).  s is folded into d (reading A2).
 #include <algorithm>
 #include <cstring>
+#include <vector>
 
 #include "common.cuh"
 #include "inft_internal.cuh"
@@ -221,17 +222,22 @@ __host__ __device__ constexpr size_t tile2d_stage_bytes(int PP) {
 }
 
 template <typename T, int MC>
-__global__ void __launch_bounds__(256) k_spread_2d_tile(const int32_t* __restrict__ seg_start,
+__global__ void __launch_bounds__(256) k_spread_2d_tile(const int4* __restrict__ work,
+                                                        const int32_t* __restrict__ seg_start,
                                                         const int32_t* __restrict__ n0s, const T* __restrict__ w,
                                                         int PP, const C2<T>* __restrict__ fT, C2<T>* __restrict__ grid,
-                                                        int Ms1, int Ms2, int nseg1, int nseg2, int R, int64_t GS) {
+                                                        C2<T>* __restrict__ part, int Ms1, int Ms2, int nseg1,
+                                                        int nseg2, int R, int64_t GS) {
     constexpr int P1 = 2 * MC + 1;
     extern __shared__ __align__(128) unsigned char sm2[];
     __shared__ uint64_t full[2];
     __shared__ int tlo[4], thi[4], tnb[5];  // candidate tile ranges, batch prefix counts
     const size_t stage_bytes = tile2d_stage_bytes<T>(PP);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int s1 = blockIdx.x / nseg2, s2 = blockIdx.x - (blockIdx.x / nseg2) * nseg2;
+    // work item: (tile, first batch, end batch, partial-sum slot or -1): heavy tiles' batch lists
+    // are split over several CTAs whose partial tiles k_spread_2d_combine adds up
+    const int4 wk = work[blockIdx.x];
+    const int s1 = wk.x / nseg2, s2 = wk.x - (wk.x / nseg2) * nseg2;
     const int row0 = s1 * 16, col0 = s2 * 16;
     const int rbase = blockIdx.y * 32;
     const int r = rbase + lane;
@@ -252,7 +258,7 @@ __global__ void __launch_bounds__(256) k_spread_2d_tile(const int32_t* __restric
         fence_barrier_init();
     }
     __syncthreads();
-    const int nbat = tnb[4];
+    const int bfirst = wk.y, bend = min(wk.z, tnb[4]);
     auto batch = [&](int b, int& base, int& nb) {
         int tq = 0;
         while (b >= tnb[tq + 1]) ++tq;
@@ -288,10 +294,10 @@ __global__ void __launch_bounds__(256) k_spread_2d_tile(const int32_t* __restric
     // rows warp and warp + 8 of the tile: a node's 13-row footprint then spreads its work over
     // all warps (balanced batches between the barriers)
     const int myrow = row0 + warp;
-    if (nbat > 0) issue(0);
+    if (bfirst < bend) issue(bfirst);
 #pragma unroll 1
-    for (int b = 0; b < nbat; ++b) {
-        if (b + 1 < nbat) {
+    for (int b = bfirst; b < bend; ++b) {
+        if (b + 1 < bend) {
             issue(b + 1);
             cp_async_wait<1>();
         } else {
@@ -326,17 +332,38 @@ __global__ void __launch_bounds__(256) k_spread_2d_tile(const int32_t* __restric
         __syncthreads();
     }
     if (active) {
-        C2<T>* g = grid + (int64_t)r * GS + (int64_t)myrow * Ms2 + col0;
+        // whole tile: straight into the grid; partial tile: into its slot, [slot][R][16][16]
+        C2<T>* g = wk.w < 0 ? grid + (int64_t)r * GS + (int64_t)myrow * Ms2 + col0
+                            : part + (((int64_t)wk.w * R + r) * 16 + warp) * 16;
+        const int64_t ld = wk.w < 0 ? Ms2 : 16;
 #pragma unroll
         for (int q = 0; q < 2; ++q)
 #pragma unroll
-            for (int c = 0; c < 16; ++c) g[(int64_t)q * 8 * Ms2 + c] = mk<T>(ax[q][c], ay[q][c]);
+            for (int c = 0; c < 16; ++c) g[(int64_t)q * 8 * ld + c] = mk<T>(ax[q][c], ay[q][c]);
+    }
+}
+
+// Sum of the partial tiles of the heavy tiles: item (tile, first slot, slots).
+template <typename T>
+__global__ void k_spread_2d_combine(const int4* __restrict__ items, const C2<T>* __restrict__ part,
+                                    C2<T>* __restrict__ grid, int Ms2, int nseg2, int R, int64_t GS) {
+    const int4 it = items[blockIdx.x];
+    const int s1 = it.x / nseg2, s2 = it.x - (it.x / nseg2) * nseg2;
+    for (int e = threadIdx.x; e < R * 256; e += blockDim.x) {
+        const int r = e >> 8, cell = e & 255;
+        T sx = 0, sy = 0;
+        for (int k = 0; k < it.z; ++k) {
+            const C2<T> v = part[((int64_t)(it.y + k) * R + r) * 256 + cell];
+            sx += v.x;
+            sy += v.y;
+        }
+        grid[(int64_t)r * GS + (int64_t)(s1 * 16 + (cell >> 4)) * Ms2 + s2 * 16 + (cell & 15)] = mk<T>(sx, sy);
     }
 }
 
 template <typename T>
-using Tile2dFn = void (*)(const int32_t*, const int32_t*, const T*, int, const C2<T>*, C2<T>*, int, int, int, int,
-                          int, int64_t);
+using Tile2dFn = void (*)(const int4*, const int32_t*, const int32_t*, const T*, int, const C2<T>*, C2<T>*, C2<T>*,
+                          int, int, int, int, int, int64_t);
 
 template <typename T>
 static Tile2dFn<T> tile2d_fn(int m) {
@@ -350,6 +377,54 @@ static Tile2dFn<T> tile2d_fn(int m) {
         case 7: return k_spread_2d_tile<T, 7>;
     }
     return nullptr;
+}
+
+// Spread work list: one item per tile, or several for a tile whose 2 x 2 neighbourhood holds
+// more than kSplitBatches node batches (partial tiles + combine items); built once per plan.
+static int split_batches() {
+    static const int v = [] {
+        const char* e = getenv("INFT_SPLIT2D");
+        const int x = e ? atoi(e) : 0;
+        return x > 0 ? x : 24;  // config 4: 4 -> 1.95 ms, 8 -> 1.60, 12 -> 1.51, 24 -> 1.48
+    }();
+    return v;
+}
+
+static void ensure_spread2d_work(Plan& p, cudaStream_t st) {
+    if (p.work2d_n >= 0) return;
+    std::vector<int32_t> ss((size_t)p.nseg_tot + 1);
+    INFT_CUDA(cudaMemcpyAsync(ss.data(), p.seg_start.p, sizeof(int32_t) * ss.size(), cudaMemcpyDeviceToHost, st));
+    INFT_CUDA(cudaStreamSynchronize(st));
+    const int n1 = (int)p.nseg[0], n2 = (int)p.nseg[1];
+    std::vector<int4> work, comb;
+    int slots = 0;
+    for (int t = 0; t < n1 * n2; ++t) {
+        const int s1 = t / n2, s2 = t % n2;
+        int nb = 0;
+        for (int tq = 0; tq < 4; ++tq) {
+            const int a = (s1 + (tq >> 1) - 1 + n1) % n1, b = (s2 + (tq & 1) - 1 + n2) % n2;
+            const int tt = a * n2 + b;
+            nb += (ss[tt + 1] - ss[tt] + kB2 - 1) / kB2;
+        }
+        const int kSplitBatches = split_batches();
+        const int parts = std::max(1, (nb + kSplitBatches - 1) / kSplitBatches);
+        if (parts == 1) {
+            work.push_back(make_int4(t, 0, 1 << 30, -1));
+        } else {
+            comb.push_back(make_int4(t, slots, parts, 0));
+            for (int q = 0; q < parts; ++q) work.push_back(make_int4(t, q * kSplitBatches, (q + 1) * kSplitBatches, slots + q));
+            slots += parts;
+        }
+    }
+    p.work2d.alloc(sizeof(int4) * std::max<size_t>(1, work.size()));
+    INFT_CUDA(cudaMemcpyAsync(p.work2d.p, work.data(), sizeof(int4) * work.size(), cudaMemcpyHostToDevice, st));
+    p.comb2d.alloc(sizeof(int4) * std::max<size_t>(1, comb.size()));
+    if (!comb.empty())
+        INFT_CUDA(cudaMemcpyAsync(p.comb2d.p, comb.data(), sizeof(int4) * comb.size(), cudaMemcpyHostToDevice, st));
+    p.work2d_n = (int64_t)work.size();
+    p.comb2d_n = (int64_t)comb.size();
+    p.slots2d = slots;
+    INFT_CUDA(cudaStreamSynchronize(st));
 }
 
 static bool tile2d_available(const Plan& p) {
@@ -508,14 +583,25 @@ static void spread(Plan& p, const C2<T>* f, C2<T>* grid, int64_t R, cudaStream_t
         INFT_CHECK_LAUNCH();
         p.launches++;
         if (tile2d_available(p)) {
-            dim3 g((unsigned)(p.nseg[0] * p.nseg[1]), (unsigned)ceil_div(R, 32));
+            ensure_spread2d_work(p, st);
+            if (p.part2d_rhs < R && p.slots2d > 0) {
+                p.part2d.alloc(sizeof(C2<T>) * (size_t)p.slots2d * R * 256);
+                p.part2d_rhs = R;
+            }
+            dim3 g((unsigned)p.work2d_n, (unsigned)ceil_div(R, 32));
             const size_t smem = 2 * tile2d_stage_bytes<T>(p.PP);
             INFT_CUDA(cudaFuncSetAttribute(tile2d_fn<T>(p.m), cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-            tile2d_fn<T>(p.m)<<<g, 256, smem, st>>>(p.seg_start.as<int32_t>(), p.n0s.as<int32_t>(), w, p.PP, fT, grid,
-                                                 (int)p.Ms[0], (int)p.Ms[1], (int)p.nseg[0], (int)p.nseg[1], (int)R,
-                                                 p.GS);
+            tile2d_fn<T>(p.m)<<<g, 256, smem, st>>>(p.work2d.as<int4>(), p.seg_start.as<int32_t>(), p.n0s.as<int32_t>(),
+                                                 w, p.PP, fT, grid, p.part2d.as<C2<T>>(), (int)p.Ms[0],
+                                                 (int)p.Ms[1], (int)p.nseg[0], (int)p.nseg[1], (int)R, p.GS);
             INFT_CHECK_LAUNCH();
             p.launches++;
+            if (p.comb2d_n > 0) {
+                k_spread_2d_combine<T><<<(unsigned)p.comb2d_n, 256, 0, st>>>(
+                    p.comb2d.as<int4>(), p.part2d.as<C2<T>>(), grid, (int)p.Ms[1], (int)p.nseg[1], (int)R, p.GS);
+                INFT_CHECK_LAUNCH();
+                p.launches++;
+            }
             return;
         }
         const int64_t warps = p.Mstot * ceil_div(R, 32);
@@ -543,6 +629,147 @@ static void spread(Plan& p, const C2<T>* f, C2<T>* grid, int64_t R, cudaStream_t
     p.launches++;
 }
 
+// 2-D gather, node-stationary: CTA = a chunk of <= kG2 nodes of one 16 x 16-cell tile x 32 RHS
+// (lane = RHS).  The chunk's weights arrive by one bulk copy; the grid rows its footprints
+// cover (16 + P1 - 1 of them, each 16 + P1 - 1 cells wide) stream through a double-buffered
+// shared row (cp.async), and warp w accumulates, in registers, the nodes w, w + 8, ... of the
+// chunk: node j adds sum_t2 w_j[t1][t2] g[row][c_j + t2] for the row's slot t1.  Heavy tiles
+// are split into several chunks (balanced CTAs); one plain store per (node, RHS).
+constexpr int kG2 = 64;
+
+template <typename T, int MC>
+__global__ void __launch_bounds__(256) k_gather_2d_tile(const int2* __restrict__ chunks, const int32_t* __restrict__ seg_start,
+                                                        const int32_t* __restrict__ n0s, const int32_t* __restrict__ perm,
+                                                        const T* __restrict__ w, int PP, const C2<T>* __restrict__ grid,
+                                                        C2<T>* __restrict__ f, int64_t N, int Ms1, int Ms2, int nseg2,
+                                                        int R, int64_t GS) {
+    constexpr int P1 = 2 * MC + 1;
+    constexpr int W = 16 + P1 - 1;  // rows and columns covered by the tile's footprints
+    constexpr int NPW = kG2 / 8;    // nodes per warp
+    extern __shared__ __align__(128) unsigned char sg[];
+    C2<T>* gsm = reinterpret_cast<C2<T>*>(sg);                    // [2][W][32]
+    T* wsm = reinterpret_cast<T*>(gsm + 2 * W * 32);              // [kG2][PP]
+    __shared__ uint64_t wbar;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int2 ch = chunks[blockIdx.x];
+    const int tile = ch.x, first = ch.y;
+    const int nn = min(kG2, __ldg(seg_start + tile + 1) - first);
+    const int s1 = tile / nseg2, s2 = tile - (tile / nseg2) * nseg2;
+    const int row0 = s1 * 16, col0 = s2 * 16;
+    const int rbase = blockIdx.y * 32;
+    const int r = rbase + lane;
+    if (threadIdx.x == 0) {
+        mbar_init(&wbar, 1);
+        fence_barrier_init();
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        const uint32_t wb = (uint32_t)(sizeof(T) * (size_t)nn * PP);
+        mbar_arrive_expect_tx(&wbar, wb);
+        bulk_g2s(wsm, w + (int64_t)first * PP, wb, &wbar);
+    }
+    auto stage_row = [&](int rho) {
+        int grow = row0 + rho;
+        if (grow >= Ms1) grow -= Ms1;
+        C2<T>* dst = gsm + (rho & 1) * W * 32;
+        for (int e = threadIdx.x; e < W * 32; e += blockDim.x) {
+            const int c = e >> 5, l = e & 31;
+            int gc = col0 + c;
+            if (gc >= Ms2) gc -= Ms2;
+            const bool ok = rbase + l < R;
+            cp_async<(int)sizeof(C2<T>)>(dst + e, grid + (int64_t)(ok ? rbase + l : 0) * GS + (int64_t)grow * Ms2 + gc,
+                                         ok ? (int)sizeof(C2<T>) : 0);
+        }
+        cp_async_commit();
+    };
+    // my nodes: slot base offsets inside the tile
+    int d1[NPW], c2[NPW];
+#pragma unroll
+    for (int q = 0; q < NPW; ++q) {
+        const int j = warp + 8 * q;
+        d1[q] = 1 << 20;
+        c2[q] = 0;
+        if (j < nn) {
+            d1[q] = __ldg(n0s + 2 * (first + j)) - row0;
+            c2[q] = __ldg(n0s + 2 * (first + j) + 1) - col0;
+        }
+    }
+    T ax[NPW], ay[NPW];
+#pragma unroll
+    for (int q = 0; q < NPW; ++q) ax[q] = ay[q] = T(0);
+    stage_row(0);
+    mbar_wait(&wbar, 0);
+#pragma unroll 1
+    for (int rho = 0; rho < W; ++rho) {
+        if (rho + 1 < W) {
+            stage_row(rho + 1);
+            cp_async_wait<1>();
+        } else {
+            cp_async_wait<0>();
+        }
+        __syncthreads();
+        const C2<T>* g = gsm + (rho & 1) * W * 32 + lane;
+#pragma unroll
+        for (int q = 0; q < NPW; ++q) {
+            const int t1 = rho - d1[q];
+            if (t1 >= 0 && t1 < P1) {
+                const T* wr = wsm + (warp + 8 * q) * PP + t1 * P1;
+                const C2<T>* gq = g + c2[q] * 32;
+                T sx = 0, sy = 0;
+#pragma unroll
+                for (int t2 = 0; t2 < P1; ++t2) {
+                    const C2<T> gv = gq[t2 * 32];
+                    sx = fma(wr[t2], gv.x, sx);
+                    sy = fma(wr[t2], gv.y, sy);
+                }
+                ax[q] += sx;
+                ay[q] += sy;
+            }
+        }
+        __syncthreads();  // row buffer (rho & 1) free for row rho + 2
+    }
+    if (r < R) {
+#pragma unroll
+        for (int q = 0; q < NPW; ++q) {
+            const int j = warp + 8 * q;
+            if (j < nn) f[(int64_t)r * N + __ldg(perm + first + j)] = mk<T>(ax[q], ay[q]);
+        }
+    }
+}
+
+template <typename T>
+using Gather2dFn = void (*)(const int2*, const int32_t*, const int32_t*, const int32_t*, const T*, int, const C2<T>*,
+                            C2<T>*, int64_t, int, int, int, int, int64_t);
+
+template <typename T>
+static Gather2dFn<T> gather2d_fn(int m) {
+    switch (m) {
+        case 1: return k_gather_2d_tile<T, 1>;
+        case 2: return k_gather_2d_tile<T, 2>;
+        case 3: return k_gather_2d_tile<T, 3>;
+        case 4: return k_gather_2d_tile<T, 4>;
+        case 5: return k_gather_2d_tile<T, 5>;
+        case 6: return k_gather_2d_tile<T, 6>;
+        case 7: return k_gather_2d_tile<T, 7>;
+    }
+    return nullptr;
+}
+
+// (tile, first node) of every chunk of <= kG2 nodes, built once per plan from seg_start
+static void ensure_gather2d_chunks(Plan& p, cudaStream_t st) {
+    if (p.chunks2d_n >= 0) return;
+    std::vector<int32_t> ss((size_t)p.nseg_tot + 1);
+    INFT_CUDA(cudaMemcpyAsync(ss.data(), p.seg_start.p, sizeof(int32_t) * ss.size(), cudaMemcpyDeviceToHost, st));
+    INFT_CUDA(cudaStreamSynchronize(st));
+    std::vector<int2> ch;
+    for (int64_t t = 0; t < p.nseg_tot; ++t)
+        for (int32_t i = ss[t]; i < ss[t + 1]; i += kG2) ch.push_back(make_int2((int)t, i));
+    p.chunks2d.alloc(sizeof(int2) * std::max<size_t>(1, ch.size()));
+    if (!ch.empty())
+        INFT_CUDA(cudaMemcpyAsync(p.chunks2d.p, ch.data(), sizeof(int2) * ch.size(), cudaMemcpyHostToDevice, st));
+    p.chunks2d_n = (int64_t)ch.size();
+}
+
 template <typename T>
 static void gather(Plan& p, const C2<T>* grid, C2<T>* f, int64_t R, cudaStream_t st) {
     if (p.N == 0) return;
@@ -555,6 +782,22 @@ static void gather(Plan& p, const C2<T>* grid, C2<T>* f, int64_t R, cudaStream_t
         return;
     }
     const T* w = p.w.as<T>();
+    if (tile2d_available(p) && !getenv_flag("INFT_GATHER2D_GENERIC")) {
+        ensure_gather2d_chunks(p, st);
+        if (p.chunks2d_n > 0) {
+            const int W = 16 + p.P1 - 1;
+            const size_t smem = sizeof(C2<T>) * 2 * W * 32 + sizeof(T) * (size_t)kG2 * p.PP;
+            Gather2dFn<T> fn = gather2d_fn<T>(p.m);
+            INFT_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+            dim3 g((unsigned)p.chunks2d_n, (unsigned)ceil_div(R, 32));
+            fn<<<g, 256, smem, st>>>(p.chunks2d.as<int2>(), p.seg_start.as<int32_t>(), p.n0s.as<int32_t>(),
+                                     p.perm.as<int32_t>(), w, p.PP, grid, f, p.N, (int)p.Ms[0], (int)p.Ms[1],
+                                     (int)p.nseg[1], (int)R, p.GS);
+            INFT_CHECK_LAUNCH();
+            p.launches++;
+        }
+        return;
+    }
     int64_t total = R * p.N;
     if (p.wt == INFT_WEIGHTS_COMPLEX)
         k_gather_generic<T, true><<<gs_blocks(total, 256), 256, 0, st>>>(p.n0s.as<int32_t>(), p.perm.as<int32_t>(), w,

@@ -117,6 +117,11 @@ struct Plan {
     // workspace
     DevBuf grid;          // [Rt][Mstot] complex (plan precision)
     DevBuf fT;            // 2-D spread: node-major copy of f, [N][R] (sorted node order)
+    DevBuf chunks2d;      // 2-D gather: (tile, first node) per chunk of <= 64 nodes
+    DevBuf work2d, comb2d, part2d;  // 2-D spread: work items, combine items, partial tiles
+    int64_t work2d_n = -1, comb2d_n = 0, part2d_rhs = 0;
+    int slots2d = 0;
+    int64_t chunks2d_n = -1;
     int64_t fT_rhs = 0;
     int64_t grid_rhs = 0; // capacity in RHS
     DevBuf stage_in[2], stage_out[2];
