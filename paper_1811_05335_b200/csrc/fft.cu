@@ -710,7 +710,9 @@ static void launch_pass_a(Plan& p, fft::Args<T>& A, int mode, const void* src, i
     const size_t smem = cs * (size_t)(2 * L * TA + SW * TA + L / fft::kRB) + 16;
     const int ntiles = (int)(R * (A.N2 / TA));
     INFT_CUDA(cudaFuncSetAttribute(ka, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    ka<<<(unsigned)std::min(ntiles, num_sms()), threads, smem, st>>>(map, dmap, A, BR, ntiles);
+    int occ = 1;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, ka, threads, smem);
+    ka<<<(unsigned)std::min(ntiles, num_sms() * std::max(1, occ)), threads, smem, st>>>(map, dmap, A, BR, ntiles);
     INFT_CHECK_LAUNCH();
     p.launches++;
 }
@@ -743,7 +745,9 @@ static void launch_pass_b(Plan& p, fft::Args<T>& A, int mode, int64_t R, cudaStr
     }
     const int ntiles = (int)(R * (A.N1 / TB));
     INFT_CUDA(cudaFuncSetAttribute(kb, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    kb<<<(unsigned)std::min(ntiles, num_sms()), threads, smem, st>>>(dmap, A, BRd, ntiles);
+    int occ = 1;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kb, threads, smem);
+    kb<<<(unsigned)std::min(ntiles, num_sms() * std::max(1, occ)), threads, smem, st>>>(dmap, A, BRd, ntiles);
     INFT_CHECK_LAUNCH();
     p.launches++;
 }

@@ -624,12 +624,24 @@ static void tmap_or_throw(CUtensorMap* m, const void* base, uint64_t inner, uint
     }
 }
 
+// segments per CTA: up to kQ, fewer when the batch is too small to give every SM ~8 CTAs
+// (config 3: 2048 segments x 2 row groups -> Q = 4)
+static int ring_q(int nseg, int64_t rowgroups) {
+    int dev = 0, nsm = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    const int64_t want = (int64_t)nsm * 8;
+    const int64_t q = ((int64_t)nseg * rowgroups + want - 1) / want;
+    return (int)std::max<int64_t>(2, std::min<int64_t>(ring::kQ, q));
+}
+
 template <typename T>
 static void ring_spread_t(Plan& p, const void* f, void* grid, int64_t R, cudaStream_t st) {
     RingFns<T> F = ring_fns<T>(p.m);
     const int wpb = ring_wpb<T>(R);
     const int nseg = (int)p.nseg[0];
-    const int nchunks = (int)ceil_div(nseg, ring::kQ);
+    const int Q = ring_q(nseg, ceil_div(R, 32 * wpb));
+    const int nchunks = (int)ceil_div(nseg, Q);
     const uint64_t ce = sizeof(C2<T>) / 8;
     CUtensorMap fm, gm;
     tmap_or_throw(&fm, f, (uint64_t)p.N * ce, (uint64_t)R, sizeof(C2<T>) * (uint64_t)p.N, 32u, "spread f");
@@ -637,8 +649,8 @@ static void ring_spread_t(Plan& p, const void* f, void* grid, int64_t R, cudaStr
     size_t smem = ring_spread_smem<T>(wpb, p.PP, p.S[0]);
     INFT_CUDA(cudaFuncSetAttribute(F.spread, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     dim3 g((unsigned)nchunks, (unsigned)ceil_div(R, 32 * wpb));
-    F.spread<<<g, 32 * wpb, smem, st>>>(fm, gm, p.seg_start.as<int32_t>(), p.w.as<T>(), p.PP, nseg, ring::kQ,
-                                        (int)p.N, p.perm_shift);
+    F.spread<<<g, 32 * wpb, smem, st>>>(fm, gm, p.seg_start.as<int32_t>(), p.w.as<T>(), p.PP, nseg, Q, (int)p.N,
+                                        p.perm_shift);
     INFT_CHECK_LAUNCH();
     p.launches++;
 }
@@ -659,7 +671,8 @@ static void ring_gather_t(Plan& p, const void* grid, void* f, int64_t R, cudaStr
     RingFns<T> F = ring_fns<T>(p.m);
     const int wpb = ring_wpb<T>(R);
     const int nseg = (int)p.nseg[0];
-    const int nchunks = (int)ceil_div(nseg, ring::kQ);
+    const int Q = ring_q(nseg, ceil_div(R, 32 * wpb));
+    const int nchunks = (int)ceil_div(nseg, Q);
     const uint64_t ce = sizeof(C2<T>) / 8;
     const int H = (int)(p.GS - p.Ms[0]);
     k_ring_halo<T><<<(unsigned)std::max<int64_t>(1, std::min<int64_t>(ceil_div(R * H, 256), 4096)), 256, 0, st>>>(
@@ -673,7 +686,7 @@ static void ring_gather_t(Plan& p, const void* grid, void* f, int64_t R, cudaStr
     INFT_CUDA(cudaFuncSetAttribute(F.gather, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     dim3 g((unsigned)nchunks, (unsigned)ceil_div(R, 32 * wpb));
     F.gather<<<g, 32 * wpb, smem, st>>>(gm, om, p.seg_start.as<int32_t>(), p.w.as<T>(), p.PP, static_cast<C2<T>*>(f),
-                                        p.N, nseg, ring::kQ, (int)R, p.perm_shift);
+                                        p.N, nseg, Q, (int)R, p.perm_shift);
     INFT_CHECK_LAUNCH();
     p.launches++;
 }
