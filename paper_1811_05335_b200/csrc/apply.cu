@@ -590,7 +590,7 @@ static void spread(Plan& p, const C2<T>* f, C2<T>* grid, int64_t R, cudaStream_t
             }
             dim3 g((unsigned)p.work2d_n, (unsigned)ceil_div(R, 32));
             const size_t smem = 2 * tile2d_stage_bytes<T>(p.PP);
-            INFT_CUDA(cudaFuncSetAttribute(tile2d_fn<T>(p.m), cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+            ensure_smem_attr((const void*)tile2d_fn<T>(p.m), smem);
             tile2d_fn<T>(p.m)<<<g, 256, smem, st>>>(p.work2d.as<int4>(), p.seg_start.as<int32_t>(), p.n0s.as<int32_t>(),
                                                  w, p.PP, fT, grid, p.part2d.as<C2<T>>(), (int)p.Ms[0],
                                                  (int)p.Ms[1], (int)p.nseg[0], (int)p.nseg[1], (int)R, p.GS);
@@ -788,7 +788,7 @@ static void gather(Plan& p, const C2<T>* grid, C2<T>* f, int64_t R, cudaStream_t
             const int W = 16 + p.P1 - 1;
             const size_t smem = sizeof(C2<T>) * 2 * W * 32 + sizeof(T) * (size_t)kG2 * p.PP;
             Gather2dFn<T> fn = gather2d_fn<T>(p.m);
-            INFT_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+            ensure_smem_attr((const void*)fn, smem);
             dim3 g((unsigned)p.chunks2d_n, (unsigned)ceil_div(R, 32));
             fn<<<g, 256, smem, st>>>(p.chunks2d.as<int2>(), p.seg_start.as<int32_t>(), p.n0s.as<int32_t>(),
                                      p.perm.as<int32_t>(), w, p.PP, grid, f, p.N, (int)p.Ms[0], (int)p.Ms[1],

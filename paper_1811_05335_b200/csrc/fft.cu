@@ -709,9 +709,8 @@ static void launch_pass_a(Plan& p, fft::Args<T>& A, int mode, const void* src, i
     }
     const size_t smem = cs * (size_t)(2 * L * TA + SW * TA + L / fft::kRB) + 16;
     const int ntiles = (int)(R * (A.N2 / TA));
-    INFT_CUDA(cudaFuncSetAttribute(ka, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    int occ = 1;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, ka, threads, smem);
+    ensure_smem_attr((const void*)ka, smem);
+    const int occ = occupancy_cached((const void*)ka, threads, smem);
     ka<<<(unsigned)std::min(ntiles, num_sms() * std::max(1, occ)), threads, smem, st>>>(map, dmap, A, BR, ntiles);
     INFT_CHECK_LAUNCH();
     p.launches++;
@@ -744,9 +743,8 @@ static void launch_pass_b(Plan& p, fft::Args<T>& A, int mode, int64_t R, cudaStr
         memset(&dmap, 0, sizeof(dmap));
     }
     const int ntiles = (int)(R * (A.N1 / TB));
-    INFT_CUDA(cudaFuncSetAttribute(kb, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    int occ = 1;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kb, threads, smem);
+    ensure_smem_attr((const void*)kb, smem);
+    const int occ = occupancy_cached((const void*)kb, threads, smem);
     kb<<<(unsigned)std::min(ntiles, num_sms() * std::max(1, occ)), threads, smem, st>>>(dmap, A, BRd, ntiles);
     INFT_CHECK_LAUNCH();
     p.launches++;

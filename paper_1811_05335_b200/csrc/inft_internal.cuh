@@ -43,6 +43,8 @@ struct Fail {
 // INFT_SYNC_CHECK=1: synchronize after every launch so a fault names its kernel's call site
 bool sync_check_enabled();
 bool getenv_flag(const char* name);  // name set to a nonzero integer
+void ensure_smem_attr(const void* fn, size_t smem);     // cached cudaFuncSetAttribute
+int occupancy_cached(const void* fn, int threads, size_t smem);
 #define INFT_CHECK_LAUNCH()                                                              \
     do {                                                                                 \
         cudaError_t e_ = cudaGetLastError();                                             \

@@ -13,11 +13,40 @@
 #include <limits>
 
 #include "common.cuh"
+#include <mutex>
+#include <map>
+#include <tuple>
+#include <unordered_map>
 #include "inft_internal.cuh"
 
 namespace inft {
 
 static thread_local std::string g_last_error;
+// Dynamic shared-memory attribute set once per (kernel, largest size so far) and occupancy
+// queried once per (kernel, threads, smem): both are driver calls on every apply otherwise.
+static std::mutex g_attr_mu;
+void ensure_smem_attr(const void* fn, size_t smem) {
+    static std::unordered_map<const void*, size_t> done;
+    std::lock_guard<std::mutex> g(g_attr_mu);
+    auto it = done.find(fn);
+    if (it != done.end() && it->second >= smem) return;
+    INFT_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    done[fn] = smem;
+}
+
+int occupancy_cached(const void* fn, int threads, size_t smem) {
+    static std::map<std::tuple<const void*, int, size_t>, int> done;
+    std::lock_guard<std::mutex> g(g_attr_mu);
+    auto key = std::make_tuple(fn, threads, smem);
+    auto it = done.find(key);
+    if (it != done.end()) return it->second;
+    int occ = 1;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, threads, smem) != cudaSuccess) occ = 1;
+    occ = occ < 1 ? 1 : occ;
+    done[key] = occ;
+    return occ;
+}
+
 bool getenv_flag(const char* name) {
     const char* e = getenv(name);
     return e && atoi(e) != 0;

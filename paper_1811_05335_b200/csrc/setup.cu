@@ -1066,7 +1066,7 @@ static void alg2(Plan& p, double tau, DevBuf& w64, cudaStream_t st) {
             DevBuf scratch;
             scratch.alloc(per * grid);
             const size_t smem = sizeof(double) * (packed_doubles(ksm) + rmax + 2) + sizeof(int) * (rmax + 2) + 16;
-            INFT_CUDA(cudaFuncSetAttribute(k_alg2_solve_lr, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+            ensure_smem_attr((const void*)k_alg2_solve_lr, smem);
             k_alg2_solve_lr<<<grid, 256, smem, st>>>(cc, gc, cols.as<int64_t>(), (int64_t)cls[k].size(),
                                                      cnt.as<int32_t>(), nmax, rmax, ksm, scratch.as<double>(), tau * tau,
                                                      1e-15, p.P, w64.as<double>(), ndrop.as<unsigned long long>(),
@@ -1094,7 +1094,7 @@ static void alg2(Plan& p, double tau, DevBuf& w64, cudaStream_t st) {
             smem = sizeof(int64_t) * nmax + sizeof(int) * (nmax + 1) + sizeof(double) * (nmax + 2) +
                    sizeof(int) * (nmax + 2) + sizeof(int) * 4 + 64;
         }
-        INFT_CUDA(cudaFuncSetAttribute(k_alg2_solve, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        ensure_smem_attr((const void*)k_alg2_solve, smem);
         k_alg2_solve<<<grid, threads[k], smem, st>>>(cc, gc, cols.as<int64_t>(), (int64_t)cls[k].size(),
                                                      cnt.as<int32_t>(), nmax, use_global,
                                                      use_global ? scratch.as<double>() : nullptr, tau * tau, p.P,
@@ -1161,7 +1161,7 @@ static void alg1(Plan& p, double tau, DevBuf& w64, cudaStream_t st) {
     int P = p.P;
     size_t smem = sizeof(double) * (2 * (size_t)P * (P + 1) + 3 * P) + sizeof(int) * (P + 1) +
                   sizeof(double) * (P + 2) + sizeof(int) * (P + 2) + sizeof(int) * 4 + 64;
-    INFT_CUDA(cudaFuncSetAttribute(k_alg1_solve, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    ensure_smem_attr((const void*)k_alg1_solve, smem);
     k_alg1_solve<<<(unsigned)std::min<int64_t>(N, 148 * 16), 64, smem, st>>>(
         K.as<double2>(), p.n0s.as<int32_t>(), l0s.as<int32_t>(), xs.as<double>(), N, Ms, p.m, P, (double)M,
         tau * tau, w64.as<double>(), ndrop.as<unsigned long long>());

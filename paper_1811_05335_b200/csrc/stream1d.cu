@@ -20,6 +20,10 @@
 #include <algorithm>
 #include <cstdlib>
 
+#include <cstring>
+#include <mutex>
+#include <unordered_map>
+
 #include "common.cuh"
 #include "inft_internal.cuh"
 #include "tma.cuh"
@@ -588,7 +592,7 @@ static void spread_t(Plan& p, const void* f, void* grid, int64_t R, cudaStream_t
             throw Fail{INFT_ERR_CUDA};
         }
         size_t smem = spread_smem<T>(rows, p.PP);
-        INFT_CUDA(cudaFuncSetAttribute(F.st, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        ensure_smem_attr((const void*)F.st, smem);
         dim3 grid_dim((unsigned)nchunks, (unsigned)ceil_div(R, rows));
         F.st<<<grid_dim, rows, smem, st>>>(map, p.seg_start.as<int32_t>(), p.w.as<T>(), p.PP,
                                            static_cast<C2<T>*>(grid), p.GS, nseg, kQ, (int)R, (int)p.N, p.perm_shift,
@@ -625,7 +629,7 @@ static void gather_t(Plan& p, const void* grid, void* f, int64_t R, cudaStream_t
             throw Fail{INFT_ERR_CUDA};
         }
         size_t smem = gather_smem<T>(rows, p.PP, p.S[0]);
-        INFT_CUDA(cudaFuncSetAttribute(F.gt, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        ensure_smem_attr((const void*)F.gt, smem);
         dim3 grid_dim((unsigned)nchunks, (unsigned)ceil_div(R, rows));
         F.gt<<<grid_dim, rows, smem, st>>>(map, p.seg_start.as<int32_t>(), p.w.as<T>(), p.PP, static_cast<C2<T>*>(f),
                                            p.N, nseg, kQ, (int)R, p.perm_shift, debug_flags());
@@ -669,8 +673,44 @@ static PFN_cuTensorMapEncodeTiled_v12000 tmap_encoder() {
     return encode;
 }
 
+// Encoded maps are cached by their arguments: an apply re-encodes the same few maps every call
+// (the encode is a driver call of about a microsecond; configs 1-2 are launch-latency bound).
+struct TmapKey {
+    const void* base;
+    uint64_t a[8];
+    bool operator==(const TmapKey& o) const {
+        return base == o.base && std::memcmp(a, o.a, sizeof(a)) == 0;
+    }
+};
+struct TmapKeyHash {
+    size_t operator()(const TmapKey& k) const {
+        size_t h = std::hash<const void*>()(k.base);
+        for (uint64_t v : k.a) h = h * 1000003u ^ std::hash<uint64_t>()(v);
+        return h;
+    }
+};
+static std::mutex g_tmap_mu;
+static std::unordered_map<TmapKey, CUtensorMap, TmapKeyHash>& tmap_cache() {
+    static std::unordered_map<TmapKey, CUtensorMap, TmapKeyHash> m;
+    return m;
+}
+static bool tmap_lookup(const TmapKey& k, CUtensorMap* out) {
+    std::lock_guard<std::mutex> g(g_tmap_mu);
+    auto it = tmap_cache().find(k);
+    if (it == tmap_cache().end()) return false;
+    *out = it->second;
+    return true;
+}
+static void tmap_store(const TmapKey& k, const CUtensorMap& m) {
+    std::lock_guard<std::mutex> g(g_tmap_mu);
+    if (tmap_cache().size() > 1024) tmap_cache().clear();
+    tmap_cache()[k] = m;
+}
+
 bool make_tmap_3d(CUtensorMap* out, const void* base, uint64_t d0, uint64_t d1, uint64_t d2, uint64_t s1,
                   uint64_t s2, uint32_t b0, uint32_t b1, int esize) {
+    const TmapKey key{base, {d0, d1, d2, s1, s2, b0, b1, (uint64_t)esize}};
+    if (tmap_lookup(key, out)) return true;
     PFN_cuTensorMapEncodeTiled_v12000 encode = tmap_encoder();
     if (!encode) return false;
     cuuint64_t dims[3] = {d0, d1, d2};
@@ -681,11 +721,15 @@ bool make_tmap_3d(CUtensorMap* out, const void* base, uint64_t d0, uint64_t d1, 
                         const_cast<void*>(base), dims, strides, box, estr,
                         CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                         CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-    return r == CUDA_SUCCESS;
+    if (r != CUDA_SUCCESS) return false;
+    tmap_store(key, *out);
+    return true;
 }
 
 bool make_tmap_2d(CUtensorMap* out, const void* base, uint64_t inner, uint64_t rows, uint64_t row_stride_bytes,
                   uint32_t box_rows) {
+    const TmapKey key{base, {inner, rows, row_stride_bytes, box_rows, ~0ull, 0, 0, 0}};
+    if (tmap_lookup(key, out)) return true;
     PFN_cuTensorMapEncodeTiled_v12000 encode = tmap_encoder();
     if (!encode) return false;
     cuuint64_t dims[2] = {inner, rows};
@@ -696,7 +740,9 @@ bool make_tmap_2d(CUtensorMap* out, const void* base, uint64_t inner, uint64_t r
                         const_cast<void*>(base), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
                         CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                         CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-    return r == CUDA_SUCCESS;
+    if (r != CUDA_SUCCESS) return false;
+    tmap_store(key, *out);
+    return true;
 }
 
 }  // namespace inft

@@ -647,7 +647,7 @@ static void ring_spread_t(Plan& p, const void* f, void* grid, int64_t R, cudaStr
     tmap_or_throw(&fm, f, (uint64_t)p.N * ce, (uint64_t)R, sizeof(C2<T>) * (uint64_t)p.N, 32u, "spread f");
     tmap_or_throw(&gm, grid, (uint64_t)p.GS * ce, (uint64_t)R, sizeof(C2<T>) * (uint64_t)p.GS, 32u, "spread grid");
     size_t smem = ring_spread_smem<T>(wpb, p.PP, p.S[0]);
-    INFT_CUDA(cudaFuncSetAttribute(F.spread, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    ensure_smem_attr((const void*)F.spread, smem);
     dim3 g((unsigned)nchunks, (unsigned)ceil_div(R, 32 * wpb));
     F.spread<<<g, 32 * wpb, smem, st>>>(fm, gm, p.seg_start.as<int32_t>(), p.w.as<T>(), p.PP, nseg, Q, (int)p.N,
                                         p.perm_shift);
@@ -683,7 +683,7 @@ static void ring_gather_t(Plan& p, const void* grid, void* f, int64_t R, cudaStr
     tmap_or_throw(&gm, grid, (uint64_t)p.GS * ce, (uint64_t)R, sizeof(C2<T>) * (uint64_t)p.GS, 32u, "gather grid");
     tmap_or_throw(&om, f, (uint64_t)p.N * ce, (uint64_t)R, sizeof(C2<T>) * (uint64_t)p.N, 32u, "gather f");
     size_t smem = ring_gather_smem<T>(wpb, p.PP, p.S[0]);
-    INFT_CUDA(cudaFuncSetAttribute(F.gather, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    ensure_smem_attr((const void*)F.gather, smem);
     dim3 g((unsigned)nchunks, (unsigned)ceil_div(R, 32 * wpb));
     F.gather<<<g, 32 * wpb, smem, st>>>(gm, om, p.seg_start.as<int32_t>(), p.w.as<T>(), p.PP, static_cast<C2<T>*>(f),
                                         p.N, nseg, Q, (int)R, p.perm_shift);
