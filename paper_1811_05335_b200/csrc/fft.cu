@@ -197,13 +197,18 @@ __device__ __forceinline__ void stage_regs(C2<T> (&a)[R], int j, const C2<T>* __
 #define INFT_FFT_RADIX 16
 #endif
 constexpr int kRB = INFT_FFT_RADIX;
+// elements per tile (4096: 64 KB at complex128, one CTA per SM; 2048: two CTAs per SM)
+#ifndef INFT_FFT_TILE
+#define INFT_FFT_TILE 4096
+#endif
+constexpr int kTileElems = INFT_FFT_TILE;
 constexpr int kLgRB = kRB == 16 ? 4 : (kRB == 8 ? 3 : 2);
 // TF independent length-L transforms per tile (compile-time: ~64 KB of shared memory, at
 // most 256 threads = TF L / 16, at most 8), thread t -> (f = t % TF, butterfly j = t / TF).
 // Static radix plan for L = 2^K: a first stage of radix 2^(K mod 4) (if any), then radix-16.
 template <typename T, int L>
 struct Geo {
-    static constexpr int TF = L >= 512 ? 4096 / L : 8;
+    static constexpr int TF = L >= kTileElems / 8 ? (kTileElems / L > 0 ? kTileElems / L : 1) : 8;
     static constexpr int NT = TF * L / kRB < 32 ? 32 : TF * L / kRB;  // threads per CTA
     // row padding of the [f][L + PAD] layout: the lanes of one 128-byte shared wavefront cover
     // TF transforms x (wavefront / TF) consecutive positions
@@ -462,10 +467,29 @@ __global__ void __launch_bounds__(Geo<T, L>::NT, 1)
         C2<T>* grow = A.grid + r * A.GS;
         C2<T>* frow = A.fhat + r * A.M;
         auto load = [&](int f, int n2, int, int) -> C2<T> { return tl[f * S + n2]; };
+        // MODE 0 with B2 a multiple of the last stage's span L/16 (e.g. sigma = 2): whether leg m
+        // is kept, its output address and its d slot follow from m alone (warp-uniform tests,
+        // one base per thread)
+        constexpr int NsL = L / 16;
+        const bool fastband = (B2 % NsL) == 0;
+        const int mlo = B2 / NsL;
+        const int jl = threadIdx.x / TB, fl = threadIdx.x - (threadIdx.x / TB) * TB;
+        const int64_t cb = (int64_t)(row0 + fl) + (int64_t)N1 * jl;
+        const int doff = (row0 & (DW - 1)) + fl;
         auto store = [&](int f, int k2, C2<T> v, int m) {
             const int64_t k = (int64_t)(row0 + f) + (int64_t)N1 * k2;
             if (MODE == 0) {
                 if (m == 0) mbar_wait(&bars[2], it & 1);
+                if (fastband) {
+                    if (m < mlo) {
+                        const T d = dsm[(jl + m * NsL) * DW + doff];
+                        frow[cb + half + (int64_t)m * NsL * N1] = mk<T>(d * v.x, d * v.y);
+                    } else if (m >= 16 - mlo) {
+                        const T d = dsm[(jl + m * NsL - (L - 2 * B2)) * DW + doff];
+                        frow[cb - (A.N - half) + (int64_t)m * NsL * N1] = mk<T>(d * v.x, d * v.y);
+                    }
+                    return;
+                }
                 int64_t c;
                 int sr;
                 if (k2 < B2) {
@@ -540,7 +564,7 @@ bool fused_fft_available(const Plan& p) {
     // pass A of the adjoint stages d (2B rows x >= 16 bytes) in the tile's unused middle rows
     {
         const int N1 = split_n1(N);
-        const int TF = N1 >= 512 ? 4096 / N1 : 8;
+        const int TF = N1 >= fft::kTileElems / 8 ? std::max(1, fft::kTileElems / N1) : 8;
         const size_t cs = p.prec == INFT_C128 ? 16 : 8, ds = cs / 2;
         const size_t dw = std::max<size_t>((size_t)TF, 16 / ds);
         if ((size_t)(N1 - 2 * B) * TF * cs < (size_t)2 * B * dw * ds) return false;
@@ -551,7 +575,7 @@ bool fused_fft_available(const Plan& p) {
     {
         const int64_t B2 = half / split_n1(N);
         const size_t ds = p.prec == INFT_C128 ? 8 : 4;
-        const int TF = N2 >= 512 ? (int)(4096 / N2) : 8;
+        const int TF = N2 >= fft::kTileElems / 8 ? std::max(1, (int)(fft::kTileElems / N2)) : 8;
         const size_t dw = std::max<size_t>((size_t)TF, 16 / ds);
         const size_t smem = p.prec == INFT_C128 ? pass_b_smem<double>((int)N2, split_n1(N), p.M[0], 0)
                                                 : pass_b_smem<float>((int)N2, split_n1(N), p.M[0], 0);
