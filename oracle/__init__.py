@@ -107,11 +107,39 @@ def window_hat_vector(M, sigma, m):
     return kb_what(k, Ms, m, sigma)
 
 
-def deconv_vector(M, sigma, m, s=1.0):
+def inv_what_vector(M, sigma, m, window="kb"):
+    """1/what(k) for k = -M/2..M/2-1 (centered).
+    window='kb': the Kaiser-Bessel window (reading A7).
+    window='dirichlet': the Dirichlet-kernel variant of Remarks P:934-957 and P:1343-1358:
+    what(k) = 1 for k = -M/2+1..M/2-1 and the entry of D^* at the unpaired frequency set to
+    zero (the text names it 1/what(M/2); in the centred range -M/2..M/2-1 it is k = -M/2,
+    reading A21)."""
+    if window == "kb":
+        return 1.0 / window_hat_vector(M, sigma, m)
+    if window == "dirichlet":
+        v = np.ones(M)
+        v[0] = 0.0
+        return v
+    raise ValueError(f"unknown window {window!r}")
+
+
+def dirichlet_kernel(x, M):
+    """D_{M/2-1}(x) = sin((M-1) pi x) / sin(pi x), eq. kernel_Dirichlet P:937-944 (closed form;
+    the limit M-1 at integer x)."""
+    x = np.asarray(x, dtype=np.float64)
+    sx = np.sin(np.pi * x)
+    with np.errstate(divide="ignore", invalid="ignore"):
+        v = np.sin((M - 1) * np.pi * x) / sx
+    return np.where(np.abs(sx) < 1e-300, float(M - 1), v)
+
+
+def deconv_vector(M, sigma, m, s=1.0, window="kb"):
     """d_k = s / (M_sigma what(k)) -- the diagonal of D (eq. matrix_D)
     with the apply scale s folded in (reading A2)."""
     Ms = msigma(M, sigma)
-    return s / (Ms * window_hat_vector(M, sigma, m))
+    if window == "kb":
+        return s / (Ms * window_hat_vector(M, sigma, m))
+    return s * inv_what_vector(M, sigma, m, window) / Ms
 
 
 # ============================================================= index sets
@@ -260,39 +288,38 @@ def dense_from_slots_2d(w, l0, Msig, P):
     return B
 
 
-def dense_inverse(x, M, sigma, m, w, s, f):
+def dense_inverse(x, M, sigma, m, w, s, f, window="kb"):
     """Dense-literal inverse NFFT  s D^* F^* B_opt^* f  (P:631 / P:1279), f [R][N]."""
     x = np.asarray(x, dtype=np.float64)
     if x.ndim == 1:
         Ms = msigma(M, sigma)
         B = dense_from_slots(w, node_base(x, Ms, m), Ms)
-        D = np.diag(1.0 / (Ms * window_hat_vector(M, sigma, m)))
+        D = np.diag(deconv_vector(M, sigma, m, 1.0, window))
         F = matrix_F(M, Ms)
     else:
-        B, D, F = _dense_2d_factors(x, M, sigma, m, w)
+        B, D, F = _dense_2d_factors(x, M, sigma, m, w, window)
     return (s * D.conj() @ F.conj().T @ B.conj().T @ np.asarray(f).T).T
 
 
-def dense_adjoint(x, M, sigma, m, w, s, h):
+def dense_adjoint(x, M, sigma, m, w, s, h, window="kb"):
     """Dense-literal inverse adjoint NFFT  s B_opt F D h  (P:1116 / P:1522), h [R][M]."""
     x = np.asarray(x, dtype=np.float64)
     if x.ndim == 1:
         Ms = msigma(M, sigma)
         B = dense_from_slots(w, node_base(x, Ms, m), Ms)
-        D = np.diag(1.0 / (Ms * window_hat_vector(M, sigma, m)))
+        D = np.diag(deconv_vector(M, sigma, m, 1.0, window))
         F = matrix_F(M, Ms)
     else:
-        B, D, F = _dense_2d_factors(x, M, sigma, m, w)
+        B, D, F = _dense_2d_factors(x, M, sigma, m, w, window)
     return (s * B @ F @ D @ np.asarray(h).T).T
 
 
-def _dense_2d_factors(x, M, sigma, m, w):
+def _dense_2d_factors(x, M, sigma, m, w, window="kb"):
     M1, M2 = M
     S = (msigma(M1, sigma), msigma(M2, sigma))
     l0 = np.stack([node_base(x[:, 0], S[0], m), node_base(x[:, 1], S[1], m)], axis=1)
     B = dense_from_slots_2d(w, l0, S, (2 * m + 1, 2 * m + 1))
-    D = np.diag(np.kron(1.0 / (S[0] * window_hat_vector(M1, sigma, m)),
-                        1.0 / (S[1] * window_hat_vector(M2, sigma, m))))
+    D = np.diag(np.kron(deconv_vector(M1, sigma, m, 1.0, window), deconv_vector(M2, sigma, m, 1.0, window)))
     F = np.kron(matrix_F(M1, S[0]), matrix_F(M2, S[1]))
     return B, D, F
 
@@ -345,31 +372,33 @@ def solve_minnorm_gram(G, y, tau=TAU_DEFAULT):
 
 
 # ------------------------------------------------ Alg. 2 ingredients
-def L_explicit(l, xs, M, sigma, m):
+def L_explicit(l, xs, M, sigma, m, window="kb"):
     """L_l = F D H_l (eq. matrix_Ll) for the nodes xs = {x_j : j in I(l)}:
     H_l = (e^{-2 pi i k x_j})_{k, j}; returns [M_sigma][|I(l)|]; row s <-> s - Msig/2."""
     Ms = msigma(M, sigma)
     k = np.arange(-M // 2, M // 2)
     H = np.exp(-2j * np.pi * np.outer(k, np.asarray(xs)))
-    D = 1.0 / (Ms * window_hat_vector(M, sigma, m))
+    D = deconv_vector(M, sigma, m, 1.0, window)
     return matrix_F(M, Ms) @ (D[:, None] * H)
 
 
-def G_kernel(dx, M, sigma, m):
+def G_kernel(dx, M, sigma, m, window="kb"):
     """G(x) = (1/M_sigma) sum_k e^{2 pi i k x} / what(k)^2 (complex), direct sum.
     (L_l^* L_l)_{jj'} = G(x_j - x_j') by F^*F = M_sigma I_M (Gram form)."""
     Ms = msigma(M, sigma)
     k = np.arange(-M // 2, M // 2)
-    c = 1.0 / window_hat_vector(M, sigma, m) ** 2 / Ms
+    c = (1.0 / window_hat_vector(M, sigma, m) ** 2 / Ms if window == "kb"
+         else inv_what_vector(M, sigma, m, window) ** 2 / Ms)
     dx = np.asarray(dx, dtype=np.float64)
     return np.exp(2j * np.pi * dx[..., None] * k) @ c
 
 
-def Kplus_kernel(dx, M, sigma, m):
+def Kplus_kernel(dx, M, sigma, m, window="kb"):
     """K+(x) = (1/M_sigma) sum_k e^{2 pi i k x} / what(k): (L_l^* e_l)_j = K+(x_j - l/M_sigma)."""
     Ms = msigma(M, sigma)
     k = np.arange(-M // 2, M // 2)
-    c = 1.0 / window_hat_vector(M, sigma, m) / Ms
+    c = (1.0 / window_hat_vector(M, sigma, m) / Ms if window == "kb"
+         else inv_what_vector(M, sigma, m, window) / Ms)
     dx = np.asarray(dx, dtype=np.float64)
     return np.exp(2j * np.pi * dx[..., None] * k) @ c
 
@@ -380,7 +409,7 @@ def wrap_diff(a):
     return a - np.floor(a + 0.5)
 
 
-def alg2_setup(x, M, sigma, m, tau=TAU_DEFAULT, form="explicit", columns=None, weights="real"):
+def alg2_setup(x, M, sigma, m, tau=TAU_DEFAULT, form="explicit", columns=None, weights="real", window="kb"):
     """Alg. "Fast optimization of the matrix B", per grid point l:
     J = I_{Msig,m}(l) (eq. set_l), minimise ||L_l b - e_l|| with the
     minimum-norm cutoff (A6); store B_opt[j, l] = b_j as slot weight.
@@ -390,7 +419,7 @@ def alg2_setup(x, M, sigma, m, tau=TAU_DEFAULT, form="explicit", columns=None, w
     Returns (w [N][2m+1], info dict)."""
     x = np.asarray(x, dtype=np.float64)
     if x.ndim == 2:
-        return _alg2_setup_2d(x, M, sigma, m, tau, form, columns, weights)
+        return _alg2_setup_2d(x, M, sigma, m, tau, form, columns, weights, window)
     Ms = msigma(M, sigma)
     N = x.size
     P = 2 * m + 1
@@ -410,7 +439,7 @@ def alg2_setup(x, M, sigma, m, tau=TAU_DEFAULT, form="explicit", columns=None, w
             continue
         l = n - Ms if n >= Ms // 2 else n  # grid index in [-Msig/2, Msig/2)
         if form == "explicit":
-            Lm = L_explicit(l, x[js], M, sigma, m)
+            Lm = L_explicit(l, x[js], M, sigma, m, window)
             e = np.zeros(Ms, dtype=np.complex128)
             e[l + Ms // 2] = 1.0
             b, nd = lstsq_minnorm_svd(Lm, e, tau, real=not cplx)
@@ -419,8 +448,8 @@ def alg2_setup(x, M, sigma, m, tau=TAU_DEFAULT, form="explicit", columns=None, w
             if cplx:
                 raise NotImplementedError("complex weights use the explicit form in the oracle")
             dx = wrap_diff(x[js][:, None] - x[js][None, :])
-            G = np.real(G_kernel(dx, M, sigma, m))
-            y = np.real(Kplus_kernel(wrap_diff(x[js] - l / Ms), M, sigma, m))
+            G = np.real(G_kernel(dx, M, sigma, m, window))
+            y = np.real(Kplus_kernel(wrap_diff(x[js] - l / Ms), M, sigma, m, window))
             b, nd = solve_minnorm_gram(G, y, tau)
             # ||L b - e||^2 = b^T G b - 2 b^T y + 1 for real b
             resid[n] = float(np.sqrt(max(b @ G @ b - 2 * b @ y + 1.0, 0.0)))
@@ -429,7 +458,7 @@ def alg2_setup(x, M, sigma, m, tau=TAU_DEFAULT, form="explicit", columns=None, w
     return w, dict(n_rank_deficient=rank_def, max_col_size=max_col, resid=resid)
 
 
-def _alg2_setup_2d(x, M, sigma, m, tau, form, columns, weights):
+def _alg2_setup_2d(x, M, sigma, m, tau, form, columns, weights, window="kb"):
     """Tensor-product reading A12 of Alg. 2: I(x_j) = I1 x I2, grid l = (l1, l2)."""
     M1, M2 = M
     S1, S2 = msigma(M1, sigma), msigma(M2, sigma)
@@ -449,8 +478,8 @@ def _alg2_setup_2d(x, M, sigma, m, tau, form, columns, weights):
     cols = range(S1 * S2) if columns is None else columns
     k1 = np.arange(-M1 // 2, M1 // 2)
     k2 = np.arange(-M2 // 2, M2 // 2)
-    D1 = 1.0 / (S1 * window_hat_vector(M1, sigma, m))
-    D2 = 1.0 / (S2 * window_hat_vector(M2, sigma, m))
+    D1 = deconv_vector(M1, sigma, m, 1.0, window)
+    D2 = deconv_vector(M2, sigma, m, 1.0, window)
     rank_def = 0
     max_col = 0
     resid = {}
@@ -476,11 +505,11 @@ def _alg2_setup_2d(x, M, sigma, m, tau, form, columns, weights):
             resid[n] = float(np.linalg.norm(Lm @ b - e))
         else:
             xs = x[js]
-            g1 = G_kernel(wrap_diff(xs[:, None, 0] - xs[None, :, 0]), M1, sigma, m)
-            g2 = G_kernel(wrap_diff(xs[:, None, 1] - xs[None, :, 1]), M2, sigma, m)
+            g1 = G_kernel(wrap_diff(xs[:, None, 0] - xs[None, :, 0]), M1, sigma, m, window)
+            g2 = G_kernel(wrap_diff(xs[:, None, 1] - xs[None, :, 1]), M2, sigma, m, window)
             G = np.real(g1 * g2)
-            y = np.real(Kplus_kernel(wrap_diff(xs[:, 0] - l1 / S1), M1, sigma, m) *
-                        Kplus_kernel(wrap_diff(xs[:, 1] - l2 / S2), M2, sigma, m))
+            y = np.real(Kplus_kernel(wrap_diff(xs[:, 0] - l1 / S1), M1, sigma, m, window) *
+                        Kplus_kernel(wrap_diff(xs[:, 1] - l2 / S2), M2, sigma, m, window))
             b, nd = solve_minnorm_gram(G, y, tau)
             resid[n] = float(np.sqrt(max(b @ G @ b - 2 * b @ y + 1.0, 0.0)))
         rank_def += nd > 0
@@ -489,17 +518,17 @@ def _alg2_setup_2d(x, M, sigma, m, tau, form, columns, weights):
 
 
 # ------------------------------------------------ Alg. 1 ingredients
-def K_kernel_matrix(x, M, sigma, m):
+def K_kernel_matrix(x, M, sigma, m, window="kb"):
     """K = A D^* F^* = (K(x_h - l/M_sigma))_{h, l} with K(x) = (1/M_sigma)
     sum_k e^{2 pi i k x}/what(-k) (eqs. matrix_K, kernel P:734-757), formed as
     the literal matrix product."""
     Ms = msigma(M, sigma)
     A = matrix_A(x, M)
-    D = 1.0 / (Ms * window_hat_vector(M, sigma, m))
+    D = deconv_vector(M, sigma, m, 1.0, window)
     return A @ (D.conj()[:, None] * matrix_F(M, Ms).conj().T)
 
 
-def alg1_setup(x, M, sigma, m, tau=TAU_DEFAULT, weights="real"):
+def alg1_setup(x, M, sigma, m, tau=TAU_DEFAULT, weights="real", window="kb"):
     """Alg. "Fast optimization of the matrix B*": per node j minimise
     ||K_j b - M e_j|| (eq. opt_ansatz1), K_j = columns l in I(x_j) of
     K (eq. matrix_Kj); b~_j is column j of B_opt^* (P:858), stored conjugated as
@@ -508,7 +537,7 @@ def alg1_setup(x, M, sigma, m, tau=TAU_DEFAULT, weights="real"):
     Ms = msigma(M, sigma)
     N = x.size
     P = 2 * m + 1
-    K = K_kernel_matrix(x, M, sigma, m)
+    K = K_kernel_matrix(x, M, sigma, m, window)
     l0 = node_base(x, Ms, m)
     live = slot_live(x, Ms, m)
     cplx = weights == "complex"
@@ -529,20 +558,20 @@ def alg1_setup(x, M, sigma, m, tau=TAU_DEFAULT, weights="real"):
 
 
 # ------------------------------------------------ objectives
-def objective_alg2(x, M, sigma, m, w):
+def objective_alg2(x, M, sigma, m, w, window="kb"):
     """||F D A^* B - I_{M_sigma}||_F (eq. matrixnorm_opt_ansatz2)."""
     Ms = msigma(M, sigma)
     B = dense_from_slots(w, node_base(x, Ms, m), Ms)
-    D = np.diag(1.0 / (Ms * window_hat_vector(M, sigma, m)))
+    D = np.diag(deconv_vector(M, sigma, m, 1.0, window))
     X = matrix_F(M, Ms) @ D @ matrix_A(x, M).conj().T @ B
     return float(np.linalg.norm(X - np.eye(Ms)))
 
 
-def objective_alg1(x, M, sigma, m, w):
+def objective_alg1(x, M, sigma, m, w, window="kb"):
     """||A D^* F^* B^* - M I_N||_F (eq. matrixnorm_opt_ansatz1)."""
     Ms = msigma(M, sigma)
     B = dense_from_slots(w, node_base(x, Ms, m), Ms)
-    X = K_kernel_matrix(x, M, sigma, m) @ B.conj().T
+    X = K_kernel_matrix(x, M, sigma, m, window) @ B.conj().T
     return float(np.linalg.norm(X - M * np.eye(len(x))))
 
 
@@ -604,7 +633,7 @@ def _split_w(w):
     return np.ascontiguousarray(w, dtype=np.float64), None
 
 
-def apply_inverse(x, M, sigma, m, w, s, f, nthreads=0):
+def apply_inverse(x, M, sigma, m, w, s, f, nthreads=0, window="kb"):
     """Fast oracle inverse NFFT  s D^* F^* B_opt^* f  (C loops), f [R][N] complex."""
     x = np.asarray(x, dtype=np.float64)
     f = np.ascontiguousarray(np.asarray(f, dtype=np.complex128))
@@ -613,7 +642,7 @@ def apply_inverse(x, M, sigma, m, w, s, f, nthreads=0):
     if x.ndim == 1:
         Ms = msigma(M, sigma)
         l0 = np.ascontiguousarray(node_base(x, Ms, m))
-        d = np.ascontiguousarray(deconv_vector(M, sigma, m, s))
+        d = np.ascontiguousarray(deconv_vector(M, sigma, m, s, window))
         out = np.zeros((R, M), dtype=np.complex128)
         rc = _clib().oracle_inverse_1d(x.size, M, Ms, 2 * m + 1, _ptr(l0), _ptr(wre), _ptr(wim),
                                        _ptr(d), _ptr(f), _ptr(out), R, nthreads)
@@ -623,8 +652,8 @@ def apply_inverse(x, M, sigma, m, w, s, f, nthreads=0):
         Mv = np.array([M1, M2], dtype=np.int64)
         Pv = np.array([2 * m + 1, 2 * m + 1], dtype=np.int32)
         l0 = np.ascontiguousarray(np.stack([node_base(x[:, 0], S[0], m), node_base(x[:, 1], S[1], m)], 1))
-        d1 = np.ascontiguousarray(deconv_vector(M1, sigma, m, s))
-        d2 = np.ascontiguousarray(deconv_vector(M2, sigma, m, 1.0))
+        d1 = np.ascontiguousarray(deconv_vector(M1, sigma, m, s, window))
+        d2 = np.ascontiguousarray(deconv_vector(M2, sigma, m, 1.0, window))
         out = np.zeros((R, M1 * M2), dtype=np.complex128)
         rc = _clib().oracle_inverse_2d(x.shape[0], _ptr(Mv), _ptr(S), _ptr(Pv), _ptr(l0), _ptr(wre),
                                        _ptr(wim), _ptr(d1), _ptr(d2), _ptr(f), _ptr(out), R, nthreads)
@@ -633,7 +662,7 @@ def apply_inverse(x, M, sigma, m, w, s, f, nthreads=0):
     return out
 
 
-def apply_adjoint(x, M, sigma, m, w, s, h, nthreads=0):
+def apply_adjoint(x, M, sigma, m, w, s, h, nthreads=0, window="kb"):
     """Fast oracle inverse adjoint NFFT  s B_opt F D h  (C loops), h [R][prod M] complex."""
     x = np.asarray(x, dtype=np.float64)
     h = np.ascontiguousarray(np.asarray(h, dtype=np.complex128))
@@ -644,7 +673,7 @@ def apply_adjoint(x, M, sigma, m, w, s, h, nthreads=0):
     if x.ndim == 1:
         Ms = msigma(M, sigma)
         l0 = np.ascontiguousarray(node_base(x, Ms, m))
-        d = np.ascontiguousarray(deconv_vector(M, sigma, m, s))
+        d = np.ascontiguousarray(deconv_vector(M, sigma, m, s, window))
         rc = _clib().oracle_adjoint_1d(N, M, Ms, 2 * m + 1, _ptr(l0), _ptr(wre), _ptr(wim),
                                        _ptr(d), _ptr(h), _ptr(out), R, nthreads)
     else:
@@ -653,8 +682,8 @@ def apply_adjoint(x, M, sigma, m, w, s, h, nthreads=0):
         Mv = np.array([M1, M2], dtype=np.int64)
         Pv = np.array([2 * m + 1, 2 * m + 1], dtype=np.int32)
         l0 = np.ascontiguousarray(np.stack([node_base(x[:, 0], S[0], m), node_base(x[:, 1], S[1], m)], 1))
-        d1 = np.ascontiguousarray(deconv_vector(M1, sigma, m, s))
-        d2 = np.ascontiguousarray(deconv_vector(M2, sigma, m, 1.0))
+        d1 = np.ascontiguousarray(deconv_vector(M1, sigma, m, s, window))
+        d2 = np.ascontiguousarray(deconv_vector(M2, sigma, m, 1.0, window))
         rc = _clib().oracle_adjoint_2d(N, _ptr(Mv), _ptr(S), _ptr(Pv), _ptr(l0), _ptr(wre),
                                        _ptr(wim), _ptr(d1), _ptr(d2), _ptr(h), _ptr(out), R, nthreads)
     if rc:
