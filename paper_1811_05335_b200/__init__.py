@@ -28,7 +28,7 @@ INFT_OK = 0
 STATUS = {0: "INFT_OK", 1: "INFT_ERR_INVALID_ARG", 2: "INFT_ERR_NODE_RANGE", 3: "INFT_ERR_ZERO_WINDOW_HAT",
           4: "INFT_ERR_NOT_PRECOMPUTED", 5: "INFT_ERR_CUDA", 6: "INFT_ERR_CUFFT", 7: "INFT_ERR_OOM",
           8: "INFT_ERR_UNSUPPORTED"}
-INFT_KAISER_BESSEL = 0
+INFT_KAISER_BESSEL, INFT_DIRICHLET = 0, 1
 INFT_AUTO, INFT_ALG1_NODEWISE, INFT_ALG2_GRIDWISE, INFT_PLAIN_NFFT = 0, 1, 2, 3
 INFT_C128, INFT_C64 = 0, 1
 INFT_WEIGHTS_REAL, INFT_WEIGHTS_COMPLEX = 0, 1
@@ -123,7 +123,7 @@ def _stream_ptr(stream):
 class Plan:
     """A plan for fixed nodes: nodes [N] or [N][2] float64 in [-1/2, 1/2)."""
 
-    def __init__(self, nodes, M, sigma, m, precision="c128", device=0, stream=None):
+    def __init__(self, nodes, M, sigma, m, precision="c128", device=0, stream=None, window="kb"):
         if isinstance(M, int):
             M = (M,)
         self.d = len(M)
@@ -142,8 +142,11 @@ class Plan:
         self.prec = INFT_C128 if precision in ("c128", INFT_C128) else INFT_C64
         Marr = (ctypes.c_int64 * self.d)(*self.M)
         h = ctypes.c_void_p()
-        _check(inft_plan(ctypes.byref(h), self.d, Marr, self.N, nptr, float(sigma), int(m), INFT_KAISER_BESSEL,
+        win = {"kb": INFT_KAISER_BESSEL, "dirichlet": INFT_DIRICHLET}[window] if isinstance(window, str) \
+            else int(window)
+        _check(inft_plan(ctypes.byref(h), self.d, Marr, self.N, nptr, float(sigma), int(m), win,
                          self.prec, int(device), _stream_ptr(stream)), "inft_plan")
+        self.window = window
         self._h = h
         self.sigma = float(sigma)
         self.m = int(m)

@@ -97,6 +97,7 @@ struct Plan {
 
     // method state
     int method = -1;
+    inft_window window = INFT_KAISER_BESSEL;
     inft_weights wt = INFT_WEIGHTS_REAL;
     double scale = 1.0;
     double tau = 1e-6;

@@ -213,9 +213,13 @@ __global__ void k_sorted_ints(const int32_t* __restrict__ perm, const int32_t* _
 
 // d_k = s / (M_sigma what(k)) = s / I0(m sqrt(b^2 - (2 pi k/M_sigma)^2)), k = -M/2..M/2-1.
 __global__ void k_deconv(double* __restrict__ dk, int64_t M, int64_t Ms, int m, double sigma, double s,
-                         int* __restrict__ bad) {
+                         int dirichlet, int* __restrict__ bad) {
     int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (c >= M) return;
+    if (dirichlet) {  // what = 1, the unpaired k = -M/2 (c = 0) zeroed (reading A21)
+        dk[c] = c == 0 ? 0.0 : s / (double)Ms;
+        return;
+    }
     double k = (double)(c - M / 2);
     const double pi = 3.141592653589793238462643383279502884;
     double b = pi * (2.0 - 1.0 / sigma);
@@ -424,7 +428,7 @@ void compute_deconv(Plan& p, double s, cudaStream_t st) {
     for (int i = 0; i < p.d; i++) {
         double* dst = p.dk.as<double>() + (i == 0 ? 0 : p.M[0]);
         k_deconv<<<grid1d(p.M[i]), 256, 0, st>>>(dst, p.M[i], p.Ms[i], p.m, p.sigma, i == 0 ? s : 1.0,
-                                                 flag.as<int>());
+                                                 p.window == INFT_DIRICHLET ? 1 : 0, flag.as<int>());
         INFT_CHECK_LAUNCH();
         p.launches++;
     }
@@ -562,7 +566,8 @@ inft_status inft_plan(inft_plan_t* out, int d, const int64_t* M, int64_t N, cons
                       int m, inft_window window, inft_precision prec, int device, inft_stream_t stream) {
     if (!out) return INFT_ERR_INVALID_ARG;
     *out = nullptr;
-    if (d < 1 || d > 2 || !M || N < 0 || (N > 0 && !nodes) || window != INFT_KAISER_BESSEL ||
+    if (d < 1 || d > 2 || !M || N < 0 || (N > 0 && !nodes) ||
+        (window != INFT_KAISER_BESSEL && window != INFT_DIRICHLET) ||
         (prec != INFT_C128 && prec != INFT_C64) || !(sigma >= 1.0) || m < 1 || N > INT32_MAX) {
         inft::set_error("inft_plan: invalid argument");
         return INFT_ERR_INVALID_ARG;
@@ -578,6 +583,7 @@ inft_status inft_plan(inft_plan_t* out, int d, const int64_t* M, int64_t N, cons
     inft::DeviceGuard g(device);
     p = new Plan();
     p->device = device;
+    p->window = window;
     p->d = d;
     p->N = N;
     p->m = m;

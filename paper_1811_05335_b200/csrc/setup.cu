@@ -113,9 +113,13 @@ __global__ void k_col_count(ColCtx c, int64_t ncol, int32_t* __restrict__ cnt) {
 
 // ------------------------------------------------------------------ kernel tables
 // 1/(M_sigma what(k)) = 1/I0(m sqrt(b^2 - (2 pi k/Ms)^2)) for k = 0..M/2 (even window).
-__global__ void k_inv_what(double* __restrict__ iw, int64_t M, int64_t Ms, int m, double sigma) {
+__global__ void k_inv_what(double* __restrict__ iw, int64_t M, int64_t Ms, int m, double sigma, int dirichlet) {
     int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (k > M / 2) return;
+    if (dirichlet) {  // what = 1; the unpaired frequency (stored at k = M/2) zeroed (reading A21)
+        iw[k] = k == M / 2 ? 0.0 : 1.0 / (double)Ms;
+        return;
+    }
     double b = kPi * (2.0 - 1.0 / sigma);
     double u = 2.0 * kPi * (double)k / (double)Ms;
     iw[k] = 1.0 / cyl_bessel_i0((double)m * sqrt(fmax(__dsub_rn(__dmul_rn(b, b), __dmul_rn(u, u)), 0.0)));
@@ -937,7 +941,8 @@ struct Tables {
 static void build_tables(Plan& p, int dim, Tables& T, double X, cudaStream_t st) {
     const int64_t M = p.M[dim], Ms = p.Ms[dim];
     T.iw.alloc(sizeof(double) * (M / 2 + 1));
-    k_inv_what<<<nblk(M / 2 + 1), 256, 0, st>>>(T.iw.as<double>(), M, Ms, p.m, p.sigma);
+    k_inv_what<<<nblk(M / 2 + 1), 256, 0, st>>>(T.iw.as<double>(), M, Ms, p.m, p.sigma,
+                                                 p.window == INFT_DIRICHLET ? 1 : 0);
     INFT_CHECK_LAUNCH();
     p.launches++;
     // piece width 2h with (pi M) h <= 1: |phase change| <= 1 rad per half piece
@@ -1140,7 +1145,8 @@ static void alg1(Plan& p, double tau, DevBuf& w64, cudaStream_t st) {
     k_sorted_nodes<<<nblk(N), 256, 0, st>>>(p.nodes.as<double>(), p.l0.as<int32_t>(), p.perm.as<int32_t>(), N, 1,
                                             xs.as<double>(), l0s.as<int32_t>());
     iw.alloc(sizeof(double) * (M / 2 + 1));
-    k_inv_what<<<nblk(M / 2 + 1), 256, 0, st>>>(iw.as<double>(), M, Ms, p.m, p.sigma);
+    k_inv_what<<<nblk(M / 2 + 1), 256, 0, st>>>(iw.as<double>(), M, Ms, p.m, p.sigma,
+                                                 p.window == INFT_DIRICHLET ? 1 : 0);
     K.alloc(sizeof(double2) * N * Ms);
     k_alg1_rows<<<nblk(N * Ms), 256, 0, st>>>(xs.as<double>(), iw.as<double>(), N, M, Ms, K.as<double2>());
     INFT_CHECK_LAUNCH();
@@ -1189,6 +1195,10 @@ void precompute(Plan& p, inft_method method, inft_weights wt, double tau, cudaSt
     p.n_rank_deficient = p.n_empty_cols = p.max_col_size = 0;
     p.tau = tau;
     if (method == INFT_PLAIN_NFFT) {
+        if (p.window != INFT_KAISER_BESSEL) {
+            set_error("INFT_PLAIN_NFFT needs a window function in space (Kaiser-Bessel)");
+            throw Fail{INFT_ERR_INVALID_ARG};
+        }
         if (p.N > 0) {
             DevBuf xs, l0s;
             xs.alloc(sizeof(double) * p.N * p.d);
