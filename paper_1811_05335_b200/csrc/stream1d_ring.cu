@@ -36,7 +36,11 @@ namespace ring {
 #endif
 constexpr int kQ = 32;                     // segments per chunk (one CTA)
 constexpr int kNB = INFT_RING_NB;          // nodes per staged batch
-constexpr int kStages = INFT_RING_STAGES;  // load pipeline depth (2: more CTAs per SM beat a deeper pipe)
+constexpr int kStages = INFT_RING_STAGES;  // spread load pipeline depth (2: more CTAs per SM beat a deeper pipe)
+#ifndef INFT_RING_STAGES_G
+#define INFT_RING_STAGES_G 3
+#endif
+constexpr int kStagesG = INFT_RING_STAGES_G;  // gather window pipeline depth (config 5: 3 -> 0.993 ms, 2 -> 1.018)
 
 #define INFT_CASES_64(X)                                                                                      \
     X(0) X(1) X(2) X(3) X(4) X(5) X(6) X(7) X(8) X(9) X(10) X(11) X(12) X(13) X(14) X(15) X(16) X(17) X(18)   \
@@ -306,12 +310,12 @@ __global__ void __launch_bounds__(128, INFT_RING_MINB) k_gather_ring(const __gri
     const uint32_t wstage = (uint32_t)SBOX * WPB * 4096u;
     const uint32_t rstage = (uint32_t)((kNB * PP * (int)sizeof(T) + 127) & ~127);
     unsigned char* wbuf = smem;
-    unsigned char* stg = smem + kStages * wstage;  // [WPB][OBOX][32][128]
+    unsigned char* stg = smem + kStagesG * wstage;  // [WPB][OBOX][32][128]
     unsigned char* rbuf = stg + (size_t)WPB * OBOX * 4096u;
-    uint64_t* fullW = reinterpret_cast<uint64_t*>(rbuf + kStages * rstage);
-    uint64_t* emptyW = fullW + kStages;
-    uint64_t* fullR = emptyW + kStages;
-    uint64_t* emptyR = fullR + kStages;
+    uint64_t* fullW = reinterpret_cast<uint64_t*>(rbuf + kStagesG * rstage);
+    uint64_t* emptyW = fullW + kStagesG;
+    uint64_t* fullR = emptyW + kStagesG;
+    uint64_t* emptyR = fullR + kStagesG;
     unsigned char* my_stg = stg + (size_t)warp * OBOX * 4096u;
 
     const int s0 = blockIdx.x * Q;
@@ -351,7 +355,7 @@ __global__ void __launch_bounds__(128, INFT_RING_MINB) k_gather_ring(const __gri
     if (threadIdx.x == 0) {
         prefetch_tmap(&gmap);
         prefetch_tmap(&omap);
-        for (int i = 0; i < kStages; ++i) {
+        for (int i = 0; i < kStagesG; ++i) {
             mbar_init(&fullW[i], 1);
             mbar_init(&emptyW[i], WPB);
             mbar_init(&fullR[i], 1);
@@ -361,8 +365,8 @@ __global__ void __launch_bounds__(128, INFT_RING_MINB) k_gather_ring(const __gri
     }
     __syncthreads();
     if (threadIdx.x == 0) {
-        for (int L = 0; L < min(kStages, nbox); ++L) issueW(L, L);
-        for (int b = 0; b < min(kStages, nbat); ++b) issueR(b, b);
+        for (int L = 0; L < min(kStagesG, nbox); ++L) issueW(L, L);
+        for (int b = 0; b < min(kStagesG, nbat); ++b) issueR(b, b);
     }
 
     T wx[K], wy[K];
@@ -371,8 +375,8 @@ __global__ void __launch_bounds__(128, INFT_RING_MINB) k_gather_ring(const __gri
     // box L -> registers of half (L & 1)
     auto consume_box = [&]() {
         const int L = nextL++;
-        const int stage = L % kStages;
-        const uint32_t parity = (uint32_t)((L / kStages) & 1);
+        const int stage = L % kStagesG;
+        const uint32_t parity = (uint32_t)((L / kStagesG) & 1);
         mbar_wait(&fullW[stage], parity);
         const unsigned char* wb = wbuf + stage * wstage + wrow;
         const int half = L & 1;
@@ -390,9 +394,9 @@ __global__ void __launch_bounds__(128, INFT_RING_MINB) k_gather_ring(const __gri
         fence_proxy_async();
         __syncwarp();
         if (lane == 0) mbar_arrive(&emptyW[stage]);
-        if (threadIdx.x == 0 && L + kStages < nbox) {
+        if (threadIdx.x == 0 && L + kStagesG < nbox) {
             mbar_wait(&emptyW[stage], parity);
-            issueW(L + kStages, stage);
+            issueW(L + kStagesG, stage);
         }
     };
     consume_box();
@@ -402,8 +406,8 @@ __global__ void __launch_bounds__(128, INFT_RING_MINB) k_gather_ring(const __gri
     C2<T>* __restrict__ fr = f + (int64_t)(active ? r : 0) * N;
     const int rstore = row0 + warp * 32;
     for (int b = 0; b < nbat; ++b) {
-        const int stage = b % kStages;
-        const uint32_t parity = (uint32_t)((b / kStages) & 1);
+        const int stage = b % kStagesG;
+        const uint32_t parity = (uint32_t)((b / kStagesG) & 1);
         int pos, cnt;
         batch_pos(b, pos, cnt);
         mbar_wait(&fullR[stage], parity);
@@ -523,9 +527,9 @@ __global__ void __launch_bounds__(128, INFT_RING_MINB) k_gather_ring(const __gri
         fence_proxy_async();
         __syncwarp();
         if (lane == 0) mbar_arrive(&emptyR[stage]);
-        if (threadIdx.x == 0 && b + kStages < nbat) {
+        if (threadIdx.x == 0 && b + kStagesG < nbat) {
             mbar_wait(&emptyR[stage], parity);
-            issueR(b + kStages, stage);
+            issueR(b + kStagesG, stage);
         }
     }
     while (nextL < nbox) consume_box();  // no copy may be in flight at exit
@@ -610,10 +614,10 @@ static size_t ring_spread_smem(int wpb, int PP, int SEG) {
 template <typename T>
 static size_t ring_gather_smem(int wpb, int PP, int SEG) {
     const int EB = 128 / (int)sizeof(C2<T>);
-    size_t wsz = (size_t)ring::kStages * (SEG / EB) * wpb * 4096;
+    size_t wsz = (size_t)ring::kStagesG * (SEG / EB) * wpb * 4096;
     size_t st = (size_t)wpb * (ring::kNB / EB) * 4096;
-    size_t r = (size_t)ring::kStages * ((ring::kNB * PP * (int)sizeof(T) + 127) & ~127);
-    return wsz + st + r + 4 * ring::kStages * sizeof(uint64_t);
+    size_t r = (size_t)ring::kStagesG * ((ring::kNB * PP * (int)sizeof(T) + 127) & ~127);
+    return wsz + st + r + 4 * ring::kStagesG * sizeof(uint64_t);
 }
 
 static void tmap_or_throw(CUtensorMap* m, const void* base, uint64_t inner, uint64_t rows, uint64_t stride,
