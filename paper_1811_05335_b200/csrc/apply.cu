@@ -577,6 +577,7 @@ static void spread(Plan& p, const C2<T>* f, C2<T>* grid, int64_t R, cudaStream_t
         if (p.fT_rhs < R) {
             p.fT.alloc(sizeof(C2<T>) * (size_t)p.N * R);
             p.fT_rhs = R;
+            p.state_version++;
         }
         C2<T>* fT = p.fT.as<C2<T>>();
         k_transpose_f<T><<<gs_blocks(R * p.N, 256), 256, 0, st>>>(f, p.perm.as<int32_t>(), fT, p.N, (int)R);
@@ -587,6 +588,7 @@ static void spread(Plan& p, const C2<T>* f, C2<T>* grid, int64_t R, cudaStream_t
             if (p.part2d_rhs < R && p.slots2d > 0) {
                 p.part2d.alloc(sizeof(C2<T>) * (size_t)p.slots2d * R * 256);
                 p.part2d_rhs = R;
+                p.state_version++;
             }
             dim3 g((unsigned)p.work2d_n, (unsigned)ceil_div(R, 32));
             const size_t smem = 2 * tile2d_stage_bytes<T>(p.PP);
@@ -815,6 +817,7 @@ static void ensure_grid(Plan& p, int64_t rhs) {
     if (p.grid_rhs >= rhs && p.grid.p) return;
     p.grid.alloc((size_t)rhs * p.GS * p.elem_bytes());
     p.grid_rhs = rhs;
+    p.state_version++;  // graphs captured on the old grid are stale
 }
 
 static int64_t grid_capacity(Plan& p, int64_t want) {
@@ -1038,16 +1041,73 @@ static void run(Plan& p, const void* in, size_t in_rhs_bytes, void* out, size_t 
     INFT_CUDA(cudaStreamWaitEvent(st, p.ev_exit, 0));
 }
 
+// Repeated applies on the same device buffers replay a CUDA graph: the second call captures
+// the launch sequence on the plan's stream s_graph (forked from / joined back to the caller's
+// stream by events, so the caller's stream may be the legacy default stream), later calls
+// launch it -- one host call instead of one per kernel, and tighter kernel-to-kernel gaps
+// (configs 1-2 are launch-latency bound).  Off while profiling, for host
+// buffers, and with INFT_GRAPHS=0; the key includes the plan's state version.
+static bool graphs_enabled() {
+    static const bool on = [] {
+        const char* e = getenv("INFT_GRAPHS");
+        return !(e && atoi(e) == 0);
+    }();
+    return on;
+}
+
+static void run_graphed(Plan& p, int dir, const void* in, size_t in_rhs_bytes, void* out, size_t out_rhs_bytes,
+                        int64_t R, cudaStream_t st, ChunkFn fn) {
+    const bool dev = (in_rhs_bytes == 0 || is_device_pointer(in)) && (out_rhs_bytes == 0 || is_device_pointer(out));
+    if (!graphs_enabled() || p.profiling || !dev) {
+        run(p, in, in_rhs_bytes, out, out_rhs_bytes, R, st, fn);
+        return;
+    }
+    Plan::GraphEntry& e = p.graphs[Plan::GraphKey{dir, in, out, R, p.state_version}];
+    if (!e.exec && e.seen++ == 0) {  // first call: plain launches (allocations, one-time tables)
+        run(p, in, in_rhs_bytes, out, out_rhs_bytes, R, st, fn);
+        return;
+    }
+    if (!p.s_graph) {
+        INFT_CUDA(cudaStreamCreateWithFlags(&p.s_graph, cudaStreamNonBlocking));
+        INFT_CUDA(cudaEventCreateWithFlags(&p.ev_g0, cudaEventDisableTiming));
+        INFT_CUDA(cudaEventCreateWithFlags(&p.ev_g1, cudaEventDisableTiming));
+    }
+    if (!e.exec) {
+        const int64_t l0 = p.launches;
+        INFT_CUDA(cudaStreamBeginCapture(p.s_graph, cudaStreamCaptureModeRelaxed));
+        cudaGraph_t g = nullptr;
+        try {
+            run(p, in, in_rhs_bytes, out, out_rhs_bytes, R, p.s_graph, fn);
+        } catch (...) {
+            cudaStreamEndCapture(p.s_graph, &g);
+            if (g) cudaGraphDestroy(g);
+            throw;
+        }
+        INFT_CUDA(cudaStreamEndCapture(p.s_graph, &g));
+        const cudaError_t ie = cudaGraphInstantiate(&e.exec, g, 0);
+        cudaGraphDestroy(g);
+        INFT_CUDA(ie);
+        e.launches = p.launches - l0;
+        p.launches = l0;  // counted again below, when the graph actually runs
+    }
+    INFT_CUDA(cudaEventRecord(p.ev_g0, st));
+    INFT_CUDA(cudaStreamWaitEvent(p.s_graph, p.ev_g0, 0));
+    INFT_CUDA(cudaGraphLaunch(e.exec, p.s_graph));
+    INFT_CUDA(cudaEventRecord(p.ev_g1, p.s_graph));
+    INFT_CUDA(cudaStreamWaitEvent(st, p.ev_g1, 0));
+    p.launches += e.launches;
+}
+
 void apply_inverse(Plan& p, const void* f, void* fhat, int64_t R, cudaStream_t st) {
     const size_t e = p.elem_bytes();
     ChunkFn fn = p.prec == INFT_C128 ? (ChunkFn)inverse_chunk<double> : (ChunkFn)inverse_chunk<float>;
-    run(p, f, (size_t)p.N * e, fhat, (size_t)p.Mtot * e, R, st, fn);
+    run_graphed(p, 0, f, (size_t)p.N * e, fhat, (size_t)p.Mtot * e, R, st, fn);
 }
 
 void apply_adjoint(Plan& p, const void* h, void* f, int64_t R, cudaStream_t st) {
     const size_t e = p.elem_bytes();
     ChunkFn fn = p.prec == INFT_C128 ? (ChunkFn)adjoint_chunk<double> : (ChunkFn)adjoint_chunk<float>;
-    run(p, h, (size_t)p.Mtot * e, f, (size_t)p.N * e, R, st, fn);
+    run_graphed(p, 1, h, (size_t)p.Mtot * e, f, (size_t)p.N * e, R, st, fn);
 }
 
 }  // namespace inft

@@ -800,6 +800,7 @@ static void fused_adjoint_t(Plan& p, const void* h, void* grid, int64_t R, cudaS
     if (s.y_rhs < R) {
         s.ybuf.alloc(sizeof(C2<T>) * (size_t)p.Ms[0] * R);
         s.y_rhs = R;
+        p.state_version++;
     }
     fft::Args<T> A = make_args<T>(p, s);
     A.grid = static_cast<C2<T>*>(grid);

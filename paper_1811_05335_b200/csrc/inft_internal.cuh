@@ -6,6 +6,7 @@
 
 #include <cstdint>
 #include <map>
+#include <tuple>
 #include <string>
 #include <vector>
 
@@ -131,6 +132,27 @@ struct Plan {
     size_t stage_in_bytes = 0, stage_out_bytes = 0;
     std::map<FftKey, cufftHandle> fft;  // batch -> plan
     cudaStream_t s_h2d = nullptr, s_d2h = nullptr;
+    // CUDA graphs of repeated device-pointer applies (apply.cu): keyed by direction, buffers,
+    // batch and plan state; captured on the plan's own stream s_graph at the second call
+    struct GraphKey {
+        int dir;
+        const void* in;
+        const void* out;
+        int64_t R;
+        int64_t version;
+        bool operator<(const GraphKey& o) const {
+            return std::tie(dir, in, out, R, version) < std::tie(o.dir, o.in, o.out, o.R, o.version);
+        }
+    };
+    struct GraphEntry {
+        int seen = 0;
+        cudaGraphExec_t exec = nullptr;
+        int64_t launches = 0;
+    };
+    std::map<GraphKey, GraphEntry> graphs;
+    int64_t state_version = 0;  // bumped whenever weights / tables change
+    cudaStream_t s_graph = nullptr;
+    cudaEvent_t ev_g0 = nullptr, ev_g1 = nullptr;
     cudaEvent_t ev_h2d[2] = {nullptr, nullptr}, ev_comp[2] = {nullptr, nullptr},
                 ev_d2h[2] = {nullptr, nullptr}, ev_entry = nullptr, ev_exit = nullptr;
 

@@ -126,6 +126,12 @@ Plan::~Plan() {
     for (auto e : ev_pool) cudaEventDestroy(e);
     for (auto& kv : fft) cufftDestroy(kv.second);
     fft.clear();
+    for (auto& kv : graphs)
+        if (kv.second.exec) cudaGraphExecDestroy(kv.second.exec);
+    graphs.clear();
+    if (s_graph) cudaStreamDestroy(s_graph);
+    if (ev_g0) cudaEventDestroy(ev_g0);
+    if (ev_g1) cudaEventDestroy(ev_g1);
     if (s_h2d) cudaStreamDestroy(s_h2d);
     if (s_d2h) cudaStreamDestroy(s_d2h);
     for (int i = 0; i < 2; i++) {
@@ -449,6 +455,7 @@ void compute_deconv(Plan& p, double s, cudaStream_t st) {
 }
 
 static void finish_weights(Plan& p, inft_method method, inft_weights wt, cudaStream_t st) {
+    p.state_version++;  // captured apply graphs refer to the old weight buffers
     // max |w| over the double copy
     DevBuf mx;
     mx.alloc(sizeof(unsigned long long));
