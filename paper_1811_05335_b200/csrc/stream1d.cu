@@ -573,11 +573,23 @@ static size_t gather_smem(int rows, int PP, int S) {
     return 1024 + kStages * (wst + rst) + 4 * kStages * sizeof(uint64_t);
 }
 
+// segments per chunk: kQ, fewer when the problem is too small to give every SM ~8 warps
+// (config 1: 64 segments, 1 RHS -> Q = 2)
+static int stream_q(int nseg, int64_t rowgroups) {
+    int dev = 0, nsm = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    const int64_t want = (int64_t)nsm * 8;
+    const int64_t q = ((int64_t)nseg * rowgroups + want - 1) / want;
+    return (int)std::max<int64_t>(2, std::min<int64_t>(kQ, q));
+}
+
 template <typename T>
 static void spread_t(Plan& p, const void* f, void* grid, int64_t R, cudaStream_t st) {
     Fns<T> F = fns_for<T>(p.m, p.S[0]);
     const int nseg = (int)p.nseg[0];
-    const int nchunks = (int)ceil_div(nseg, kQ);
+    const int Q = stream_q(nseg, ceil_div(R, 32));
+    const int nchunks = (int)ceil_div(nseg, Q);
     // complex64: the f-tile boxes start at arbitrary node offsets, i.e. 8-byte aligned,
     // and a tensor-map load whose innermost start is not 16-byte aligned raises
     // "illegal instruction" (measured: tools/tma_probe.cu, offset 1 faults, offset 2
@@ -595,14 +607,14 @@ static void spread_t(Plan& p, const void* f, void* grid, int64_t R, cudaStream_t
         ensure_smem_attr((const void*)F.st, smem);
         dim3 grid_dim((unsigned)nchunks, (unsigned)ceil_div(R, rows));
         F.st<<<grid_dim, rows, smem, st>>>(map, p.seg_start.as<int32_t>(), p.w.as<T>(), p.PP,
-                                           static_cast<C2<T>*>(grid), p.GS, nseg, kQ, (int)R, (int)p.N, p.perm_shift,
+                                           static_cast<C2<T>*>(grid), p.GS, nseg, Q, (int)R, (int)p.N, p.perm_shift,
                                            debug_flags());
     } else {
         const int nrg = (int)ceil_div(R, 32);
         const int64_t warps = (int64_t)nchunks * nrg;
         F.sr<<<(unsigned)ceil_div(warps * 32, 128), 128, 0, st>>>(
             p.seg_start.as<int32_t>(), p.delta.as<int32_t>(), p.perm.as<int32_t>(), p.w.as<T>(), p.PP,
-            static_cast<const C2<T>*>(f), static_cast<C2<T>*>(grid), p.N, p.GS, nseg, kQ, nchunks, (int)R, nrg);
+            static_cast<const C2<T>*>(f), static_cast<C2<T>*>(grid), p.N, p.GS, nseg, Q, nchunks, (int)R, nrg);
     }
     INFT_CHECK_LAUNCH();
     p.launches++;
@@ -612,7 +624,8 @@ template <typename T>
 static void gather_t(Plan& p, const void* grid, void* f, int64_t R, cudaStream_t st) {
     Fns<T> F = fns_for<T>(p.m, p.S[0]);
     const int nseg = (int)p.nseg[0];
-    const int nchunks = (int)ceil_div(nseg, kQ);
+    const int Q = stream_q(nseg, ceil_div(R, 32));
+    const int nchunks = (int)ceil_div(nseg, Q);
     if (p.perm_shift >= 0 && !force_reg()) {
         const int wpb = wpb_for(R);
         const int rows = 32 * wpb;
@@ -632,13 +645,13 @@ static void gather_t(Plan& p, const void* grid, void* f, int64_t R, cudaStream_t
         ensure_smem_attr((const void*)F.gt, smem);
         dim3 grid_dim((unsigned)nchunks, (unsigned)ceil_div(R, rows));
         F.gt<<<grid_dim, rows, smem, st>>>(map, p.seg_start.as<int32_t>(), p.w.as<T>(), p.PP, static_cast<C2<T>*>(f),
-                                           p.N, nseg, kQ, (int)R, p.perm_shift, debug_flags());
+                                           p.N, nseg, Q, (int)R, p.perm_shift, debug_flags());
     } else {
         const int nrg = (int)ceil_div(R, 32);
         const int64_t warps = (int64_t)nchunks * nrg;
         F.gr<<<(unsigned)ceil_div(warps * 32, 128), 128, 0, st>>>(
             p.seg_start.as<int32_t>(), p.delta.as<int32_t>(), p.perm.as<int32_t>(), p.w.as<T>(), p.PP,
-            static_cast<const C2<T>*>(grid), static_cast<C2<T>*>(f), p.N, p.GS, p.Ms[0], nseg, kQ, nchunks, (int)R,
+            static_cast<const C2<T>*>(grid), static_cast<C2<T>*>(f), p.N, p.GS, p.Ms[0], nseg, Q, nchunks, (int)R,
             nrg);
     }
     INFT_CHECK_LAUNCH();
