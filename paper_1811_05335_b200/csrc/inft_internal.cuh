@@ -61,6 +61,23 @@ int occupancy_cached(const void* fn, int threads, size_t smem);
 struct DevBuf {
     void* p = nullptr;
     size_t bytes = 0;
+    DevBuf() = default;
+    DevBuf(const DevBuf&) = delete;
+    DevBuf& operator=(const DevBuf&) = delete;
+    DevBuf(DevBuf&& o) noexcept : p(o.p), bytes(o.bytes) {
+        o.p = nullptr;
+        o.bytes = 0;
+    }
+    DevBuf& operator=(DevBuf&& o) noexcept {
+        if (this != &o) {
+            free_();
+            p = o.p;
+            bytes = o.bytes;
+            o.p = nullptr;
+            o.bytes = 0;
+        }
+        return *this;
+    }
     void alloc(size_t b);
     void free_();
     ~DevBuf() { free_(); }
@@ -150,6 +167,13 @@ struct Plan {
         int64_t launches = 0;
     };
     std::map<GraphKey, GraphEntry> graphs;
+    // ring kernels: node-balanced chunk tables (segment boundaries), per target node count
+    struct ChunkTable {
+        DevBuf buf;
+        int n = 0;
+    };
+    std::map<int64_t, ChunkTable> ring_chunk_cache;
+    std::vector<int32_t> seg_host;  // host copy of seg_start (1-D)
     int64_t state_version = 0;  // bumped whenever weights / tables change
     cudaStream_t s_graph = nullptr;
     cudaEvent_t ev_g0 = nullptr, ev_g1 = nullptr;

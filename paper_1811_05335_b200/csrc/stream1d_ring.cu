@@ -17,6 +17,8 @@
 #include <cstdlib>
 #include <type_traits>
 
+#include <vector>
+
 #include "common.cuh"
 #include "inft_internal.cuh"
 #include "tma.cuh"
@@ -74,6 +76,7 @@ template <typename T, int MC>
 __global__ void __launch_bounds__(128, INFT_RING_MINB) k_spread_ring(const __grid_constant__ CUtensorMap fmap,
                                                      const __grid_constant__ CUtensorMap gmap,
                                                      const int32_t* __restrict__ seg_start,
+                                                     const int32_t* __restrict__ chunks,
                                                      const T* __restrict__ w, int PPrt, int nseg, int Q, int N,
                                                      int cshift) {
     constexpr int SEG = 2 * MC;
@@ -104,8 +107,9 @@ __global__ void __launch_bounds__(128, INFT_RING_MINB) k_spread_ring(const __gri
     uint64_t* empty = full + kStages;
     unsigned char* my_stg = stg + (size_t)warp * SBOX * 4096u;
 
-    const int s0 = blockIdx.x * Q;
-    const int s1 = min(s0 + Q, nseg);
+    // chunk = Q segments, or a node-balanced run of segments from the chunk table
+    const int s0 = chunks ? __ldg(chunks + blockIdx.x) : (int)blockIdx.x * Q;
+    const int s1 = chunks ? __ldg(chunks + blockIdx.x + 1) : min(s0 + Q, nseg);
     const int sp = s0 == 0 ? nseg - 1 : s0 - 1;
     const int a0 = __ldg(seg_start + sp), a1 = __ldg(seg_start + sp + 1);
     const int b0 = __ldg(seg_start + s0), b1 = __ldg(seg_start + s1);
@@ -286,6 +290,7 @@ template <typename T, int MC>
 __global__ void __launch_bounds__(128, INFT_RING_MINB) k_gather_ring(const __grid_constant__ CUtensorMap gmap,
                                                      const __grid_constant__ CUtensorMap omap,
                                                      const int32_t* __restrict__ seg_start,
+                                                     const int32_t* __restrict__ chunks,
                                                      const T* __restrict__ w, int PPrt, C2<T>* __restrict__ f,
                                                      int64_t Nl, int nseg, int Q, int R, int cshift) {
     constexpr int SEG = 2 * MC;
@@ -318,8 +323,9 @@ __global__ void __launch_bounds__(128, INFT_RING_MINB) k_gather_ring(const __gri
     uint64_t* emptyR = fullR + kStagesG;
     unsigned char* my_stg = stg + (size_t)warp * OBOX * 4096u;
 
-    const int s0 = blockIdx.x * Q;
-    const int s1 = min(s0 + Q, nseg);
+    // chunk = Q segments, or a node-balanced run of segments from the chunk table
+    const int s0 = chunks ? __ldg(chunks + blockIdx.x) : (int)blockIdx.x * Q;
+    const int s1 = chunks ? __ldg(chunks + blockIdx.x + 1) : min(s0 + Q, nseg);
     const int nbox = s1 - s0 + 1;  // box L = grid points of segment s0 + L (halo covers L = nseg)
     const int b0 = __ldg(seg_start + s0), b1 = __ldg(seg_start + s1);
     const int wrap = N - cshift;
@@ -541,9 +547,10 @@ __global__ void __launch_bounds__(128, INFT_RING_MINB) k_gather_ring(const __gri
 // =========================================================================== host
 template <typename T>
 struct RingFns {
-    void (*spread)(const CUtensorMap, const CUtensorMap, const int32_t*, const T*, int, int, int, int, int) = nullptr;
-    void (*gather)(const CUtensorMap, const CUtensorMap, const int32_t*, const T*, int, C2<T>*, int64_t, int, int,
-                   int, int) = nullptr;
+    void (*spread)(const CUtensorMap, const CUtensorMap, const int32_t*, const int32_t*, const T*, int, int, int, int,
+                   int) = nullptr;
+    void (*gather)(const CUtensorMap, const CUtensorMap, const int32_t*, const int32_t*, const T*, int, C2<T>*, int64_t,
+                   int, int, int, int) = nullptr;
 };
 
 template <typename T>
@@ -628,15 +635,42 @@ static void tmap_or_throw(CUtensorMap* m, const void* base, uint64_t inner, uint
     }
 }
 
-// segments per CTA: up to kQ, fewer when the batch is too small to give every SM ~8 CTAs
-// (config 3: 2048 segments x 2 row groups -> Q = 4)
-static int ring_q(int nseg, int64_t rowgroups) {
+// Chunks of consecutive segments, one CTA each (per row group): balanced by node count, not
+// by segment count, so that dense regions (Chebyshev edges) do not set the tail.  A chunk
+// closes at >= T nodes or kQ segments, T = N / (~8 CTAs per SM / row groups).  Cached per T.
+static const int32_t* ring_chunks(Plan& p, int64_t rowgroups, int& nchunks, cudaStream_t st) {
     int dev = 0, nsm = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-    const int64_t want = (int64_t)nsm * 8;
-    const int64_t q = ((int64_t)nseg * rowgroups + want - 1) / want;
-    return (int)std::max<int64_t>(2, std::min<int64_t>(ring::kQ, q));
+    const int64_t want = std::max<int64_t>(1, (int64_t)nsm * 8 / std::max<int64_t>(1, rowgroups));
+    const int64_t T = std::max<int64_t>(1, (p.N + want - 1) / want);
+    auto it = p.ring_chunk_cache.find(T);
+    if (it == p.ring_chunk_cache.end()) {
+        const int nseg = (int)p.nseg[0];
+        if (p.seg_host.empty()) {
+            p.seg_host.resize((size_t)nseg + 1);
+            INFT_CUDA(cudaMemcpyAsync(p.seg_host.data(), p.seg_start.p, sizeof(int32_t) * (nseg + 1),
+                                      cudaMemcpyDeviceToHost, st));
+            INFT_CUDA(cudaStreamSynchronize(st));
+        }
+        std::vector<int32_t> c{0};
+        int64_t acc = 0;
+        for (int sgi = 0; sgi < nseg; ++sgi) {
+            acc += p.seg_host[sgi + 1] - p.seg_host[sgi];
+            if (acc >= T || sgi + 1 - c.back() >= ring::kQ || sgi + 1 == nseg) {
+                c.push_back(sgi + 1);
+                acc = 0;
+            }
+        }
+        Plan::ChunkTable ct;
+        ct.n = (int)c.size() - 1;
+        ct.buf.alloc(sizeof(int32_t) * c.size());
+        INFT_CUDA(cudaMemcpyAsync(ct.buf.p, c.data(), sizeof(int32_t) * c.size(), cudaMemcpyHostToDevice, st));
+        INFT_CUDA(cudaStreamSynchronize(st));
+        it = p.ring_chunk_cache.emplace(T, std::move(ct)).first;
+    }
+    nchunks = it->second.n;
+    return it->second.buf.as<int32_t>();
 }
 
 template <typename T>
@@ -644,8 +678,8 @@ static void ring_spread_t(Plan& p, const void* f, void* grid, int64_t R, cudaStr
     RingFns<T> F = ring_fns<T>(p.m);
     const int wpb = ring_wpb<T>(R);
     const int nseg = (int)p.nseg[0];
-    const int Q = ring_q(nseg, ceil_div(R, 32 * wpb));
-    const int nchunks = (int)ceil_div(nseg, Q);
+    int nchunks = 0;
+    const int32_t* chunks = ring_chunks(p, ceil_div(R, 32 * wpb), nchunks, st);
     const uint64_t ce = sizeof(C2<T>) / 8;
     CUtensorMap fm, gm;
     tmap_or_throw(&fm, f, (uint64_t)p.N * ce, (uint64_t)R, sizeof(C2<T>) * (uint64_t)p.N, 32u, "spread f");
@@ -653,8 +687,8 @@ static void ring_spread_t(Plan& p, const void* f, void* grid, int64_t R, cudaStr
     size_t smem = ring_spread_smem<T>(wpb, p.PP, p.S[0]);
     ensure_smem_attr((const void*)F.spread, smem);
     dim3 g((unsigned)nchunks, (unsigned)ceil_div(R, 32 * wpb));
-    F.spread<<<g, 32 * wpb, smem, st>>>(fm, gm, p.seg_start.as<int32_t>(), p.w.as<T>(), p.PP, nseg, Q, (int)p.N,
-                                        p.perm_shift);
+    F.spread<<<g, 32 * wpb, smem, st>>>(fm, gm, p.seg_start.as<int32_t>(), chunks, p.w.as<T>(), p.PP, nseg, 0,
+                                        (int)p.N, p.perm_shift);
     INFT_CHECK_LAUNCH();
     p.launches++;
 }
@@ -675,8 +709,8 @@ static void ring_gather_t(Plan& p, const void* grid, void* f, int64_t R, cudaStr
     RingFns<T> F = ring_fns<T>(p.m);
     const int wpb = ring_wpb<T>(R);
     const int nseg = (int)p.nseg[0];
-    const int Q = ring_q(nseg, ceil_div(R, 32 * wpb));
-    const int nchunks = (int)ceil_div(nseg, Q);
+    int nchunks = 0;
+    const int32_t* chunks = ring_chunks(p, ceil_div(R, 32 * wpb), nchunks, st);
     const uint64_t ce = sizeof(C2<T>) / 8;
     const int H = (int)(p.GS - p.Ms[0]);
     k_ring_halo<T><<<(unsigned)std::max<int64_t>(1, std::min<int64_t>(ceil_div(R * H, 256), 4096)), 256, 0, st>>>(
@@ -689,8 +723,8 @@ static void ring_gather_t(Plan& p, const void* grid, void* f, int64_t R, cudaStr
     size_t smem = ring_gather_smem<T>(wpb, p.PP, p.S[0]);
     ensure_smem_attr((const void*)F.gather, smem);
     dim3 g((unsigned)nchunks, (unsigned)ceil_div(R, 32 * wpb));
-    F.gather<<<g, 32 * wpb, smem, st>>>(gm, om, p.seg_start.as<int32_t>(), p.w.as<T>(), p.PP, static_cast<C2<T>*>(f),
-                                        p.N, nseg, Q, (int)R, p.perm_shift);
+    F.gather<<<g, 32 * wpb, smem, st>>>(gm, om, p.seg_start.as<int32_t>(), chunks, p.w.as<T>(), p.PP,
+                                        static_cast<C2<T>*>(f), p.N, nseg, 0, (int)R, p.perm_shift);
     INFT_CHECK_LAUNCH();
     p.launches++;
 }
