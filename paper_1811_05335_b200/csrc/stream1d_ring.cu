@@ -605,7 +605,12 @@ bool ring_available(const Plan& p) {
 
 template <typename T>
 static int ring_wpb(int64_t R) {
-    return (int)std::min<int64_t>(4, std::max<int64_t>(1, ceil_div(R, 32)));
+    static const int cap = [] {
+        const char* e = getenv("INFT_RING_WPB");
+        const int v = e ? atoi(e) : 0;
+        return v >= 1 && v <= 4 ? v : 1;  // config 5: 1 warp 5.455 ms/step, 2 warps 5.55
+    }();
+    return (int)std::min<int64_t>(cap, std::max<int64_t>(1, ceil_div(R, 32)));
 }
 
 template <typename T>
