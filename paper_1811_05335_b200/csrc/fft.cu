@@ -389,11 +389,17 @@ __global__ void __launch_bounds__(Geo<T, L>::NT, 1)
             const T d = dsm[(n1 < B ? n1 : n1 - (L - 2 * B)) * DW + (col0 & (DW - 1)) + f];
             return mk<T>(d * v.x, d * v.y);
         };
-        const C2<T> wq = cmul<T>(tqa, tqb);
-        C2<T> wcur = cmul<T>(t0a, t0b);
+        // the twiddle products are formed at the first store (last stage), so the table loads
+        // issued above complete under the earlier stages instead of stalling here
+        C2<T> wq, wcur;
         C2<T>* orow = (MODE == 0) ? A.grid + r * A.GS : A.ybuf + r * A.N;
         auto store = [&](int f, int k1, C2<T> v, int m) {
-            if (m > 0) wcur = cmul<T>(wcur, wq);
+            if (m == 0) {
+                wq = cmul<T>(tqa, tqb);
+                wcur = cmul<T>(t0a, t0b);
+            } else {
+                wcur = cmul<T>(wcur, wq);
+            }
             orow[(int64_t)k1 * N2 + col0 + f] = cmul<T>(v, wcur);
         };
         cta_fft<T, SIGN, L>(tws, work, load, store);
