@@ -896,7 +896,8 @@ static void inverse_chunk(Plan& p, const void* f, void* fhat, int64_t Rc, cudaSt
         StageTimer t(p, 0, st);
         spread<T>(p, static_cast<const C2<T>*>(f), g, Rc, st);
     }
-    if (use_fused(p)) {  // a3 + a4 in two fused passes (fft.cu)
+    // a3 + a4 in two fused passes (fft.cu); pass B's TMA store boxes need a 16-byte aligned fhat
+    if (use_fused(p) && (reinterpret_cast<uintptr_t>(fhat) & 15) == 0) {
         {
             StageTimer t(p, 1, st);  // pass A: column FFTs + four-step twiddles (in place)
             fused_fft_inverse(p, g, fhat, Rc, st, 1);

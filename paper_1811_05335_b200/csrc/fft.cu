@@ -262,7 +262,9 @@ __device__ __forceinline__ void run_stage(const C2<T>* tw, C2<T>* sm, Load&& loa
                 a[p][m] = sm[sidx<G>(f, n)];
         }
     }
-    if constexpr (SI > 0) __syncthreads();  // everyone has read the shared buffer
+    // everyone has read the shared buffer (also for a single-stage transform: its outputs are
+    // staged in the buffer its inputs came from)
+    if constexpr (SI > 0 || last) __syncthreads();
 #pragma unroll
     for (int p = 0; p < per; ++p) {
         const int t = threadIdx.x + p * G::NT;
@@ -318,8 +320,8 @@ __host__ __device__ constexpr size_t d_offset(int L, int ST, int SW, int TB) {
 //                     the other rows are zero and never read), output to ybuf.
 template <typename T, int SIGN, int MODE, int L>
 __global__ void __launch_bounds__(Geo<T, L>::NT, 1)
-    k_pass_a(const __grid_constant__ CUtensorMap map, const __grid_constant__ CUtensorMap dmap, Args<T> A, int BR,
-             int ntiles) {
+    k_pass_a(const __grid_constant__ CUtensorMap map, const __grid_constant__ CUtensorMap dmap,
+             const __grid_constant__ CUtensorMap omap, Args<T> A, int BR, int ntiles) {
     extern __shared__ __align__(128) unsigned char smraw[];
     constexpr int CE = (int)(sizeof(C2<T>) / 8);
     using G = Geo<T, L>;
@@ -370,7 +372,10 @@ __global__ void __launch_bounds__(Geo<T, L>::NT, 1)
     if (threadIdx.x == 0 && (int)blockIdx.x < ntiles) issue(blockIdx.x, 0);
     for (int id = blockIdx.x; id < ntiles; id += gridDim.x, ++it) {
         const int b = it & 1;
-        if (threadIdx.x == 0 && id + (int)gridDim.x < ntiles) issue(id + gridDim.x, b ^ 1);
+        if (threadIdx.x == 0 && id + (int)gridDim.x < ntiles) {
+            bulk_wait_read<0>();  // the previous tile's output store has left buffer b ^ 1
+            issue(id + gridDim.x, b ^ 1);
+        }
         const int64_t r = id / tiles_per_rhs;
         const int col0 = (id % tiles_per_rhs) * TA;
         // loads independent of the tile data, issued before waiting for it:
@@ -392,6 +397,12 @@ __global__ void __launch_bounds__(Geo<T, L>::NT, 1)
         // the twiddle products are formed at the first store (last stage), so the table loads
         // issued above complete under the earlier stages instead of stalling here
         C2<T> wq, wcur;
+        // kStageA: outputs staged in tile[b] (consumed by the first stage) as [k1][TA] and
+        // stored by TMA boxes; otherwise plain stores from registers.  The boxes are only TA
+        // columns (64 B) wide: measured on config 5, plain stores are faster for pass A
+        // (0.886 vs 0.944 ms) while pass B gains from staging (0.907 -> 0.854 ms).
+        constexpr bool kStageA = false;
+        C2<T>* stg = tile + b * L * TA;
         C2<T>* orow = (MODE == 0) ? A.grid + r * A.GS : A.ybuf + r * A.N;
         auto store = [&](int f, int k1, C2<T> v, int m) {
             if (m == 0) {
@@ -400,12 +411,20 @@ __global__ void __launch_bounds__(Geo<T, L>::NT, 1)
             } else {
                 wcur = cmul<T>(wcur, wq);
             }
-            orow[(int64_t)k1 * N2 + col0 + f] = cmul<T>(v, wcur);
+            if (kStageA)
+                stg[k1 * TA + f] = cmul<T>(v, wcur);
+            else
+                orow[(int64_t)k1 * N2 + col0 + f] = cmul<T>(v, wcur);
         };
         cta_fft<T, SIGN, L>(tws, work, load, store);
-        fence_proxy_async();  // this thread's reads of tile[b] precede the next TMA into it
-        __syncthreads();      // tile[b] and work free for the next iteration
+        fence_proxy_async();  // staged outputs / tile[b] reads before the async proxy uses it
+        __syncthreads();      // tile[b] free (or staged), work free for the next iteration
+        if (kStageA && threadIdx.x == 0) {
+            for (int q = 0; q < L; q += BR) tma_store_3d(&omap, col0 * CE, q, (int)r, stg + q * TA);
+            bulk_commit();
+        }
     }
+    if (threadIdx.x == 0) bulk_wait<0>();
 }
 
 // Pass B (rows, length L = N2, TF = TB rows per tile, tile layout [f][S]):
@@ -413,10 +432,12 @@ __global__ void __launch_bounds__(Geo<T, L>::NT, 1)
 //   MODE 1 (adjoint): input ybuf rows, output grid (natural order) + halo.
 template <typename T, int SIGN, int MODE, int L>
 __global__ void __launch_bounds__(Geo<T, L>::NT, 1)
-    k_pass_b(const __grid_constant__ CUtensorMap dmap, Args<T> A, int BRd, int ntiles) {
+    k_pass_b(const __grid_constant__ CUtensorMap dmap, const __grid_constant__ CUtensorMap omap, Args<T> A, int BRd,
+             int BRo, int ntiles) {
     extern __shared__ __align__(128) unsigned char smraw[];
     using G = Geo<T, L>;
     constexpr int TB = G::TF, S = G::ST, SW = G::SW;
+    constexpr int CE = (int)(sizeof(C2<T>) / 8);
     // MODE 0: the deconvolution factors of the tile's kept outputs, [2 B2][DW] (rows: k2 in
     // [0, B2), then k2 in [N2 - B2, N2)), fetched by TMA while the first stages run
     constexpr int DW = (int)(16 / sizeof(T)) > TB ? (int)(16 / sizeof(T)) : TB;
@@ -455,7 +476,10 @@ __global__ void __launch_bounds__(Geo<T, L>::NT, 1)
         const int64_t r = id / tiles_per_rhs;
         const int row0 = (id % tiles_per_rhs) * TB;
         if (threadIdx.x == 0) {
-            if (id + (int)gridDim.x < ntiles) issue(id + gridDim.x, b ^ 1);
+            if (id + (int)gridDim.x < ntiles) {
+                bulk_wait_read<0>();  // the previous tile's output store has left buffer b ^ 1
+                issue(id + gridDim.x, b ^ 1);
+            }
             if (MODE == 0) {
                 // d rows [B2, 2 B2) (k2 < B2) and [0, B2) (k2 >= N2 - B2), columns row0 ..
                 // the box's inner start must be 16-byte aligned (an unaligned start coordinate
@@ -471,7 +495,9 @@ __global__ void __launch_bounds__(Geo<T, L>::NT, 1)
         mbar_wait(&bars[b], (it >> 1) & 1);
         const C2<T>* tl = tile + b * S * TB;
         C2<T>* grow = A.grid + r * A.GS;
-        C2<T>* frow = A.fhat + r * A.M;
+        // outputs staged in tile[b] (consumed by the first stage) and stored by TMA boxes:
+        // MODE 1 as [k2][TB] (all N2 rows), MODE 0 as [2 B2][TB] (kept rows, d applied)
+        C2<T>* stg = tile + b * S * TB;
         auto load = [&](int f, int n2, int, int) -> C2<T> { return tl[f * S + n2]; };
         // MODE 0 with B2 a multiple of the last stage's span L/16 (e.g. sigma = 2): whether leg m
         // is kept, its output address and its d slot follow from m alone (warp-uniform tests,
@@ -480,44 +506,50 @@ __global__ void __launch_bounds__(Geo<T, L>::NT, 1)
         const bool fastband = (B2 % NsL) == 0;
         const int mlo = B2 / NsL;
         const int jl = threadIdx.x / TB, fl = threadIdx.x - (threadIdx.x / TB) * TB;
-        const int64_t cb = (int64_t)(row0 + fl) + (int64_t)N1 * jl;
         const int doff = (row0 & (DW - 1)) + fl;
         auto store = [&](int f, int k2, C2<T> v, int m) {
             const int64_t k = (int64_t)(row0 + f) + (int64_t)N1 * k2;
             if (MODE == 0) {
                 if (m == 0) mbar_wait(&bars[2], it & 1);
-                if (fastband) {
-                    if (m < mlo) {
-                        const T d = dsm[(jl + m * NsL) * DW + doff];
-                        frow[cb + half + (int64_t)m * NsL * N1] = mk<T>(d * v.x, d * v.y);
-                    } else if (m >= 16 - mlo) {
-                        const T d = dsm[(jl + m * NsL - (L - 2 * B2)) * DW + doff];
-                        frow[cb - (A.N - half) + (int64_t)m * NsL * N1] = mk<T>(d * v.x, d * v.y);
-                    }
-                    return;
-                }
-                int64_t c;
                 int sr;
-                if (k2 < B2) {
-                    c = k + half;
+                if (fastband) {
+                    if (m < mlo)
+                        sr = jl + m * NsL;
+                    else if (m >= 16 - mlo)
+                        sr = jl + m * NsL - (L - 2 * B2);
+                    else
+                        return;
+                } else if (k2 < B2) {
                     sr = k2;
                 } else if (k2 >= L - B2) {
-                    c = k - (A.N - half);
                     sr = k2 - (L - 2 * B2);
                 } else {
                     return;
                 }
-                const T d = dsm[sr * DW + (row0 & (DW - 1)) + f];
-                frow[c] = mk<T>(d * v.x, d * v.y);
+                const T d = dsm[sr * DW + doff];
+                stg[sr * TB + f] = mk<T>(d * v.x, d * v.y);
             } else {
-                grow[k] = v;
-                if (k < A.H) grow[A.N + k] = v;
+                stg[k2 * TB + f] = v;
+                if (k < A.H) grow[A.N + k] = v;  // the gather's halo copy of the first cells
             }
         };
         cta_fft<T, SIGN, L>(tws, work, load, store);
-        fence_proxy_async();
+        fence_proxy_async();  // staged outputs before the TMA store; tile[b] reads before reuse
         __syncthreads();
+        if (threadIdx.x == 0) {
+            if (MODE == 0) {
+                // staged rows [0, B2) -> fhat rows [B2, 2 B2); [B2, 2 B2) -> fhat rows [0, B2)
+                for (int q = 0; q < B2; q += BRo) {
+                    tma_store_3d(&omap, row0 * CE, B2 + q, (int)r, stg + q * TB);
+                    tma_store_3d(&omap, row0 * CE, q, (int)r, stg + (B2 + q) * TB);
+                }
+            } else {
+                for (int q = 0; q < L; q += BRo) tma_store_3d(&omap, row0 * CE, q, (int)r, stg + q * TB);
+            }
+            bulk_commit();
+        }
     }
+    if (threadIdx.x == 0) bulk_wait<0>();
 }
 
 }  // namespace fft
@@ -588,6 +620,7 @@ bool fused_fft_available(const Plan& p) {
         if (smem == 0 || smem > 227 * 1024) return false;
         if (B2 > 256 && B2 % 256) return false;
         if ((B2 * dw * ds) % 128) return false;
+        if (((size_t)B2 * TF * 2 * ds) % 128) return false;  // staged output box offsets
     }
     // pass A's TMA box is TF columns wide and must span >= 16 bytes (TF = 1 only for N1 = 4096)
     if (p.prec == INFT_C64 && split_n1(N) >= 4096) return false;
@@ -650,9 +683,9 @@ static fft::Args<T> make_args(Plan& p, FftState& s) {
 }
 
 template <typename T>
-using PassAFn = void (*)(const CUtensorMap, const CUtensorMap, fft::Args<T>, int, int);
+using PassAFn = void (*)(const CUtensorMap, const CUtensorMap, const CUtensorMap, fft::Args<T>, int, int);
 template <typename T>
-using PassBFn = void (*)(const CUtensorMap, fft::Args<T>, int, int);
+using PassBFn = void (*)(const CUtensorMap, const CUtensorMap, fft::Args<T>, int, int, int);
 
 template <typename T, int L>
 static void pick_L(int mode, PassAFn<T>& a, PassBFn<T>& b) {
@@ -733,6 +766,14 @@ static void launch_pass_a(Plan& p, fft::Args<T>& A, int mode, const void* src, i
                                 sizeof(T) * (uint64_t)A.M, (uint32_t)DW, (uint32_t)BR, (int)sizeof(T));
     }
     if (mode == 0) dmap = map;
+    // output boxes: MODE 0 in place on the grid (same map), MODE 1 into ybuf [R][N1][N2]
+    CUtensorMap omap = map;
+    if (mode == 1 && !make_tmap_3d(&omap, A.ybuf, (uint64_t)A.N2 * CE, (uint64_t)A.N1, (uint64_t)R,
+                                   cs * (uint64_t)A.N2, cs * (uint64_t)A.N, (uint32_t)(TA * CE),
+                                   (uint32_t)std::min(L, 256))) {
+        set_error("cuTensorMapEncodeTiled failed (fused FFT pass A output)");
+        throw Fail{INFT_ERR_CUDA};
+    }
     if (!ok) {
         set_error("cuTensorMapEncodeTiled failed (fused FFT pass A)");
         throw Fail{INFT_ERR_CUDA};
@@ -741,7 +782,9 @@ static void launch_pass_a(Plan& p, fft::Args<T>& A, int mode, const void* src, i
     const int ntiles = (int)(R * (A.N2 / TA));
     ensure_smem_attr((const void*)ka, smem);
     const int occ = occupancy_cached((const void*)ka, threads, smem);
-    ka<<<(unsigned)std::min(ntiles, num_sms() * std::max(1, occ)), threads, smem, st>>>(map, dmap, A, BR, ntiles);
+    ka<<<(unsigned)std::min(ntiles, num_sms() * std::max(1, occ)), threads, smem, st>>>(map, dmap, omap, A,
+                                                                                        mode == 0 ? std::min(L, 256) : BR,
+                                                                                        ntiles);
     INFT_CHECK_LAUNCH();
     p.launches++;
 }
@@ -772,10 +815,25 @@ static void launch_pass_b(Plan& p, fft::Args<T>& A, int mode, int64_t R, cudaStr
     } else {
         memset(&dmap, 0, sizeof(dmap));
     }
+    // output boxes: MODE 0 -> fhat viewed as [R][M / N1][N1] (kept rows), MODE 1 -> the grid
+    // viewed as [R][N2][N1] (row k2, column k1 of k = k1 + N1 k2)
+    constexpr int CE = (int)(sizeof(C2<T>) / 8);
+    CUtensorMap omap;
+    const int BRo = mode == 0 ? std::min(B2, 256) : std::min(L, 256);
+    const bool ok = mode == 0
+                        ? make_tmap_3d(&omap, A.fhat, (uint64_t)A.N1 * CE, (uint64_t)(A.M / A.N1), (uint64_t)R,
+                                       cs * (uint64_t)A.N1, cs * (uint64_t)A.M, (uint32_t)(TB * CE), (uint32_t)BRo)
+                        : make_tmap_3d(&omap, A.grid, (uint64_t)A.N1 * CE, (uint64_t)A.N2, (uint64_t)R,
+                                       cs * (uint64_t)A.N1, cs * (uint64_t)A.GS, (uint32_t)(TB * CE), (uint32_t)BRo);
+    if (!ok) {
+        set_error("cuTensorMapEncodeTiled failed (fused FFT pass B output)");
+        throw Fail{INFT_ERR_CUDA};
+    }
     const int ntiles = (int)(R * (A.N1 / TB));
     ensure_smem_attr((const void*)kb, smem);
     const int occ = occupancy_cached((const void*)kb, threads, smem);
-    kb<<<(unsigned)std::min(ntiles, num_sms() * std::max(1, occ)), threads, smem, st>>>(dmap, A, BRd, ntiles);
+    kb<<<(unsigned)std::min(ntiles, num_sms() * std::max(1, occ)), threads, smem, st>>>(dmap, omap, A, BRd, BRo,
+                                                                                        ntiles);
     INFT_CHECK_LAUNCH();
     p.launches++;
 }

@@ -95,6 +95,14 @@ __device__ __forceinline__ void cp_async_wait() {
     asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
 }
 
+// 3-D tiled tensor copy shared -> global (bulk async-group).
+__device__ __forceinline__ void tma_store_3d(const CUtensorMap* map, int c0, int c1, int c2, const void* src) {
+    asm volatile("cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%1, %2, %3}], [%4];" ::"l"(
+                     reinterpret_cast<uint64_t>(map)),
+                 "r"(c0), "r"(c1), "r"(c2), "r"(smem_addr(src))
+                 : "memory");
+}
+
 // Order this thread's prior generic-proxy shared-memory accesses before later
 // async-proxy (TMA / bulk copy) accesses: required before releasing a stage
 // buffer that the next TMA will overwrite (cross-proxy WAR hazard).
