@@ -322,6 +322,7 @@ template <typename T, int SIGN, int MODE, int L>
 __global__ void __launch_bounds__(Geo<T, L>::NT, 1)
     k_pass_a(const __grid_constant__ CUtensorMap map, const __grid_constant__ CUtensorMap dmap,
              const __grid_constant__ CUtensorMap omap, Args<T> A, int BR, int ntiles) {
+    constexpr bool kStageA = false;  // see the store lambda
     extern __shared__ __align__(128) unsigned char smraw[];
     constexpr int CE = (int)(sizeof(C2<T>) / 8);
     using G = Geo<T, L>;
@@ -373,7 +374,8 @@ __global__ void __launch_bounds__(Geo<T, L>::NT, 1)
     for (int id = blockIdx.x; id < ntiles; id += gridDim.x, ++it) {
         const int b = it & 1;
         if (threadIdx.x == 0 && id + (int)gridDim.x < ntiles) {
-            bulk_wait_read<0>();  // the previous tile's output store has left buffer b ^ 1
+            // (a bulk wait costs even with nothing outstanding: only when outputs are staged)
+            if (kStageA) bulk_wait_read<0>();  // the previous tile's output store has left b ^ 1
             issue(id + gridDim.x, b ^ 1);
         }
         const int64_t r = id / tiles_per_rhs;
@@ -401,7 +403,6 @@ __global__ void __launch_bounds__(Geo<T, L>::NT, 1)
         // stored by TMA boxes; otherwise plain stores from registers.  The boxes are only TA
         // columns (64 B) wide: measured on config 5, plain stores are faster for pass A
         // (0.886 vs 0.944 ms) while pass B gains from staging (0.907 -> 0.854 ms).
-        constexpr bool kStageA = false;
         C2<T>* stg = tile + b * L * TA;
         C2<T>* orow = (MODE == 0) ? A.grid + r * A.GS : A.ybuf + r * A.N;
         auto store = [&](int f, int k1, C2<T> v, int m) {
@@ -424,7 +425,7 @@ __global__ void __launch_bounds__(Geo<T, L>::NT, 1)
             bulk_commit();
         }
     }
-    if (threadIdx.x == 0) bulk_wait<0>();
+    if (kStageA && threadIdx.x == 0) bulk_wait<0>();
 }
 
 // Pass B (rows, length L = N2, TF = TB rows per tile, tile layout [f][S]):
@@ -434,6 +435,7 @@ template <typename T, int SIGN, int MODE, int L>
 __global__ void __launch_bounds__(Geo<T, L>::NT, 1)
     k_pass_b(const __grid_constant__ CUtensorMap dmap, const __grid_constant__ CUtensorMap omap, Args<T> A, int BRd,
              int BRo, int ntiles) {
+    constexpr bool kStageB = sizeof(T) == 8;  // see the store lambda
     extern __shared__ __align__(128) unsigned char smraw[];
     using G = Geo<T, L>;
     constexpr int TB = G::TF, S = G::ST, SW = G::SW;
@@ -477,7 +479,7 @@ __global__ void __launch_bounds__(Geo<T, L>::NT, 1)
         const int row0 = (id % tiles_per_rhs) * TB;
         if (threadIdx.x == 0) {
             if (id + (int)gridDim.x < ntiles) {
-                bulk_wait_read<0>();  // the previous tile's output store has left buffer b ^ 1
+                if (kStageB) bulk_wait_read<0>();  // the previous tile's output store has left b ^ 1
                 issue(id + gridDim.x, b ^ 1);
             }
             if (MODE == 0) {
@@ -495,9 +497,11 @@ __global__ void __launch_bounds__(Geo<T, L>::NT, 1)
         mbar_wait(&bars[b], (it >> 1) & 1);
         const C2<T>* tl = tile + b * S * TB;
         C2<T>* grow = A.grid + r * A.GS;
-        // outputs staged in tile[b] (consumed by the first stage) and stored by TMA boxes:
-        // MODE 1 as [k2][TB] (all N2 rows), MODE 0 as [2 B2][TB] (kept rows, d applied)
+        // complex128: outputs staged in tile[b] (consumed by the first stage) and stored by TMA
+        // boxes -- MODE 1 as [k2][TB] (all N2 rows), MODE 0 as [2 B2][TB] (kept rows, d applied);
+        // complex64 (16-byte-wide boxes) keeps plain stores (config 5: staging 0.87 ms vs 0.70)
         C2<T>* stg = tile + b * S * TB;
+        C2<T>* frow = A.fhat + r * A.M;
         auto load = [&](int f, int n2, int, int) -> C2<T> { return tl[f * S + n2]; };
         // MODE 0 with B2 a multiple of the last stage's span L/16 (e.g. sigma = 2): whether leg m
         // is kept, its output address and its d slot follow from m alone (warp-uniform tests,
@@ -527,16 +531,25 @@ __global__ void __launch_bounds__(Geo<T, L>::NT, 1)
                     return;
                 }
                 const T d = dsm[sr * DW + doff];
-                stg[sr * TB + f] = mk<T>(d * v.x, d * v.y);
+                if (kStageB) {
+                    stg[sr * TB + f] = mk<T>(d * v.x, d * v.y);
+                } else {
+                    // fhat column c = k +- ... : staged row sr < B2 <-> fhat row sr + B2, else sr - B2
+                    const int64_t c = (int64_t)(sr < B2 ? sr + B2 : sr - B2) * N1 + row0 + f;
+                    frow[c] = mk<T>(d * v.x, d * v.y);
+                }
             } else {
-                stg[k2 * TB + f] = v;
+                if (kStageB)
+                    stg[k2 * TB + f] = v;
+                else
+                    grow[k] = v;
                 if (k < A.H) grow[A.N + k] = v;  // the gather's halo copy of the first cells
             }
         };
         cta_fft<T, SIGN, L>(tws, work, load, store);
         fence_proxy_async();  // staged outputs before the TMA store; tile[b] reads before reuse
         __syncthreads();
-        if (threadIdx.x == 0) {
+        if (kStageB && threadIdx.x == 0) {
             if (MODE == 0) {
                 // staged rows [0, B2) -> fhat rows [B2, 2 B2); [B2, 2 B2) -> fhat rows [0, B2)
                 for (int q = 0; q < B2; q += BRo) {
@@ -549,7 +562,7 @@ __global__ void __launch_bounds__(Geo<T, L>::NT, 1)
             bulk_commit();
         }
     }
-    if (threadIdx.x == 0) bulk_wait<0>();
+    if (kStageB && threadIdx.x == 0) bulk_wait<0>();
 }
 
 }  // namespace fft
