@@ -600,6 +600,8 @@ bool ring_available(const Plan& p) {
         return false;
     if (p.S[0] != 2 * p.m) return false;
     if (p.prec == INFT_C64 && !ring_c64_spread_enabled()) return false;
+    // the f / output tensor maps need a row stride (N elements) that is a multiple of 16 bytes
+    if ((p.N * (int64_t)p.elem_bytes()) % 16) return false;
     return p.prec == INFT_C128 ? ring_fns<double>(p.m).spread != nullptr : ring_fns<float>(p.m).spread != nullptr;
 }
 

@@ -1,0 +1,88 @@
+"""GPU: seeded random problems (sizes, sigma, m, node sets, batch) against the oracle -- a
+sweep over the dispatch space (ring / register / generic 1-D kernels, fused FFT / cuFFT, 2-D
+tile kernels, complex weights, graphs on repeated calls), each compared element-wise."""
+import numpy as np
+import pytest
+
+import oracle as O
+import synth as S
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def torch():
+    import torch as t
+    assert t.cuda.is_available()
+    return t
+
+
+@pytest.fixture(scope="module")
+def P():
+    import paper_1811_05335_b200 as P
+    return P
+
+
+def _case(seed):
+    rng = np.random.default_rng(1000 + seed)
+    d = 1 if seed % 4 else 2
+    sigma = float(rng.choice([1.5, 2.0, 2.0, 3.0]))
+    if d == 1:
+        M = int(rng.choice([64, 96, 256, 320, 1024, 2048, 4096]))
+        while (sigma * M) % 2 or abs(sigma * M - round(sigma * M)) > 1e-9:
+            M += 2
+        m = int(rng.integers(1, 12))
+        m = min(m, int(sigma * M) // 2)
+        N = int(rng.integers(1, 3 * M))
+        kind = rng.choice(["jittered", "iid", "cheb", "cluster"])
+        if kind == "jittered":
+            x = S.jittered(N, seed)
+        elif kind == "iid":
+            x = np.sort(rng.random(N) - 0.5)
+        elif kind == "cheb":
+            x = S.chebyshev(N)
+        else:
+            x = np.clip(rng.normal(0.0, 0.05, N), -0.5, 0.5 - 1e-9)
+        if rng.random() < 0.5:
+            x = x[rng.permutation(N)]
+    else:
+        M = (int(rng.choice([16, 32, 48])), int(rng.choice([16, 32, 64])))
+        m = int(rng.integers(1, 6))
+        N = int(rng.integers(1, 4 * M[0] * M[1] // 4))
+        x = rng.random((N, 2)) - 0.5
+    R = int(rng.choice([1, 2, 5, 33, 64]))
+    cplx = rng.random() < 0.2
+    prec = "c64" if rng.random() < 0.3 else "c128"
+    return d, M, sigma, m, x, R, cplx, prec
+
+
+@pytest.mark.parametrize("seed", range(24))
+def test_random_problem(P, torch, seed):
+    d, M, sigma, m, x, R, cplx, prec = _case(seed)
+    rng = np.random.default_rng(seed)
+    if d == 1:
+        live = O.slot_live(x, O.msigma(M, sigma), m)
+    else:
+        l1 = O.slot_live(x[:, 0], O.msigma(M[0], sigma), m)
+        l2 = O.slot_live(x[:, 1], O.msigma(M[1], sigma), m)
+        live = (l1[:, :, None] & l2[:, None, :]).reshape(x.shape[0], -1)
+    w = rng.standard_normal(live.shape) * live
+    if cplx:
+        w = w + 1j * rng.standard_normal(live.shape) * live
+    plan = P.Plan(x, M, sigma, m, precision=prec).set_bopt(w, "alg2")
+    dt = torch.complex128 if prec == "c128" else torch.complex64
+    N = x.shape[0]
+    Mt = int(np.prod(M))
+    f = torch.from_numpy(S.normal_complex(R, N, seed)).to("cuda", dt)
+    h = torch.from_numpy(S.normal_complex(R, Mt, seed + 1)).to("cuda", dt)
+    tol = 1e-12 if prec == "c128" else 1e-5
+    c = lambda t: t.cpu().numpy().astype(np.complex128)  # noqa: E731
+    ref_i = O.apply_inverse(x, M, sigma, m, w, 1.0, c(f))
+    ref_a = O.apply_adjoint(x, M, sigma, m, w, 1.0, c(h))
+    for _ in range(3):  # plain call, graph capture, graph replay
+        out_i = torch.empty(R, Mt, dtype=dt, device="cuda")
+        out_a = torch.empty(R, N, dtype=dt, device="cuda")
+        plan.apply(f, out=out_i)
+        plan.adjoint_apply(h, out=out_a)
+        assert O.rel_l2(c(out_i), ref_i) <= tol, (seed, d, M, sigma, m, N, R, cplx, prec)
+        assert O.rel_l2(c(out_a), ref_a) <= tol, (seed, d, M, sigma, m, N, R, cplx, prec)
