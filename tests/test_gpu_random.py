@@ -1,6 +1,8 @@
 """GPU: seeded random problems (sizes, sigma, m, node sets, batch) against the oracle -- a
 sweep over the dispatch space (ring / register / generic 1-D kernels, fused FFT / cuFFT, 2-D
 tile kernels, complex weights, graphs on repeated calls), each compared element-wise."""
+import os
+
 import numpy as np
 import pytest
 
@@ -56,7 +58,8 @@ def _case(seed):
     return d, M, sigma, m, x, R, cplx, prec
 
 
-@pytest.mark.parametrize("seed", range(24))
+# INFT_RANDOM_CASES=n widens the sweep (160 cases pass on the round-1 build)
+@pytest.mark.parametrize("seed", range(int(os.environ.get("INFT_RANDOM_CASES", "24"))))
 def test_random_problem(P, torch, seed):
     d, M, sigma, m, x, R, cplx, prec = _case(seed)
     rng = np.random.default_rng(seed)
