@@ -89,3 +89,41 @@ def test_random_problem(P, torch, seed):
         plan.adjoint_apply(h, out=out_a)
         assert O.rel_l2(c(out_i), ref_i) <= tol, (seed, d, M, sigma, m, N, R, cplx, prec)
         assert O.rel_l2(c(out_a), ref_a) <= tol, (seed, d, M, sigma, m, N, R, cplx, prec)
+
+
+def _resid_1d(x, M, sigma, m, js, n, b, window="kb"):
+    Ms = O.msigma(M, sigma)
+    l = n - Ms if n >= Ms // 2 else n
+    xs = x[js]
+    G = np.real(O.G_kernel(O.wrap_diff(xs[:, None] - xs[None, :]), M, sigma, m, window))
+    y = np.real(O.Kplus_kernel(O.wrap_diff(xs - l / Ms), M, sigma, m, window))
+    bo, _ = O.solve_minnorm_gram(G, y)
+    r = lambda v: float(np.sqrt(max(v @ G @ v - 2 * v @ y + 1.0, 0.0)))  # noqa: E731
+    return r(b), r(bo)
+
+
+@pytest.mark.parametrize("seed", range(12))
+def test_random_alg2_setup(P, seed):
+    """GPU Alg. 2 setup on random 1-D problems: every sampled column reaches the oracle's
+    optimum of ||L_l b - e_l|| (Gram form, reading A6)."""
+    rng = np.random.default_rng(5000 + seed)
+    M = int(rng.choice([16, 32, 64, 128]))
+    sigma = float(rng.choice([1.5, 2.0, 3.0]))
+    if (sigma * M) % 2:
+        sigma = 2.0
+    m = int(rng.integers(1, 9))
+    m = min(m, int(sigma * M) // 2)
+    N = int(rng.integers(4, 4 * M))
+    x = np.sort(rng.random(N) - 0.5) if rng.random() < 0.5 else S.jittered(N, seed)
+    window = "dirichlet" if rng.random() < 0.3 else "kb"
+    plan = P.Plan(x, M, sigma, m, window=window).precompute("alg2")
+    w = plan.get_bopt()
+    assert np.all(np.isfinite(w))
+    Ms = O.msigma(M, sigma)
+    sets = O.grid_node_sets(x, Ms, m)
+    cols = [n for n in range(Ms) if sets[n]]
+    for n in rng.choice(cols, min(12, len(cols)), replace=False):
+        js = [j for j, _ in sets[n]]
+        ts = [t for _, t in sets[n]]
+        rg, ro = _resid_1d(x, M, sigma, m, js, n, w[js, ts], window)
+        assert abs(rg - ro) <= 1e-6, (seed, n, rg, ro)
