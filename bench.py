@@ -42,6 +42,8 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--no-dist-e2e", action="store_true",
+                    help="N > 1: skip the scatter/apply/gather timing through rank 0")
     ap.add_argument("--e2e-one-plan", action="store_true",
                     help="e2e: inverse and adjoint on one plan/stream (serialised) instead of two")
     return ap.parse_args()
@@ -243,6 +245,59 @@ def run_e2e(args, plan, f, h, R, N, M, e, cdt, ws, dev, stream, torch, dist, pla
                     + ("; inverse and adjoint on two plans/streams" if plan2 is not None else "")}
 
 
+def run_dist_e2e(plan, R, N, M, cdt, ws, rank, dev, steps, torch, dist):
+    """SURVEY 8(e) with-communication time: rank 0 owns the whole batch (R per rank), scatters
+    the inputs f and h over NCCL, every rank applies to its shard, and the outputs are gathered
+    back to rank 0; per step, max over ranks.  Reported next to the rank-resident weak-scaling
+    `value` (the efficiency measure).  Complex tensors travel as float views."""
+    Rg = R * ws
+    g = torch.Generator(device=dev).manual_seed(7)
+    F = torch.randn(Rg, N, dtype=cdt, device=dev, generator=g) if rank == 0 else None
+    H = torch.randn(Rg, M, dtype=cdt, device=dev, generator=g) if rank == 0 else None
+    fo = torch.empty(Rg, M, dtype=cdt, device=dev) if rank == 0 else None
+    ho = torch.empty(Rg, N, dtype=cdt, device=dev) if rank == 0 else None
+    f_loc = torch.empty(R, N, dtype=cdt, device=dev)
+    h_loc = torch.empty(R, M, dtype=cdt, device=dev)
+    oi = torch.empty(R, M, dtype=cdt, device=dev)
+    oa = torch.empty(R, N, dtype=cdt, device=dev)
+    real = torch.view_as_real
+
+    def chunks(t):
+        return [real(c) for c in t.chunk(ws)] if t is not None else None
+
+    def step():
+        dist.scatter(real(f_loc), chunks(F), src=0)
+        dist.scatter(real(h_loc), chunks(H), src=0)
+        plan.apply(f_loc, out=oi)
+        plan.adjoint_apply(h_loc, out=oa)
+        dist.gather(real(oi), chunks(fo), dst=0)
+        dist.gather(real(oa), chunks(ho), dst=0)
+
+    step()
+    dist.barrier()
+    if torch.cuda.is_available():
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(steps):
+            step()
+        e1.record()
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1) / steps
+    else:  # gloo tests on CPU
+        t0 = time.perf_counter()
+        for _ in range(steps):
+            step()
+        ms = (time.perf_counter() - t0) * 1e3 / steps
+    t = torch.tensor([ms], dtype=torch.float64, device=dev)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms = float(t.item())
+    bytes_moved = int((Rg * (N + M) * 2) * (16 if cdt == torch.complex128 else 8))
+    return {"value": 2 * Rg / (ms / 1e3), "unit": "solves/s", "ms_per_step": ms,
+            "collective_bytes_per_step": bytes_moved,
+            "note": "rank 0 scatters f, h and gathers fhat, f over NCCL each step (SURVEY 8(e))"}
+
+
 def main():
     args = parse()
     if args.impl == "reference":
@@ -362,6 +417,12 @@ def main():
         except Exception as ex:
             e2e = {"value": None, "unit": "solves/s", "error": str(ex)[:300]}
 
+    # ---------------------------------------------------------------- with-communication time (N > 1)
+    dist_e2e = None
+    if ws > 1 and not args.no_dist_e2e:
+        dist_e2e = run_dist_e2e(plan, R, N, M, cdt, ws, rank, torch.device("cuda", dev), max(2, args.e2e_steps),
+                                torch, dist)
+
     # ---------------------------------------------------------------- CPU oracle baseline (rank 0, N = 1)
     cpu = None
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:
@@ -385,7 +446,7 @@ def main():
                        "rhs_per_gpu": R, "global_batch": R * ws, "parallelism": f"rhs-sharded x{ws}",
                        "l2": "inputs larger than L2 (no flush needed)", "precision": args.prec},
             "apply_hbm_gbs": apply_gbs, "apply_hbm_frac": apply_gbs / peak,
-            "roofline": roofline, "stages": stages, "cpu_baseline": cpu, "e2e": e2e,
+            "roofline": roofline, "stages": stages, "cpu_baseline": cpu, "e2e": e2e, "dist_e2e": dist_e2e,
             "gpu_launches": launches, "clocks": clocks,
             "setup": {"plan_s": t_plan, "precompute_s": t_setup, "n_rank_deficient": info["n_rank_deficient"],
                       "max_col_size": info["max_col_size"], "fast_path": info["fast_path"],
