@@ -320,9 +320,8 @@ __host__ __device__ constexpr size_t d_offset(int L, int ST, int SW, int TB) {
 //                     the other rows are zero and never read), output to ybuf.
 template <typename T, int SIGN, int MODE, int L>
 __global__ void __launch_bounds__(Geo<T, L>::NT, 1)
-    k_pass_a(const __grid_constant__ CUtensorMap map, const __grid_constant__ CUtensorMap dmap,
-             const __grid_constant__ CUtensorMap omap, Args<T> A, int BR, int ntiles) {
-    constexpr bool kStageA = false;  // see the store lambda
+    k_pass_a(const __grid_constant__ CUtensorMap map, const __grid_constant__ CUtensorMap dmap, Args<T> A, int BR,
+             int ntiles) {
     extern __shared__ __align__(128) unsigned char smraw[];
     constexpr int CE = (int)(sizeof(C2<T>) / 8);
     using G = Geo<T, L>;
@@ -373,11 +372,7 @@ __global__ void __launch_bounds__(Geo<T, L>::NT, 1)
     if (threadIdx.x == 0 && (int)blockIdx.x < ntiles) issue(blockIdx.x, 0);
     for (int id = blockIdx.x; id < ntiles; id += gridDim.x, ++it) {
         const int b = it & 1;
-        if (threadIdx.x == 0 && id + (int)gridDim.x < ntiles) {
-            // (a bulk wait costs even with nothing outstanding: only when outputs are staged)
-            if (kStageA) bulk_wait_read<0>();  // the previous tile's output store has left b ^ 1
-            issue(id + gridDim.x, b ^ 1);
-        }
+        if (threadIdx.x == 0 && id + (int)gridDim.x < ntiles) issue(id + gridDim.x, b ^ 1);
         const int64_t r = id / tiles_per_rhs;
         const int col0 = (id % tiles_per_rhs) * TA;
         // loads independent of the tile data, issued before waiting for it:
@@ -399,11 +394,9 @@ __global__ void __launch_bounds__(Geo<T, L>::NT, 1)
         // the twiddle products are formed at the first store (last stage), so the table loads
         // issued above complete under the earlier stages instead of stalling here
         C2<T> wq, wcur;
-        // kStageA: outputs staged in tile[b] (consumed by the first stage) as [k1][TA] and
-        // stored by TMA boxes; otherwise plain stores from registers.  The boxes are only TA
-        // columns (64 B) wide: measured on config 5, plain stores are faster for pass A
-        // (0.886 vs 0.944 ms) while pass B gains from staging (0.907 -> 0.854 ms).
-        C2<T>* stg = tile + b * L * TA;
+        // plain stores from registers: staging the outputs in tile[b] and storing them by TMA
+        // boxes (as pass B does) was slower here -- the boxes are only TA columns (64 B) wide
+        // (config 5: 0.944 vs 0.886 ms)
         C2<T>* orow = (MODE == 0) ? A.grid + r * A.GS : A.ybuf + r * A.N;
         auto store = [&](int f, int k1, C2<T> v, int m) {
             if (m == 0) {
@@ -412,20 +405,12 @@ __global__ void __launch_bounds__(Geo<T, L>::NT, 1)
             } else {
                 wcur = cmul<T>(wcur, wq);
             }
-            if (kStageA)
-                stg[k1 * TA + f] = cmul<T>(v, wcur);
-            else
-                orow[(int64_t)k1 * N2 + col0 + f] = cmul<T>(v, wcur);
+            orow[(int64_t)k1 * N2 + col0 + f] = cmul<T>(v, wcur);
         };
         cta_fft<T, SIGN, L>(tws, work, load, store);
-        fence_proxy_async();  // staged outputs / tile[b] reads before the async proxy uses it
-        __syncthreads();      // tile[b] free (or staged), work free for the next iteration
-        if (kStageA && threadIdx.x == 0) {
-            for (int q = 0; q < L; q += BR) tma_store_3d(&omap, col0 * CE, q, (int)r, stg + q * TA);
-            bulk_commit();
-        }
+        fence_proxy_async();  // this thread's reads of tile[b] precede the next TMA into it
+        __syncthreads();      // tile[b] and work free for the next iteration
     }
-    if (kStageA && threadIdx.x == 0) bulk_wait<0>();
 }
 
 // Pass B (rows, length L = N2, TF = TB rows per tile, tile layout [f][S]):
@@ -696,7 +681,7 @@ static fft::Args<T> make_args(Plan& p, FftState& s) {
 }
 
 template <typename T>
-using PassAFn = void (*)(const CUtensorMap, const CUtensorMap, const CUtensorMap, fft::Args<T>, int, int);
+using PassAFn = void (*)(const CUtensorMap, const CUtensorMap, fft::Args<T>, int, int);
 template <typename T>
 using PassBFn = void (*)(const CUtensorMap, const CUtensorMap, fft::Args<T>, int, int, int);
 
@@ -779,14 +764,6 @@ static void launch_pass_a(Plan& p, fft::Args<T>& A, int mode, const void* src, i
                                 sizeof(T) * (uint64_t)A.M, (uint32_t)DW, (uint32_t)BR, (int)sizeof(T));
     }
     if (mode == 0) dmap = map;
-    // output boxes: MODE 0 in place on the grid (same map), MODE 1 into ybuf [R][N1][N2]
-    CUtensorMap omap = map;
-    if (mode == 1 && !make_tmap_3d(&omap, A.ybuf, (uint64_t)A.N2 * CE, (uint64_t)A.N1, (uint64_t)R,
-                                   cs * (uint64_t)A.N2, cs * (uint64_t)A.N, (uint32_t)(TA * CE),
-                                   (uint32_t)std::min(L, 256))) {
-        set_error("cuTensorMapEncodeTiled failed (fused FFT pass A output)");
-        throw Fail{INFT_ERR_CUDA};
-    }
     if (!ok) {
         set_error("cuTensorMapEncodeTiled failed (fused FFT pass A)");
         throw Fail{INFT_ERR_CUDA};
@@ -795,9 +772,7 @@ static void launch_pass_a(Plan& p, fft::Args<T>& A, int mode, const void* src, i
     const int ntiles = (int)(R * (A.N2 / TA));
     ensure_smem_attr((const void*)ka, smem);
     const int occ = occupancy_cached((const void*)ka, threads, smem);
-    ka<<<(unsigned)std::min(ntiles, num_sms() * std::max(1, occ)), threads, smem, st>>>(map, dmap, omap, A,
-                                                                                        mode == 0 ? std::min(L, 256) : BR,
-                                                                                        ntiles);
+    ka<<<(unsigned)std::min(ntiles, num_sms() * std::max(1, occ)), threads, smem, st>>>(map, dmap, A, BR, ntiles);
     INFT_CHECK_LAUNCH();
     p.launches++;
 }
