@@ -324,10 +324,13 @@ __global__ void __launch_bounds__(128, INFT_RING_MINB) k_gather_ring(const __gri
     unsigned char* my_stg = stg + (size_t)warp * OBOX * 4096u;
 
     // chunk = Q segments, or a node-balanced run of segments from the chunk table
-    const int s0 = chunks ? __ldg(chunks + blockIdx.x) : (int)blockIdx.x * Q;
-    const int s1 = chunks ? __ldg(chunks + blockIdx.x + 1) : min(s0 + Q, nseg);
+    // chunk = Q segments, or an entry (s0, s1, first node, end node) of the gather's chunk
+    // table: node-balanced runs of segments, and heavy segments split into node ranges
+    const int s0 = chunks ? __ldg(chunks + 4 * blockIdx.x) : (int)blockIdx.x * Q;
+    const int s1 = chunks ? __ldg(chunks + 4 * blockIdx.x + 1) : min(s0 + Q, nseg);
     const int nbox = s1 - s0 + 1;  // box L = grid points of segment s0 + L (halo covers L = nseg)
-    const int b0 = __ldg(seg_start + s0), b1 = __ldg(seg_start + s1);
+    const int b0 = chunks ? __ldg(chunks + 4 * blockIdx.x + 2) : __ldg(seg_start + s0);
+    const int b1 = chunks ? __ldg(chunks + 4 * blockIdx.x + 3) : __ldg(seg_start + s1);
     const int wrap = N - cshift;
     const int bw = (cshift > 0 && b0 < wrap && wrap < b1) ? wrap : b1;
     const int c1 = (bw - b0 + kNB - 1) / kNB;
@@ -680,6 +683,60 @@ static const int32_t* ring_chunks(Plan& p, int64_t rowgroups, int& nchunks, cuda
     return it->second.buf.as<int32_t>();
 }
 
+// Gather chunks (s0, s1, first node, end node): as ring_chunks, but a segment holding more
+// than T nodes is split into node ranges of about T (each output is independent in the
+// gather; Chebyshev nodes put 651 of 32768 nodes in one segment of config 3).
+static const int32_t* ring_gather_chunks(Plan& p, int64_t rowgroups, int& nchunks, cudaStream_t st) {
+    int dev = 0, nsm = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    const int64_t want = std::max<int64_t>(1, (int64_t)nsm * 8 / std::max<int64_t>(1, rowgroups));
+    const int64_t T = std::max<int64_t>(1, (p.N + want - 1) / want);
+    const int64_t key = -1 - T;  // negative keys: gather tables
+    auto it = p.ring_chunk_cache.find(key);
+    if (it == p.ring_chunk_cache.end()) {
+        const int nseg = (int)p.nseg[0];
+        if (p.seg_host.empty()) {
+            p.seg_host.resize((size_t)nseg + 1);
+            INFT_CUDA(cudaMemcpyAsync(p.seg_host.data(), p.seg_start.p, sizeof(int32_t) * (nseg + 1),
+                                      cudaMemcpyDeviceToHost, st));
+            INFT_CUDA(cudaStreamSynchronize(st));
+        }
+        const std::vector<int32_t>& ss = p.seg_host;
+        std::vector<int32_t> c;
+        int open = 0;  // first segment of the open chunk
+        int64_t acc = 0;
+        auto close = [&](int s1) {
+            if (s1 > open) c.insert(c.end(), {open, s1, ss[open], ss[s1]});
+            open = s1;
+            acc = 0;
+        };
+        for (int sgi = 0; sgi < nseg; ++sgi) {
+            const int64_t n = ss[sgi + 1] - ss[sgi];
+            if (n > T) {  // heavy segment: its own chunks, node ranges of ~T
+                close(sgi);
+                const int parts = (int)((n + T - 1) / T);
+                for (int q = 0; q < parts; ++q)
+                    c.insert(c.end(), {sgi, sgi + 1, (int)(ss[sgi] + n * q / parts), (int)(ss[sgi] + n * (q + 1) / parts)});
+                open = sgi + 1;
+                continue;
+            }
+            acc += n;
+            if (acc >= T || sgi + 1 - open >= ring::kQ) close(sgi + 1);
+        }
+        close(nseg);
+        Plan::ChunkTable ct;
+        ct.n = (int)(c.size() / 4);
+        ct.buf.alloc(sizeof(int32_t) * std::max<size_t>(4, c.size()));
+        if (!c.empty())
+            INFT_CUDA(cudaMemcpyAsync(ct.buf.p, c.data(), sizeof(int32_t) * c.size(), cudaMemcpyHostToDevice, st));
+        INFT_CUDA(cudaStreamSynchronize(st));
+        it = p.ring_chunk_cache.emplace(key, std::move(ct)).first;
+    }
+    nchunks = it->second.n;
+    return it->second.buf.as<int32_t>();
+}
+
 template <typename T>
 static void ring_spread_t(Plan& p, const void* f, void* grid, int64_t R, cudaStream_t st) {
     RingFns<T> F = ring_fns<T>(p.m);
@@ -717,7 +774,7 @@ static void ring_gather_t(Plan& p, const void* grid, void* f, int64_t R, cudaStr
     const int wpb = ring_wpb<T>(R);
     const int nseg = (int)p.nseg[0];
     int nchunks = 0;
-    const int32_t* chunks = ring_chunks(p, ceil_div(R, 32 * wpb), nchunks, st);
+    const int32_t* chunks = ring_gather_chunks(p, ceil_div(R, 32 * wpb), nchunks, st);
     const uint64_t ce = sizeof(C2<T>) / 8;
     const int H = (int)(p.GS - p.Ms[0]);
     k_ring_halo<T><<<(unsigned)std::max<int64_t>(1, std::min<int64_t>(ceil_div(R * H, 256), 4096)), 256, 0, st>>>(
