@@ -225,7 +225,9 @@ struct Geo {
     // first-stage butterfly, so the first stage's strided writes RF j + m spread over the
     // banks) when one wavefront spans several butterflies of a transform (PAD > 1); row
     // stride SW = PAD (mod WAVE) like ST
-    static constexpr int SKD = (PAD > 1 && RF >= 4) ? RF : L;  // skew divisor (L: none)
+    // (radix-8 build: one slot per 8 positions -- conflict-free for first-stage radices 2..8
+    //  at 12.5 % extra rows, which keeps pass B of M_sigma = 2^21 inside 227 KB)
+    static constexpr int SKD = kRB == 8 ? (PAD > 1 ? 8 : L) : ((PAD > 1 && RF >= 4) ? RF : L);  // skew divisor (L: none)
     static constexpr int SW0 = L + L / SKD;
     static constexpr int SW = SW0 + ((PAD - SW0 % WAVE) % WAVE + WAVE) % WAVE;
 };
@@ -488,10 +490,10 @@ __global__ void __launch_bounds__(Geo<T, L>::NT, 1)
         C2<T>* stg = tile + b * S * TB;
         C2<T>* frow = A.fhat + r * A.M;
         auto load = [&](int f, int n2, int, int) -> C2<T> { return tl[f * S + n2]; };
-        // MODE 0 with B2 a multiple of the last stage's span L/16 (e.g. sigma = 2): whether leg m
-        // is kept, its output address and its d slot follow from m alone (warp-uniform tests,
+        // MODE 0 with B2 a multiple of the last stage's span L/kRB (e.g. sigma = 2): whether leg
+        // m is kept, its output address and its d slot follow from m alone (warp-uniform tests,
         // one base per thread)
-        constexpr int NsL = L / 16;
+        constexpr int NsL = L / kRB;
         const bool fastband = (B2 % NsL) == 0;
         const int mlo = B2 / NsL;
         const int jl = threadIdx.x / TB, fl = threadIdx.x - (threadIdx.x / TB) * TB;
@@ -504,7 +506,7 @@ __global__ void __launch_bounds__(Geo<T, L>::NT, 1)
                 if (fastband) {
                     if (m < mlo)
                         sr = jl + m * NsL;
-                    else if (m >= 16 - mlo)
+                    else if (m >= kRB - mlo)
                         sr = jl + m * NsL - (L - 2 * B2);
                     else
                         return;

@@ -895,6 +895,165 @@ __global__ void k_alg1_solve(const double2* __restrict__ K, const int32_t* __res
     }
 }
 
+// ------------------------------------------------------------------ Alg. 1, Gram by grid pairs
+// The normal equations of node j need Re(K_j^* K_j) and M Re K_j^* e_j with
+// K_j = (K(x_h - l/Ms))_{h, l in I(x_j)} and K(t) = sum_k c_k e^{2 pi i k t}, c_k = iw_|k|
+// (= 1/(Ms what(k)); k = -M/2 uses iw_{M/2}).  The Gram entry of two slots depends only on
+// their grid columns l, l + delta (delta = 0..2m), not on the node:
+//   Gam(l, delta) = Re sum_h conj K(x_h - l/Ms) K(x_h - (l + delta)/Ms)
+//                 = Re sum_{|q| < M} Sp(q) C_delta(q) e^{-2 pi i q l / Ms},
+//   Sp(q) = sum_h e^{2 pi i q x_h},   C_delta(q) = sum_k c_{k-q} c_k e^{-2 pi i k delta / Ms}
+// (expand both sums, q = k' - k).  So every node's Gram matrix comes from one node sum Sp
+// (O(N M)), 2m+1 correlations C_delta (FFTs of length 2M) and 2m+1 FFTs of length Ms, instead
+// of forming every K_j (O(N^2)).  The right-hand side
+// M Re K(x_j - l/Ms) comes from the piecewise-Chebyshev table of Re K+ that Alg. 2 uses.
+constexpr int kSpQ = 32;  // consecutive frequencies per thread (phase recurrence length)
+__global__ void __launch_bounds__(128) k_alg1_sp(const double* __restrict__ xs, int64_t N, int64_t M,
+                                                 double2* __restrict__ sp) {
+    __shared__ double xt[1024];
+    const int64_t q0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * kSpQ;
+    double ax[kSpQ], ay[kSpQ];
+#pragma unroll
+    for (int u = 0; u < kSpQ; ++u) ax[u] = ay[u] = 0.0;
+    for (int64_t h0 = 0; h0 < N; h0 += 1024) {
+        const int nh = (int)(N - h0 < 1024 ? N - h0 : 1024);
+        __syncthreads();
+        for (int i = threadIdx.x; i < nh; i += blockDim.x) xt[i] = xs[h0 + i];
+        __syncthreads();
+        if (q0 >= M) continue;
+        for (int i = 0; i < nh; ++i) {
+            const double x = xt[i];
+            // e^{2 pi i q0 x}: the phase q0 x reduced exactly (two-product), then the
+            // recurrence z <- z e^{2 pi i x} over the next kSpQ - 1 frequencies
+            const double hi = (double)q0 * x;
+            const double lo = fma((double)q0, x, -hi);
+            double zs, zc, s1, c1;
+            sincospi(2.0 * ((hi - rint(hi)) + lo), &zs, &zc);
+            sincospi(2.0 * x, &s1, &c1);
+#pragma unroll
+            for (int u = 0; u < kSpQ; ++u) {
+                ax[u] += zc;
+                ay[u] += zs;
+                const double nc = fma(zc, c1, -zs * s1);
+                zs = fma(zc, s1, zs * c1);
+                zc = nc;
+            }
+        }
+    }
+#pragma unroll
+    for (int u = 0; u < kSpQ; ++u)
+        if (q0 + u < M) sp[q0 + u] = make_double2(ax[u], ay[u]);
+}
+
+// rows delta < P: U_delta[n] = c_k e^{-2 pi i k delta / Ms}; row P: V[n] = c_k (k = n - M/2,
+// n < M; zero padded to L = 2M)
+__global__ void k_alg1_corr_in(const double* __restrict__ iw, int64_t M, int64_t Ms, int P, int64_t L,
+                               double2* __restrict__ buf) {
+    const int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (idx >= (int64_t)(P + 1) * L) return;
+    const int r = (int)(idx / L);
+    const int64_t n = idx - (int64_t)r * L;
+    double2 v = make_double2(0.0, 0.0);
+    if (n < M) {
+        const int64_t k = n - M / 2;
+        const double c = iw[k < 0 ? -k : k];
+        if (r == P) {
+            v.x = c;
+        } else {
+            // e^{-2 pi i k delta / Ms}, k delta reduced mod Ms in integers (exact)
+            const int64_t e = ((k * r) % Ms + Ms) % Ms;
+            double sn, cs;
+            sincospi(-2.0 * (double)e / (double)Ms, &sn, &cs);
+            v = make_double2(c * cs, c * sn);
+        }
+    }
+    buf[idx] = v;
+}
+
+// U_delta^ <- U_delta^ conj(V^) / L  (then the inverse FFT gives C_delta(q) at q mod L)
+__global__ void k_alg1_corr_mul(int P, int64_t L, double2* __restrict__ buf) {
+    const int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (idx >= (int64_t)P * L) return;
+    const int64_t nu = idx % L;
+    const double2 u = buf[idx], v = buf[(int64_t)P * L + nu];
+    const double s = 1.0 / (double)L;
+    buf[idx] = make_double2((u.x * v.x + u.y * v.y) * s, (u.y * v.x - u.x * v.y) * s);
+}
+
+// Z_delta[l] = sum_{q = l mod Ms, |q| < M} Sp(q) C_delta(q)   (Sp(-q) = conj Sp(q))
+__global__ void k_alg1_fold(const double2* __restrict__ sp, const double2* __restrict__ corr, int64_t M, int64_t Ms,
+                            int64_t L, int P, double2* __restrict__ z) {
+    const int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (idx >= (int64_t)P * Ms) return;
+    const int r = (int)(idx / Ms);
+    const int64_t l = idx - (int64_t)r * Ms;
+    double ax = 0.0, ay = 0.0;
+    // q = l + t Ms over -M < q < M
+    int64_t q = l - ((l + M - 1) / Ms) * Ms;
+    for (; q < M; q += Ms) {
+        if (q <= -M) continue;
+        double2 s = sp[q < 0 ? -q : q];
+        if (q < 0) s.y = -s.y;
+        const double2 c = corr[(int64_t)r * L + (q < 0 ? q + L : q)];
+        ax += s.x * c.x - s.y * c.y;
+        ay += s.x * c.y + s.y * c.x;
+    }
+    z[idx] = make_double2(ax, ay);
+}
+
+// Per node j (one CTA): Gram from Gam (real parts of the transformed Z rows), rhs from the
+// Re K+ table, then the same min-norm eigen-solve as k_alg1_solve.
+__global__ void k_alg1_solve_gam(const double2* __restrict__ gam, KTab tab, const int32_t* __restrict__ n0s,
+                                 const int32_t* __restrict__ l0s, const double* __restrict__ xs, int64_t N,
+                                 int64_t Ms, int m, int P, double Mscale, double tau2, double* __restrict__ w64,
+                                 unsigned long long* __restrict__ ndrop) {
+    extern __shared__ double sm[];
+    const int nmax = P;
+    const int ld = nmax + 1;
+    double* A = sm;
+    double* V = A + nmax * ld;
+    double* y = V + nmax * ld;
+    double* u = y + nmax;
+    double* b = u + nmax;
+    int* lt = reinterpret_cast<int*>(b + nmax);
+    double* cs = reinterpret_cast<double*>(lt + nmax + (nmax & 1));
+    int* pq = reinterpret_cast<int*>(cs + nmax + 2);
+    int* cntr = pq + nmax + 2;
+    for (int64_t j = blockIdx.x; j < N; j += gridDim.x) {
+        if (threadIdx.x == 0) {
+            int k = 0;
+            for (int t = 0; t < P; t++) {
+                bool live = in_support(xs[j], l0s[j], t, Ms, m);
+                for (int t2 = t - (int)Ms; live && t2 >= 0; t2 -= (int)Ms)
+                    if (in_support(xs[j], l0s[j], t2, Ms, m)) live = false;
+                if (live) lt[k++] = t;
+            }
+            *cntr = k;
+        }
+        __syncthreads();
+        const int nc = *cntr;
+        for (int idx = threadIdx.x; idx < nc * nc; idx += blockDim.x) {
+            const int a = idx / nc, c = idx % nc;
+            if (c < a) continue;
+            const int64_t la = md(n0s[j] + lt[a], Ms);
+            const double s = gam[(int64_t)(lt[c] - lt[a]) * Ms + la].x;
+            A[a * ld + c] = s;
+            A[c * ld + a] = s;
+        }
+        for (int a = threadIdx.x; a < nc; a += blockDim.x) {
+            const int64_t la = md(n0s[j] + lt[a], Ms);
+            y[a] = Mscale * tab_eval(tab, tab.cK, wrapd(xs[j] - (double)la / (double)Ms));
+        }
+        __syncthreads();
+        jacobi_eig(A, V, nc, ld, cs, pq, cntr);
+        __syncthreads();
+        int dropped = minnorm_from_eig(A, V, nc, ld, y, u, b, tau2);
+        for (int a = threadIdx.x; a < nc; a += blockDim.x) w64[j * P + lt[a]] = b[a];
+        if (threadIdx.x == 0 && dropped > 0) atomicAdd(ndrop, 1ull);
+        __syncthreads();
+    }
+}
+
 // ------------------------------------------------------------------ plain window B
 // w[i][t] = w~_m(x - l/Ms) = sum_z w_m(x - l/Ms + z) on live slots (eq. matrix_B, A7).
 __global__ void k_window_weights(const double* __restrict__ xs, const int32_t* __restrict__ l0s, int64_t N, int d,
@@ -1128,25 +1287,71 @@ static void alg2(Plan& p, double tau, DevBuf& w64, cudaStream_t st) {
     }
 }
 
-static void alg1(Plan& p, double tau, DevBuf& w64, cudaStream_t st) {
-    if (p.d != 1) {
-        set_error("Alg. 1 (node-wise) is implemented for d = 1");
-        throw Fail{INFT_ERR_UNSUPPORTED};
+// Alg. 1 normal equations: dense K (INFT_ALG1=dense; N * M_sigma <= 2^28) or Gram by grid
+// pairs (INFT_ALG1=gram; default once N * M_sigma > 2^24, see k_alg1_sp)
+static bool alg1_use_gram(const Plan& p) {
+    const char* e = getenv("INFT_ALG1");
+    if (e && !strcmp(e, "gram")) return true;
+    if (e && !strcmp(e, "dense")) return false;
+    return (double)p.N * (double)p.Ms[0] > (double)(1ll << 24);
+}
+
+static void cufft_z2z_many(int64_t n, int batch, double2* data, int dir, cudaStream_t st, const char* what) {
+    cufftHandle h;
+    int nn[1] = {(int)n};
+    INFT_CUFFT(cufftPlanMany(&h, 1, nn, nullptr, 1, (int)n, nullptr, 1, (int)n, CUFFT_Z2Z, batch));
+    cufftSetStream(h, st);
+    const cufftResult r = cufftExecZ2Z(h, (cufftDoubleComplex*)data, (cufftDoubleComplex*)data, dir);
+    cufftDestroy(h);
+    if (r != CUFFT_SUCCESS) {
+        set_error(std::string("cufftExecZ2Z failed: ") + what);
+        throw Fail{INFT_ERR_CUFFT};
     }
+}
+
+static void alg1_gram(Plan& p, DevBuf& xs, DevBuf& l0s, DevBuf& iw, double tau, size_t solve_smem, DevBuf& w64,
+                      DevBuf& ndrop, cudaStream_t st) {
     const int64_t N = p.N, M = p.M[0], Ms = p.Ms[0];
-    if ((double)N * (double)Ms > (double)(1ll << 28)) {
-        set_error("Alg. 1 forms K = A D^* F^* densely: N * M_sigma must be <= 2^28");
-        throw Fail{INFT_ERR_UNSUPPORTED};
-    }
-    if (N == 0) return;
-    DevBuf xs, l0s, iw, K;
-    xs.alloc(sizeof(double) * N);
-    l0s.alloc(sizeof(int32_t) * N);
-    k_sorted_nodes<<<nblk(N), 256, 0, st>>>(p.nodes.as<double>(), p.l0.as<int32_t>(), p.perm.as<int32_t>(), N, 1,
-                                            xs.as<double>(), l0s.as<int32_t>());
-    iw.alloc(sizeof(double) * (M / 2 + 1));
-    k_inv_what<<<nblk(M / 2 + 1), 256, 0, st>>>(iw.as<double>(), M, Ms, p.m, p.sigma,
-                                                 p.window == INFT_DIRICHLET ? 1 : 0);
+    const int P = p.P;
+    // Sp(q) = sum_h e^{2 pi i q x_h}, q in [0, M)
+    DevBuf sp, cb, zb;
+    sp.alloc(sizeof(double2) * M);
+    const int64_t nthr = ceil_div(M, (int64_t)kSpQ);
+    k_alg1_sp<<<(unsigned)ceil_div(nthr, (int64_t)128), 128, 0, st>>>(xs.as<double>(), N, M, sp.as<double2>());
+    INFT_CHECK_LAUNCH();
+    // C_delta(q), |q| < M: correlations by FFTs of length L = 2M (no wrap)
+    const int64_t L = 2 * M;
+    cb.alloc(sizeof(double2) * (size_t)(P + 1) * L);
+    k_alg1_corr_in<<<nblk((int64_t)(P + 1) * L), 256, 0, st>>>(iw.as<double>(), M, Ms, P, L, cb.as<double2>());
+    INFT_CHECK_LAUNCH();
+    cufft_z2z_many(L, P + 1, cb.as<double2>(), CUFFT_FORWARD, st, "Alg. 1 correlation (forward)");
+    k_alg1_corr_mul<<<nblk((int64_t)P * L), 256, 0, st>>>(P, L, cb.as<double2>());
+    INFT_CHECK_LAUNCH();
+    cufft_z2z_many(L, P, cb.as<double2>(), CUFFT_INVERSE, st, "Alg. 1 correlation (inverse)");
+    // Gam(l, delta) = Re FFT_l[ sum_{q = l mod Ms} Sp(q) C_delta(q) ]
+    zb.alloc(sizeof(double2) * (size_t)P * Ms);
+    k_alg1_fold<<<nblk((int64_t)P * Ms), 256, 0, st>>>(sp.as<double2>(), cb.as<double2>(), M, Ms, L, P,
+                                                          zb.as<double2>());
+    INFT_CHECK_LAUNCH();
+    cufft_z2z_many(Ms, P, zb.as<double2>(), CUFFT_FORWARD, st, "Alg. 1 Gram table");
+    // rhs table: Re K+ on |x| <= (2m+1)/Ms
+    Tables T;
+    build_tables(p, 0, T, std::min(1.0, (2.0 * p.m + 1.0) / (double)Ms), st);
+    ensure_smem_attr((const void*)k_alg1_solve_gam, solve_smem);
+    k_alg1_solve_gam<<<(unsigned)std::min<int64_t>(N, 148 * 16), 64, solve_smem, st>>>(
+        zb.as<double2>(), T.tab, p.n0s.as<int32_t>(), l0s.as<int32_t>(), xs.as<double>(), N, Ms, p.m, P,
+        (double)M, tau * tau, w64.as<double>(), ndrop.as<unsigned long long>());
+    INFT_CHECK_LAUNCH();
+    p.launches += 5;
+    INFT_CUDA(cudaStreamSynchronize(st));  // the buffers above die here
+}
+
+// dense form: K = A D^* F^* row by row (one FFT of length Ms per node), Gram sums over all rows
+static void alg1_dense(Plan& p, DevBuf& xs, DevBuf& l0s, DevBuf& iw, double tau, size_t solve_smem, DevBuf& w64,
+                       DevBuf& ndrop, cudaStream_t st) {
+    const int64_t N = p.N, M = p.M[0], Ms = p.Ms[0];
+    const int P = p.P;
+    DevBuf K;
     K.alloc(sizeof(double2) * N * Ms);
     k_alg1_rows<<<nblk(N * Ms), 256, 0, st>>>(xs.as<double>(), iw.as<double>(), N, M, Ms, K.as<double2>());
     INFT_CHECK_LAUNCH();
@@ -1161,18 +1366,46 @@ static void alg1(Plan& p, double tau, DevBuf& w64, cudaStream_t st) {
         set_error("cufftExecZ2Z (Alg. 1 kernel matrix) failed");
         throw Fail{INFT_ERR_CUFFT};
     }
-    DevBuf ndrop;
-    ndrop.alloc(sizeof(unsigned long long));
-    INFT_CUDA(cudaMemsetAsync(ndrop.p, 0, sizeof(unsigned long long), st));
-    int P = p.P;
-    size_t smem = sizeof(double) * (2 * (size_t)P * (P + 1) + 3 * P) + sizeof(int) * (P + 1) +
-                  sizeof(double) * (P + 2) + sizeof(int) * (P + 2) + sizeof(int) * 4 + 64;
-    ensure_smem_attr((const void*)k_alg1_solve, smem);
-    k_alg1_solve<<<(unsigned)std::min<int64_t>(N, 148 * 16), 64, smem, st>>>(
+    ensure_smem_attr((const void*)k_alg1_solve, solve_smem);
+    k_alg1_solve<<<(unsigned)std::min<int64_t>(N, 148 * 16), 64, solve_smem, st>>>(
         K.as<double2>(), p.n0s.as<int32_t>(), l0s.as<int32_t>(), xs.as<double>(), N, Ms, p.m, P, (double)M,
         tau * tau, w64.as<double>(), ndrop.as<unsigned long long>());
     INFT_CHECK_LAUNCH();
     p.launches++;
+    INFT_CUDA(cudaStreamSynchronize(st));  // K dies here
+}
+
+static void alg1(Plan& p, double tau, DevBuf& w64, cudaStream_t st) {
+    if (p.d != 1) {
+        set_error("Alg. 1 (node-wise) is implemented for d = 1");
+        throw Fail{INFT_ERR_UNSUPPORTED};
+    }
+    const int64_t N = p.N, M = p.M[0], Ms = p.Ms[0];
+    const bool gram = alg1_use_gram(p);
+    if (!gram && (double)N * (double)Ms > (double)(1ll << 28)) {
+        set_error("Alg. 1 dense form (INFT_ALG1=dense) needs N * M_sigma <= 2^28");
+        throw Fail{INFT_ERR_UNSUPPORTED};
+    }
+    if (N == 0) return;
+    DevBuf xs, l0s, iw;
+    xs.alloc(sizeof(double) * N);
+    l0s.alloc(sizeof(int32_t) * N);
+    k_sorted_nodes<<<nblk(N), 256, 0, st>>>(p.nodes.as<double>(), p.l0.as<int32_t>(), p.perm.as<int32_t>(), N, 1,
+                                            xs.as<double>(), l0s.as<int32_t>());
+    iw.alloc(sizeof(double) * (M / 2 + 1));
+    k_inv_what<<<nblk(M / 2 + 1), 256, 0, st>>>(iw.as<double>(), M, Ms, p.m, p.sigma,
+                                                 p.window == INFT_DIRICHLET ? 1 : 0);
+    DevBuf ndrop;
+    ndrop.alloc(sizeof(unsigned long long));
+    INFT_CUDA(cudaMemsetAsync(ndrop.p, 0, sizeof(unsigned long long), st));
+    const int P = p.P;
+    const size_t solve_smem = sizeof(double) * (2 * (size_t)P * (P + 1) + 3 * P) + sizeof(int) * (P + 1) +
+                              sizeof(double) * (P + 2) + sizeof(int) * (P + 2) + sizeof(int) * 4 + 64;
+    if (gram) {
+        alg1_gram(p, xs, l0s, iw, tau, solve_smem, w64, ndrop, st);
+    } else {
+        alg1_dense(p, xs, l0s, iw, tau, solve_smem, w64, ndrop, st);
+    }
     unsigned long long nd = 0;
     INFT_CUDA(cudaMemcpyAsync(&nd, ndrop.p, sizeof(nd), cudaMemcpyDeviceToHost, st));
     INFT_CUDA(cudaStreamSynchronize(st));
