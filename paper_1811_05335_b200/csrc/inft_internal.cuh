@@ -171,9 +171,11 @@ struct Plan {
     struct ChunkTable {
         DevBuf buf;
         int n = 0;
+        int nfix = 0, nslots = 0;  // spread tables: fix entries after the chunks, side slots
     };
     std::map<int64_t, ChunkTable> ring_chunk_cache;
     std::vector<int32_t> seg_host;  // host copy of seg_start (1-D)
+    DevBuf ring_side;               // ring spread: side slots of split heavy segments [slot][R][2m]
     int64_t state_version = 0;  // bumped whenever weights / tables change
     cudaStream_t s_graph = nullptr;
     cudaEvent_t ev_g0 = nullptr, ev_g1 = nullptr;

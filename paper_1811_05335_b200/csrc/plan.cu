@@ -83,7 +83,7 @@ void DevBuf::free_() {
 
 size_t Plan::workspace_bytes() const {
     size_t t = nodes.bytes + l0.bytes + bin.bytes + perm.bytes + seg_start.bytes + n0s.bytes +
-               delta.bytes + dk.bytes + dkf.bytes + w.bytes + w64.bytes + grid.bytes + fT.bytes;
+               delta.bytes + dk.bytes + dkf.bytes + w.bytes + w64.bytes + grid.bytes + fT.bytes + ring_side.bytes;
     for (int i = 0; i < 2; i++) t += stage_in[i].bytes + stage_out[i].bytes;
     for (auto& kv : fft) {
         size_t ws = 0;

@@ -37,6 +37,10 @@ namespace ring {
 #define INFT_RING_MINB 1
 #endif
 constexpr int kQ = 32;                     // segments per chunk (one CTA)
+// spread table modes (ring_spread_table)
+constexpr int kSidePart = 1;   // node range of a heavy segment: own half and spill to side slots
+constexpr int kSideNoPro = 2;  // previous segment heavy: no prologue (its parts' spills are added)
+constexpr int kSideCarry = 4;  // next segment heavy: spill into s1 to a side slot
 constexpr int kNB = INFT_RING_NB;          // nodes per staged batch
 constexpr int kStages = INFT_RING_STAGES;  // spread load pipeline depth (2: more CTAs per SM beat a deeper pipe)
 #ifndef INFT_RING_STAGES_G
@@ -78,7 +82,7 @@ __global__ void __launch_bounds__(128, INFT_RING_MINB) k_spread_ring(const __gri
                                                      const int32_t* __restrict__ seg_start,
                                                      const int32_t* __restrict__ chunks,
                                                      const T* __restrict__ w, int PPrt, int nseg, int Q, int N,
-                                                     int cshift) {
+                                                     int cshift, C2<T>* __restrict__ side, int R) {
     constexpr int SEG = 2 * MC;
     constexpr int VEC = 16 / (int)sizeof(T);
     constexpr int PP = ((2 * MC + 2 + VEC - 1) / VEC) * VEC;  // record stride (host: Plan::PP)
@@ -107,12 +111,21 @@ __global__ void __launch_bounds__(128, INFT_RING_MINB) k_spread_ring(const __gri
     uint64_t* empty = full + kStages;
     unsigned char* my_stg = stg + (size_t)warp * SBOX * 4096u;
 
-    // chunk = Q segments, or a node-balanced run of segments from the chunk table
-    const int s0 = chunks ? __ldg(chunks + blockIdx.x) : (int)blockIdx.x * Q;
-    const int s1 = chunks ? __ldg(chunks + blockIdx.x + 1) : min(s0 + Q, nseg);
+    // chunk = Q segments, or an entry (s0, s1, first node, end node, mode, slot) of the spread
+    // table (ring_spread_table): node-balanced runs of segments, and heavy segments split into
+    // node ranges whose windows go to side slots (kSidePart); a run next to a heavy segment
+    // skips the prologue (kSideNoPro) and/or parks its spill into segment s1 (kSideCarry);
+    // k_spread_ring_fix adds the side slots in a fixed order
+    const int* ce = chunks + 6 * blockIdx.x;
+    const int s0 = chunks ? __ldg(ce) : (int)blockIdx.x * Q;
+    const int s1 = chunks ? __ldg(ce + 1) : min(s0 + Q, nseg);
+    const int mode = chunks ? __ldg(ce + 4) : 0;
+    const int slot = chunks ? __ldg(ce + 5) : 0;
     const int sp = s0 == 0 ? nseg - 1 : s0 - 1;
-    const int a0 = __ldg(seg_start + sp), a1 = __ldg(seg_start + sp + 1);
-    const int b0 = __ldg(seg_start + s0), b1 = __ldg(seg_start + s1);
+    const bool pro_on = !(mode & (kSideNoPro | kSidePart));
+    const int a0 = pro_on ? __ldg(seg_start + sp) : 0, a1 = pro_on ? __ldg(seg_start + sp + 1) : 0;
+    const int b0 = chunks ? __ldg(ce + 2) : __ldg(seg_start + s0);
+    const int b1 = chunks ? __ldg(ce + 3) : __ldg(seg_start + s1);
     const int wrap = N - cshift;
     const int aw = (cshift > 0 && a0 < wrap && wrap < a1) ? wrap : a1;
     const int bw = (cshift > 0 && b0 < wrap && wrap < b1) ? wrap : b1;
@@ -166,9 +179,19 @@ __global__ void __launch_bounds__(128, INFT_RING_MINB) k_spread_ring(const __gri
 
     // finish segment cur_k: store its own half (main segments only), zero it, advance.
     // The half is selected by a branch (never a runtime register index).
+    // side slot q of this lane's row: [q][R][SEG] complex (plain stores: 16 consecutive values)
+    auto side_store = [&](int q, int H0) {
+        if (row0 + (int)threadIdx.x < R) {
+            C2<T>* dst = side + ((int64_t)q * R + row0 + threadIdx.x) * SEG;
+#pragma unroll
+            for (int u = 0; u < SEG; ++u) dst[u] = mk<T>(ax[H0 + u], ay[H0 + u]);
+        }
+    };
     auto store_half = [&](auto HALF) {
         constexpr int H0 = decltype(HALF)::value * SEG;
-        if (cur_k >= 1) {
+        if (cur_k >= 1 && (mode & kSidePart)) {
+            side_store(2 * slot, H0);  // a part of a heavy segment: its own half to the side
+        } else if (cur_k >= 1) {
             if (lane == 0) bulk_wait_read<0>();  // staging tile free again
             __syncwarp();
 #pragma unroll
@@ -282,7 +305,56 @@ __global__ void __launch_bounds__(128, INFT_RING_MINB) k_spread_ring(const __gri
         }
     }
     while (cur_k <= s1 - s0) flush();
+    // the window's first half now holds the spill into segment s1
+    if (mode & kSidePart) side_store(2 * slot + 1, 0);
+    if (mode & kSideCarry) side_store(slot, 0);
     if (lane == 0) bulk_wait<0>();
+}
+
+// Side slots back into the grid (after k_spread_ring; one thread per (entry, row, u)):
+// entry (t, kind, p0, p1, q0, q1, c, -) --
+//   kind 0, heavy segment t: grid[t] = spill in + sum_{p0..p1} own(p), spill in = carry slot c
+//           of the run ending at t, or (c < 0, t - 1 heavy too) sum_{q0..q1} spill(q);
+//   kind 1, segment t after a heavy one: grid[t] += sum_{q0..q1} spill(q).
+// Parts are slots 2p (own) / 2p + 1 (spill); carries are single slots; fixed summation order.
+template <typename T, int SEG>
+__global__ void k_spread_ring_fix(const int32_t* __restrict__ fix, int nfix, const C2<T>* __restrict__ side,
+                                  C2<T>* __restrict__ grid, int64_t GS, int R) {
+    const int64_t total = (int64_t)nfix * R * SEG;
+    for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
+         idx += (int64_t)gridDim.x * blockDim.x) {
+        const int u = (int)(idx % SEG);
+        const int64_t rr = idx / SEG;
+        const int r = (int)(rr % R);
+        const int e = (int)(rr / R);
+        const int* f = fix + 8 * e;
+        const int t = f[0], kind = f[1], p0 = f[2], p1 = f[3], q0 = f[4], q1 = f[5], c = f[6];
+        auto at = [&](int q) { return side[((int64_t)q * R + r) * SEG + u]; };
+        T x = 0, y = 0;
+        if (kind == 0 && c >= 0) {
+            const C2<T> v = at(c);
+            x = v.x;
+            y = v.y;
+        } else {
+            for (int q = q0; q < q1; ++q) {
+                const C2<T> v = at(2 * q + 1);
+                x += v.x;
+                y += v.y;
+            }
+        }
+        C2<T>* g = grid + (int64_t)r * GS + (int64_t)t * SEG + u;
+        if (kind == 0) {
+            for (int q = p0; q < p1; ++q) {
+                const C2<T> v = at(2 * q);
+                x += v.x;
+                y += v.y;
+            }
+            *g = mk<T>(x, y);
+        } else {
+            const C2<T> v = *g;
+            *g = mk<T>(v.x + x, v.y + y);
+        }
+    }
 }
 
 // ------------------------------------------------------------------------- gather
@@ -551,7 +623,8 @@ __global__ void __launch_bounds__(128, INFT_RING_MINB) k_gather_ring(const __gri
 template <typename T>
 struct RingFns {
     void (*spread)(const CUtensorMap, const CUtensorMap, const int32_t*, const int32_t*, const T*, int, int, int, int,
-                   int) = nullptr;
+                   int, C2<T>*, int) = nullptr;
+    void (*fix)(const int32_t*, int, const C2<T>*, C2<T>*, int64_t, int) = nullptr;
     void (*gather)(const CUtensorMap, const CUtensorMap, const int32_t*, const int32_t*, const T*, int, C2<T>*, int64_t,
                    int, int, int, int) = nullptr;
 };
@@ -564,14 +637,17 @@ static RingFns<T> ring_fns(int m) {
         if (m == 4) {
             F.spread = ring::k_spread_ring<T, 4>;
             F.gather = ring::k_gather_ring<T, 4>;
+            F.fix = ring::k_spread_ring_fix<T, 8>;
         }
     }
     if (m == 8) {
         F.spread = ring::k_spread_ring<T, 8>;
         F.gather = ring::k_gather_ring<T, 8>;
+        F.fix = ring::k_spread_ring_fix<T, 16>;
     } else if (m == 16) {
         F.spread = ring::k_spread_ring<T, 16>;
         F.gather = ring::k_gather_ring<T, 16>;
+        F.fix = ring::k_spread_ring_fix<T, 32>;
     }
     return F;
 }
@@ -645,16 +721,37 @@ static void tmap_or_throw(CUtensorMap* m, const void* base, uint64_t inner, uint
     }
 }
 
-// Chunks of consecutive segments, one CTA each (per row group): balanced by node count, not
-// by segment count, so that dense regions (Chebyshev edges) do not set the tail.  A chunk
-// closes at >= T nodes or kQ segments, T = N / (~8 CTAs per SM / row groups).  Cached per T.
-static const int32_t* ring_chunks(Plan& p, int64_t rowgroups, int& nchunks, cudaStream_t st) {
+// target chunk-CTAs per SM over all row groups (INFT_RING_CPS, default 16; config 3 c128:
+// 8 -> 0.516 ms/step, 16 -> 0.477, 32 -> 0.469; config 5 unchanged within noise)
+static int ring_cps() {
+    static const int v = [] {
+        const char* e = getenv("INFT_RING_CPS");
+        const int x = e ? atoi(e) : 0;
+        return x >= 1 && x <= 256 ? x : 16;
+    }();
+    return v;
+}
+
+// Spread table: as ring_gather_chunks (defined below), entries (s0, s1, first node, end node, mode, slot), but
+// a heavy segment's node ranges cannot write the grid directly (they share its cells and its
+// spill into the next segment): each writes its window halves to side slots, and the runs
+// around it skip the prologue / park their spill (kSide*); the fix entries (8 ints, see
+// k_spread_ring_fix) sum the side slots into the grid in a fixed order.  Without heavy
+// segments this is ring_chunks' table with no side slots.
+struct SpreadTable {
+    const int32_t* chunks = nullptr;
+    const int32_t* fix = nullptr;
+    int nchunks = 0, nfix = 0, nslots = 0;
+};
+
+static SpreadTable ring_spread_table(Plan& p, int64_t rowgroups, cudaStream_t st) {
     int dev = 0, nsm = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-    const int64_t want = std::max<int64_t>(1, (int64_t)nsm * 8 / std::max<int64_t>(1, rowgroups));
+    const int64_t want = std::max<int64_t>(1, (int64_t)nsm * ring_cps() / std::max<int64_t>(1, rowgroups));
     const int64_t T = std::max<int64_t>(1, (p.N + want - 1) / want);
-    auto it = p.ring_chunk_cache.find(T);
+    const int64_t key = (int64_t(1) << 40) + T;  // spread tables
+    auto it = p.ring_chunk_cache.find(key);
     if (it == p.ring_chunk_cache.end()) {
         const int nseg = (int)p.nseg[0];
         if (p.seg_host.empty()) {
@@ -663,34 +760,96 @@ static const int32_t* ring_chunks(Plan& p, int64_t rowgroups, int& nchunks, cuda
                                       cudaMemcpyDeviceToHost, st));
             INFT_CUDA(cudaStreamSynchronize(st));
         }
-        std::vector<int32_t> c{0};
+        const std::vector<int32_t>& ss = p.seg_host;
+        auto heavy = [&](int sg) {
+            sg = ((sg % nseg) + nseg) % nseg;
+            return ss[sg + 1] - ss[sg] > T;
+        };
+        // pass 1: runs and parts; part indices per heavy segment
+        std::vector<int32_t> c;          // 6 ints per chunk
+        std::vector<int> part0(nseg + 1, 0);  // first part index of heavy segment s (prefix)
+        int nparts = 0;
+        int open = 0;
         int64_t acc = 0;
+        auto close = [&](int s1) {
+            if (s1 > open) {
+                int mode = 0;
+                if (heavy(open - 1)) mode |= ring::kSideNoPro;
+                if (heavy(s1)) mode |= ring::kSideCarry;
+                c.insert(c.end(), {open, s1, ss[open], ss[s1], mode, -1});
+            }
+            open = s1;
+            acc = 0;
+        };
         for (int sgi = 0; sgi < nseg; ++sgi) {
-            acc += p.seg_host[sgi + 1] - p.seg_host[sgi];
-            if (acc >= T || sgi + 1 - c.back() >= ring::kQ || sgi + 1 == nseg) {
-                c.push_back(sgi + 1);
-                acc = 0;
+            const int64_t n = ss[sgi + 1] - ss[sgi];
+            part0[sgi] = nparts;
+            if (n > T) {
+                close(sgi);
+                const int parts = (int)((n + T - 1) / T);
+                for (int q = 0; q < parts; ++q)
+                    c.insert(c.end(), {sgi, sgi + 1, (int)(ss[sgi] + n * q / parts),
+                                       (int)(ss[sgi] + n * (q + 1) / parts), ring::kSidePart, nparts++});
+                open = sgi + 1;
+                continue;
+            }
+            acc += n;
+            if (acc >= T || sgi + 1 - open >= ring::kQ) close(sgi + 1);
+        }
+        close(nseg);
+        part0[nseg] = nparts;
+        // carry slots after the part slots; carry_of[t] = slot of the run ending at t
+        int nslots = 2 * nparts;
+        std::vector<int> carry_of(nseg, -1);
+        for (size_t i = 0; i < c.size(); i += 6)
+            if (c[i + 4] & ring::kSideCarry) {
+                c[i + 5] = nslots;
+                carry_of[c[i + 1] % nseg] = nslots++;
+            }
+        // fix entries
+        std::vector<int32_t> fx;
+        for (int t = 0; t < nseg && nparts > 0; ++t) {
+            const int tp = (t + nseg - 1) % nseg;
+            const bool hp = heavy(tp);
+            const int q0 = part0[tp], q1 = part0[tp + 1];
+            if (heavy(t)) {
+                fx.insert(fx.end(), {t, 0, part0[t], part0[t + 1], hp ? q0 : 0, hp ? q1 : 0, hp ? -1 : carry_of[t], 0});
+            } else if (hp) {
+                fx.insert(fx.end(), {t, 1, 0, 0, q0, q1, -1, 0});
             }
         }
         Plan::ChunkTable ct;
-        ct.n = (int)c.size() - 1;
-        ct.buf.alloc(sizeof(int32_t) * c.size());
-        INFT_CUDA(cudaMemcpyAsync(ct.buf.p, c.data(), sizeof(int32_t) * c.size(), cudaMemcpyHostToDevice, st));
+        ct.n = (int)(c.size() / 6);
+        ct.nfix = (int)(fx.size() / 8);
+        ct.nslots = nslots;
+        std::vector<int32_t> all(c);
+        all.insert(all.end(), fx.begin(), fx.end());
+        ct.buf.alloc(sizeof(int32_t) * std::max<size_t>(8, all.size()));
+        if (!all.empty())
+            INFT_CUDA(cudaMemcpyAsync(ct.buf.p, all.data(), sizeof(int32_t) * all.size(), cudaMemcpyHostToDevice, st));
         INFT_CUDA(cudaStreamSynchronize(st));
-        it = p.ring_chunk_cache.emplace(T, std::move(ct)).first;
+        it = p.ring_chunk_cache.emplace(key, std::move(ct)).first;
     }
-    nchunks = it->second.n;
-    return it->second.buf.as<int32_t>();
+    SpreadTable t;
+    t.nchunks = it->second.n;
+    t.nfix = it->second.nfix;
+    t.nslots = it->second.nslots;
+    t.chunks = it->second.buf.as<int32_t>();
+    t.fix = t.chunks + 6 * t.nchunks;
+    return t;
 }
 
-// Gather chunks (s0, s1, first node, end node): as ring_chunks, but a segment holding more
+// Chunks of consecutive segments, one CTA each (per row group): balanced by node count, not
+// by segment count, so that dense regions (Chebyshev edges) do not set the tail.  A chunk
+// closes at >= T nodes or kQ segments, T = N / (~8 CTAs per SM / row groups).  Cached per T.
+// Gather chunks (s0, s1, first node, end node): a segment holding more
 // than T nodes is split into node ranges of about T (each output is independent in the
 // gather; Chebyshev nodes put 651 of 32768 nodes in one segment of config 3).
 static const int32_t* ring_gather_chunks(Plan& p, int64_t rowgroups, int& nchunks, cudaStream_t st) {
     int dev = 0, nsm = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-    const int64_t want = std::max<int64_t>(1, (int64_t)nsm * 8 / std::max<int64_t>(1, rowgroups));
+    const int64_t want = std::max<int64_t>(1, (int64_t)nsm * ring_cps() / std::max<int64_t>(1, rowgroups));
     const int64_t T = std::max<int64_t>(1, (p.N + want - 1) / want);
     const int64_t key = -1 - T;  // negative keys: gather tables
     auto it = p.ring_chunk_cache.find(key);
@@ -742,8 +901,14 @@ static void ring_spread_t(Plan& p, const void* f, void* grid, int64_t R, cudaStr
     RingFns<T> F = ring_fns<T>(p.m);
     const int wpb = ring_wpb<T>(R);
     const int nseg = (int)p.nseg[0];
-    int nchunks = 0;
-    const int32_t* chunks = ring_chunks(p, ceil_div(R, 32 * wpb), nchunks, st);
+    const SpreadTable tb = ring_spread_table(p, ceil_div(R, 32 * wpb), st);
+    const int nchunks = tb.nchunks;
+    const int32_t* chunks = tb.chunks;
+    const size_t side_bytes = sizeof(C2<T>) * (size_t)tb.nslots * (size_t)R * p.S[0];
+    if (side_bytes > p.ring_side.bytes) {
+        p.ring_side.alloc(side_bytes);
+        p.state_version++;
+    }
     const uint64_t ce = sizeof(C2<T>) / 8;
     CUtensorMap fm, gm;
     tmap_or_throw(&fm, f, (uint64_t)p.N * ce, (uint64_t)R, sizeof(C2<T>) * (uint64_t)p.N, 32u, "spread f");
@@ -752,9 +917,16 @@ static void ring_spread_t(Plan& p, const void* f, void* grid, int64_t R, cudaStr
     ensure_smem_attr((const void*)F.spread, smem);
     dim3 g((unsigned)nchunks, (unsigned)ceil_div(R, 32 * wpb));
     F.spread<<<g, 32 * wpb, smem, st>>>(fm, gm, p.seg_start.as<int32_t>(), chunks, p.w.as<T>(), p.PP, nseg, 0,
-                                        (int)p.N, p.perm_shift);
+                                        (int)p.N, p.perm_shift, p.ring_side.as<C2<T>>(), (int)R);
     INFT_CHECK_LAUNCH();
     p.launches++;
+    if (tb.nfix > 0) {
+        const int64_t total = (int64_t)tb.nfix * R * p.S[0];
+        F.fix<<<(unsigned)std::min<int64_t>(ceil_div(total, 256), 4096), 256, 0, st>>>(
+            tb.fix, tb.nfix, p.ring_side.as<C2<T>>(), static_cast<C2<T>*>(grid), p.GS, (int)R);
+        INFT_CHECK_LAUNCH();
+        p.launches++;
+    }
 }
 
 template <typename T>
