@@ -97,7 +97,7 @@ typedef struct {
     int64_t max_col_size;      /* max |I(l)| (Alg. 2) or max |I(x_j)| (Alg. 1) */
     double max_abs_w;          /* max |B_opt entry| */
     int32_t perm_identity;     /* 1 if the bin sort left the caller's node order unchanged */
-    int32_t fast_path;         /* 1 if the register-window spread/gather kernels are used */
+    int32_t fast_path;         /* 1: register-window spread/gather kernels, 2: their TMA-staged ring variant */
     int32_t fused_fft;         /* 1 if the fused two-pass FFT (with deconvolution) replaces cuFFT */
     int32_t max_lowrank_rank;  /* Alg. 2: largest pivoted-Cholesky rank among columns with |I(l)| > 64 */
     size_t workspace_bytes;    /* device bytes currently owned by the plan */

@@ -749,7 +749,7 @@ inft_status inft_get_info(inft_plan_t plan, inft_info* info) {
     info->max_col_size = p->max_col_size;
     info->max_abs_w = p->max_abs_w;
     info->perm_identity = p->perm_identity ? 1 : 0;
-    info->fast_path = p->fast1d ? 1 : 0;
+    info->fast_path = p->fast1d ? (inft::ring_available(*p) ? 2 : 1) : 0;
     info->fused_fft = (inft::fused_fft_available(*p) && !p->no_fused_fft) ? 1 : 0;
     info->max_lowrank_rank = (int32_t)p->max_lowrank_rank;
     info->workspace_bytes = p->workspace_bytes();

@@ -325,7 +325,7 @@ def test_complex_weights_generic_equals_oracle_and_fast_path(P, torch):
     # generic (complex with zero imaginary part) vs fast (real) kernels
     pr = P.Plan(x, M, sigma, m).set_bopt(w, "alg2")
     pz = P.Plan(x, M, sigma, m).set_bopt(w + 0j, "alg2")
-    assert pr.info()["fast_path"] == 1
+    assert pr.info()["fast_path"] >= 1
     a = pr.apply(_dev(torch, f)).cpu().numpy()
     b = pz.apply(_dev(torch, f)).cpu().numpy()
     assert O.rel_l2(a, b) < 1e-14
