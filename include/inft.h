@@ -188,6 +188,42 @@ inft_status inft_get_profile(inft_plan_t plan, inft_profile* out, int reset);
  * benchmarks; cuFFT's internal kernels are not counted). */
 int64_t inft_kernel_launches(inft_plan_t plan);
 
+/* ---------------------------------------------------------------------------
+ * Quadratic case M = N (paper Section "The quadratic case",
+ * P:344-489, adjoint Remark P:576-584).  For N distinct nodes y_j and the
+ * equispaced targets x_l = -1/2 + l/N + delta (delta in (0, 1/N),
+ * 0 selects 1/(2N), reading A23), the inverse NFFT A fhat = f with
+ * A = (e^{2 pi i k y_j})_{j, k=-N/2..N/2-1} is solved by the Lagrange relation
+ *   g_l = a_l sum_j f_j b_j (cot(pi (x_l - y_j)) - i)        (eq. lagrange_formula)
+ *   fcheck_k = (1/N) sum_l g_l e^{-2 pi i k x_l}              (Alg. step 6, one FFT)
+ * a_l = prod_n sin(pi (x_l - y_n)), b_j = prod_{n != j} 1/sin(pi (y_j - y_n))
+ * (eq. coeff_ab) in the log domain with counted signs and the
+ * balancing shift s = (max ln|b| - max ln|a|)/2 (Remark P:431-449, reading A22).
+ * The sums are evaluated directly on the GPU (O(N^2), exact; the paper's fast
+ * summation P:386-428 is not used).  Complex128 only; RHS-major [R][N] data,
+ * host or device pointers (host data staged synchronously).
+ * ------------------------------------------------------------------------- */
+typedef struct inft_quad_s* inft_quad_t; /* opaque quadratic-case plan */
+
+/* Build: copies the nodes (host or device, N doubles in [-1/2, 1/2)), computes
+ * x, a, b, s on `device`.  N even, >= 2.  Synchronous.  Errors:
+ * INFT_ERR_INVALID_ARG (N odd / < 2, delta outside (0, 1/N)), INFT_ERR_NODE_RANGE
+ * (a node outside [-1/2, 1/2), or coincident nodes: y_j = y_n or y_j = x_l). */
+inft_status inft_quad_plan(inft_quad_t* out, int64_t N, const double* nodes, double delta, int device,
+                           inft_stream_t stream);
+/* Inverse NFFT, quadratic case: f [R][N] (samples at the nodes, caller order)
+ * -> fhat [R][N], centered index c = k + N/2.  Stream-ordered (device data). */
+inft_status inft_quad_apply(inft_quad_t plan, const void* f, void* fhat, int64_t R, inft_stream_t stream);
+/* Inverse adjoint NFFT, quadratic case (eq. lagrange_formula_adjoint):
+ * h [R][N] centered -> f [R][N] with f = (A^*)^{-1} h, v = (1/N) sum_k h_k e^{2 pi i k x_l}. */
+inft_status inft_quad_adjoint_apply(inft_quad_t plan, const void* h, void* f, int64_t R, inft_stream_t stream);
+/* Host copies of the targets x [N], signed stabilised a [N], b [N] and the shift s
+ * (any pointer may be NULL).  Synchronous. */
+inft_status inft_quad_get_coeffs(inft_quad_t plan, double* x, double* a, double* b, double* s);
+/* Kernel launches issued by this plan (cuFFT's not counted). */
+inft_status inft_quad_kernel_launches(inft_quad_t plan, int64_t* count);
+inft_status inft_quad_destroy(inft_quad_t plan);
+
 const char* inft_status_string(inft_status status);
 /* Thread-local text of the last error (CUDA / cuFFT message), "" if none. */
 const char* inft_last_error(void);

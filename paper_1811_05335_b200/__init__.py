@@ -69,6 +69,12 @@ EXPORTS = {
     "inft_set_profiling": ([_P, _I], _I),
     "inft_get_profile": ([_P, ctypes.POINTER(InftProfile), _I], _I),
     "inft_kernel_launches": ([_P], _I64),
+    "inft_quad_plan": ([ctypes.POINTER(_P), _I64, _P, ctypes.c_double, _I, _P], _I),
+    "inft_quad_apply": ([_P, _P, _P, _I64, _P], _I),
+    "inft_quad_adjoint_apply": ([_P, _P, _P, _I64, _P], _I),
+    "inft_quad_get_coeffs": ([_P, _P, _P, _P, _P], _I),
+    "inft_quad_kernel_launches": ([_P, ctypes.POINTER(_I64)], _I),
+    "inft_quad_destroy": ([_P], _I),
     "inft_status_string": ([_I], ctypes.c_char_p),
     "inft_last_error": ([], ctypes.c_char_p),
 }
@@ -253,4 +259,71 @@ class Plan:
         return out
 
 
-__all__ = ["Plan", "InftError", "LIB_PATH", "EXPORTS", "STAGES"] + list(EXPORTS)
+class QuadPlan:
+    """Quadratic case M = N (inft_quad_*; P:344-489, P:576-584): nodes [N] float64 in
+    [-1/2, 1/2), N even; targets x_l = -1/2 + l/N + delta (delta = 0: 1/(2N)).  Complex128."""
+
+    def __init__(self, nodes, delta=0.0, device=0, stream=None):
+        if hasattr(nodes, "data_ptr"):
+            nd = nodes.contiguous()
+            self._nodes_ref = nd
+            N, nptr = nd.shape[0], nd.data_ptr()
+        else:
+            nd = np.ascontiguousarray(np.asarray(nodes, dtype=np.float64))
+            N, nptr = nd.shape[0], nd.ctypes.data
+        self.N = int(N)
+        self.device = int(device)
+        h = ctypes.c_void_p()
+        _check(inft_quad_plan(ctypes.byref(h), self.N, nptr, float(delta), self.device, _stream_ptr(stream)),
+               "inft_quad_plan")
+        self._h = h
+
+    def close(self):
+        if getattr(self, "_h", None):
+            inft_quad_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def coeffs(self):
+        """(x, a, b, s): targets, signed stabilised a_l and b_j, shift s (host copies)."""
+        x, a, b = (np.empty(self.N) for _ in range(3))
+        s = ctypes.c_double()
+        _check(inft_quad_get_coeffs(self._h, x.ctypes.data, a.ctypes.data, b.ctypes.data, ctypes.byref(s)),
+               "inft_quad_get_coeffs")
+        return x, a, b, s.value
+
+    def kernel_launches(self):
+        c = ctypes.c_int64()
+        _check(inft_quad_kernel_launches(self._h, ctypes.byref(c)), "inft_quad_kernel_launches")
+        return int(c.value)
+
+    def _out(self, like, shape):
+        if hasattr(like, "device"):
+            import torch
+            return torch.empty(shape, dtype=torch.complex128, device=like.device)
+        return np.empty(shape, dtype=np.complex128)
+
+    def apply(self, f, out=None, stream=None):
+        """Inverse NFFT, quadratic case: f [R][N] -> fhat [R][N] (k = -N/2..N/2-1)."""
+        R = f.shape[0] if f.ndim == 2 else 1
+        if out is None:
+            out = self._out(f, (R, self.N))
+        _check(inft_quad_apply(self._h, _ptr(f), _ptr(out), R, _stream_ptr(stream)), "inft_quad_apply")
+        return out
+
+    def adjoint_apply(self, h, out=None, stream=None):
+        """Inverse adjoint NFFT, quadratic case: h [R][N] -> f [R][N]."""
+        R = h.shape[0] if h.ndim == 2 else 1
+        if out is None:
+            out = self._out(h, (R, self.N))
+        _check(inft_quad_adjoint_apply(self._h, _ptr(h), _ptr(out), R, _stream_ptr(stream)),
+               "inft_quad_adjoint_apply")
+        return out
+
+
+__all__ = ["Plan", "QuadPlan", "InftError", "LIB_PATH", "EXPORTS", "STAGES"] + list(EXPORTS)
