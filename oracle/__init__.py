@@ -100,10 +100,38 @@ def msigma(M, sigma):
     return iv
 
 
-def window_hat_vector(M, sigma, m):
-    """what(k) for k = -M/2..M/2-1 (centered)."""
+def bspline_centred(v, n):
+    """Centred cardinal B-spline M_n (support [-n/2, n/2], integral 1) by the recursion
+    M_1 = chi_[-1/2, 1/2),  M_n(v) = ((n/2 + v) M_{n-1}(v + 1/2) + (n/2 - v) M_{n-1}(v - 1/2)) / (n - 1)."""
+    v = np.asarray(v, dtype=np.float64)
+    # level k holds M_k at the offsets v + j - (n - k)/2, j = 0..n-k (the ones M_n(v) needs)
+    off = [v + (j - 0.5 * (n - 1)) for j in range(n)]
+    cur = [((o >= -0.5) & (o < 0.5)).astype(np.float64) for o in off]
+    for k in range(2, n + 1):
+        off = [v + (j - 0.5 * (n - k)) for j in range(n - k + 1)]
+        cur = [((0.5 * k + off[j]) * cur[j + 1] + (0.5 * k - off[j]) * cur[j]) / (k - 1) for j in range(n - k + 1)]
+    return cur[0]
+
+
+def bspline_w(x, Msig, m):
+    """B-spline window of the paper's experiments (reading A24):
+    w(x) = M_2m(M_sigma x), support [-m/M_sigma, m/M_sigma] (no truncation)."""
+    return bspline_centred(Msig * np.asarray(x, dtype=np.float64), 2 * m)
+
+
+def bspline_what(k, Msig, m):
+    """what(k) = int w(x) e^{-2 pi i k x} dx = (1/M_sigma) sinc(pi k/M_sigma)^{2m} (the B-spline's
+    Fourier transform; pinned by quadrature in tests/test_oracle_bspline.py)."""
+    k = np.asarray(k, dtype=np.float64)
+    return np.sinc(k / Msig) ** (2 * m) / Msig
+
+
+def window_hat_vector(M, sigma, m, window="kb"):
+    """what(k) for k = -M/2..M/2-1 (centered): Kaiser-Bessel (A7) or B-spline (A24)."""
     Ms = msigma(M, sigma)
     k = np.arange(-M // 2, M // 2)
+    if window == "bspline":
+        return bspline_what(k, Ms, m)
     return kb_what(k, Ms, m, sigma)
 
 
@@ -114,8 +142,8 @@ def inv_what_vector(M, sigma, m, window="kb"):
     what(k) = 1 for k = -M/2+1..M/2-1 and the entry of D^* at the unpaired frequency set to
     zero (the text names it 1/what(M/2); in the centred range -M/2..M/2-1 it is k = -M/2,
     reading A21)."""
-    if window == "kb":
-        return 1.0 / window_hat_vector(M, sigma, m)
+    if window in ("kb", "bspline"):
+        return 1.0 / window_hat_vector(M, sigma, m, window)
     if window == "dirichlet":
         v = np.ones(M)
         v[0] = 0.0
@@ -137,8 +165,8 @@ def deconv_vector(M, sigma, m, s=1.0, window="kb"):
     """d_k = s / (M_sigma what(k)) -- the diagonal of D (eq. matrix_D)
     with the apply scale s folded in (reading A2)."""
     Ms = msigma(M, sigma)
-    if window == "kb":
-        return s / (Ms * window_hat_vector(M, sigma, m))
+    if window in ("kb", "bspline"):
+        return s / (Ms * window_hat_vector(M, sigma, m, window))
     return s * inv_what_vector(M, sigma, m, window) / Ms
 
 
@@ -234,21 +262,28 @@ def matrix_F(M, Msig):
     return np.exp(2j * np.pi * np.outer(l, k) / Msig)
 
 
-def matrix_B_window(x, M, sigma, m):
+def _w_periodic(x, Ms, m, sigma, window):
+    if window == "bspline":
+        x = np.asarray(x, dtype=np.float64)
+        return bspline_w(x - 1.0, Ms, m) + bspline_w(x, Ms, m) + bspline_w(x + 1.0, Ms, m)
+    return kb_w_periodic(x, Ms, m, sigma)
+
+
+def matrix_B_window(x, M, sigma, m, window="kb"):
     """Window matrix B = (w~_m(x_j - l/M_sigma))_{j, l} (eq. matrix_B)."""
     Ms = msigma(M, sigma)
     l = np.arange(-Ms // 2, Ms // 2)
-    return kb_w_periodic(np.asarray(x)[:, None] - l[None, :] / Ms, Ms, m, sigma)
+    return _w_periodic(np.asarray(x)[:, None] - l[None, :] / Ms, Ms, m, sigma, window)
 
 
-def window_slot_weights(x, M, sigma, m):
+def window_slot_weights(x, M, sigma, m, window="kb"):
     """Slot weights of the window matrix B: w[j][t] = w~_m(x_j - (l0_j+t)/M_sigma)
     on live slots (ordinary NFFT, the INFT_PLAIN_NFFT method)."""
     Ms = msigma(M, sigma)
     x = np.asarray(x, dtype=np.float64)
     l0 = node_base(x, Ms, m)
     t = np.arange(2 * m + 1)
-    w = kb_w_periodic(x[:, None] - (l0[:, None] + t[None, :]) / Ms, Ms, m, sigma)
+    w = _w_periodic(x[:, None] - (l0[:, None] + t[None, :]) / Ms, Ms, m, sigma, window)
     return np.where(slot_live(x, Ms, m), w, 0.0)
 
 
