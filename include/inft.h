@@ -62,11 +62,14 @@ typedef enum {
 
 typedef enum {
     INFT_KAISER_BESSEL = 0, /* reading A7: what(k) = I0(m sqrt(b^2-(2 pi k/M_sigma)^2))/M_sigma, b = pi(2-1/sigma) */
-    INFT_DIRICHLET = 1      /* Dirichlet-kernel variant, Remarks P:934-957 / P:1343-1358 (reading A21):
+    INFT_DIRICHLET = 1,     /* Dirichlet-kernel variant, Remarks P:934-957 / P:1343-1358 (reading A21):
                              * what(k) = 1 for |k| < M/2, the k = -M/2 entry of D zeroed, so
                              * d_k = s/M_sigma (k != -M/2); only with the optimised B_opt
                              * (ALG1/ALG2 or inft_set_bopt): there is no window function in space,
                              * INFT_PLAIN_NFFT returns INFT_ERR_INVALID_ARG */
+    INFT_BSPLINE = 2        /* B-spline window of the paper's experiments (reading A24):
+                             * w(x) = M_2m(M_sigma x), the centred cardinal B-spline of order 2m
+                             * (support [-m, m]/M_sigma, exact), what(k) = sinc(pi k/M_sigma)^2m / M_sigma */
 } inft_window;
 
 typedef enum {

@@ -28,7 +28,7 @@ INFT_OK = 0
 STATUS = {0: "INFT_OK", 1: "INFT_ERR_INVALID_ARG", 2: "INFT_ERR_NODE_RANGE", 3: "INFT_ERR_ZERO_WINDOW_HAT",
           4: "INFT_ERR_NOT_PRECOMPUTED", 5: "INFT_ERR_CUDA", 6: "INFT_ERR_CUFFT", 7: "INFT_ERR_OOM",
           8: "INFT_ERR_UNSUPPORTED"}
-INFT_KAISER_BESSEL, INFT_DIRICHLET = 0, 1
+INFT_KAISER_BESSEL, INFT_DIRICHLET, INFT_BSPLINE = 0, 1, 2
 INFT_AUTO, INFT_ALG1_NODEWISE, INFT_ALG2_GRIDWISE, INFT_PLAIN_NFFT = 0, 1, 2, 3
 INFT_C128, INFT_C64 = 0, 1
 INFT_WEIGHTS_REAL, INFT_WEIGHTS_COMPLEX = 0, 1
@@ -148,7 +148,7 @@ class Plan:
         self.prec = INFT_C128 if precision in ("c128", INFT_C128) else INFT_C64
         Marr = (ctypes.c_int64 * self.d)(*self.M)
         h = ctypes.c_void_p()
-        win = {"kb": INFT_KAISER_BESSEL, "dirichlet": INFT_DIRICHLET}[window] if isinstance(window, str) \
+        win = {"kb": INFT_KAISER_BESSEL, "dirichlet": INFT_DIRICHLET, "bspline": INFT_BSPLINE}[window] if isinstance(window, str) \
             else int(window)
         _check(inft_plan(ctypes.byref(h), self.d, Marr, self.N, nptr, float(sigma), int(m), win,
                          self.prec, int(device), _stream_ptr(stream)), "inft_plan")

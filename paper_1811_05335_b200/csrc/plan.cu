@@ -219,11 +219,20 @@ __global__ void k_sorted_ints(const int32_t* __restrict__ perm, const int32_t* _
 
 // d_k = s / (M_sigma what(k)) = s / I0(m sqrt(b^2 - (2 pi k/M_sigma)^2)), k = -M/2..M/2-1.
 __global__ void k_deconv(double* __restrict__ dk, int64_t M, int64_t Ms, int m, double sigma, double s,
-                         int dirichlet, int* __restrict__ bad) {
+                         int window, int* __restrict__ bad) {
     int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (c >= M) return;
-    if (dirichlet) {  // what = 1, the unpaired k = -M/2 (c = 0) zeroed (reading A21)
+    if (window == INFT_DIRICHLET) {  // what = 1, the unpaired k = -M/2 (c = 0) zeroed (reading A21)
         dk[c] = c == 0 ? 0.0 : s / (double)Ms;
+        return;
+    }
+    if (window == INFT_BSPLINE) {  // M_sigma what(k) = sinc(pi k/M_sigma)^{2m} (reading A24)
+        const int64_t k = c - M / 2;
+        const double t = (double)k / (double)Ms;  // |t| <= 1/(2 sigma) <= 1/2
+        const double sc = k == 0 ? 1.0 : sinpi(t) / (3.141592653589793238462643383279502884 * t);
+        const double v = pow(sc, 2.0 * m);
+        if (!(v > 0.0)) atomicOr(bad, 1);
+        dk[c] = s / v;
         return;
     }
     double k = (double)(c - M / 2);
@@ -434,7 +443,7 @@ void compute_deconv(Plan& p, double s, cudaStream_t st) {
     for (int i = 0; i < p.d; i++) {
         double* dst = p.dk.as<double>() + (i == 0 ? 0 : p.M[0]);
         k_deconv<<<grid1d(p.M[i]), 256, 0, st>>>(dst, p.M[i], p.Ms[i], p.m, p.sigma, i == 0 ? s : 1.0,
-                                                 p.window == INFT_DIRICHLET ? 1 : 0, flag.as<int>());
+                                                 (int)p.window, flag.as<int>());
         INFT_CHECK_LAUNCH();
         p.launches++;
     }
@@ -574,8 +583,9 @@ inft_status inft_plan(inft_plan_t* out, int d, const int64_t* M, int64_t N, cons
     if (!out) return INFT_ERR_INVALID_ARG;
     *out = nullptr;
     if (d < 1 || d > 2 || !M || N < 0 || (N > 0 && !nodes) ||
-        (window != INFT_KAISER_BESSEL && window != INFT_DIRICHLET) ||
-        (prec != INFT_C128 && prec != INFT_C64) || !(sigma >= 1.0) || m < 1 || N > INT32_MAX) {
+        (window != INFT_KAISER_BESSEL && window != INFT_DIRICHLET && window != INFT_BSPLINE) ||
+        (prec != INFT_C128 && prec != INFT_C64) || !(sigma >= 1.0) || m < 1 || N > INT32_MAX ||
+        (window == INFT_BSPLINE && m > 16)) {  // B-spline evaluation buffer: order 2m <= 32
         inft::set_error("inft_plan: invalid argument");
         return INFT_ERR_INVALID_ARG;
     }

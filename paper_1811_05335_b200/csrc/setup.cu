@@ -113,11 +113,17 @@ __global__ void k_col_count(ColCtx c, int64_t ncol, int32_t* __restrict__ cnt) {
 
 // ------------------------------------------------------------------ kernel tables
 // 1/(M_sigma what(k)) = 1/I0(m sqrt(b^2 - (2 pi k/Ms)^2)) for k = 0..M/2 (even window).
-__global__ void k_inv_what(double* __restrict__ iw, int64_t M, int64_t Ms, int m, double sigma, int dirichlet) {
+__global__ void k_inv_what(double* __restrict__ iw, int64_t M, int64_t Ms, int m, double sigma, int window) {
     int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (k > M / 2) return;
-    if (dirichlet) {  // what = 1; the unpaired frequency (stored at k = M/2) zeroed (reading A21)
+    if (window == INFT_DIRICHLET) {  // what = 1; the unpaired frequency (stored at k = M/2) zeroed (reading A21)
         iw[k] = k == M / 2 ? 0.0 : 1.0 / (double)Ms;
+        return;
+    }
+    if (window == INFT_BSPLINE) {  // 1/(M_sigma what(k)) = sinc(pi k/M_sigma)^{-2m} (reading A24)
+        const double t = (double)k / (double)Ms;
+        const double sc = k == 0 ? 1.0 : sinpi(t) / (kPi * t);
+        iw[k] = 1.0 / pow(sc, 2.0 * m);
         return;
     }
     double b = kPi * (2.0 - 1.0 / sigma);
@@ -1056,8 +1062,21 @@ __global__ void k_alg1_solve_gam(const double2* __restrict__ gam, KTab tab, cons
 
 // ------------------------------------------------------------------ plain window B
 // w[i][t] = w~_m(x - l/Ms) = sum_z w_m(x - l/Ms + z) on live slots (eq. matrix_B, A7).
+// centred cardinal B-spline of order n (support [-n/2, n/2]) at v: N_n(v + n/2) by the
+// recursion N_k(u) = (u N_{k-1}(u) + (k - u) N_{k-1}(u - 1)) / (k - 1), N_1 = chi_[0, 1)
+__device__ double bspline_centred(double v, int n) {
+    const double u = v + 0.5 * n;
+    if (!(u >= 0.0 && u < (double)n)) return 0.0;
+    double c[33];  // c[j] = N_k(u - j), j = 0..n
+    for (int j = 0; j <= n; ++j) c[j] = (u - j >= 0.0 && u - j < 1.0) ? 1.0 : 0.0;
+    for (int k = 2; k <= n; ++k)
+        for (int j = 0; j < n; ++j) c[j] = ((u - j) * c[j] + (k - (u - j)) * c[j + 1]) / (k - 1);
+    return c[0];
+}
+
 __global__ void k_window_weights(const double* __restrict__ xs, const int32_t* __restrict__ l0s, int64_t N, int d,
-                                 int64_t Ms1, int64_t Ms2, int m, double sigma, int P1, double* __restrict__ w64) {
+                                 int64_t Ms1, int64_t Ms2, int m, double sigma, int P1, int window,
+                                 double* __restrict__ w64) {
     const int P = d == 2 ? P1 * P1 : P1;
     int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (idx >= N * P) return;
@@ -1082,8 +1101,12 @@ __global__ void k_window_weights(const double* __restrict__ xs, const int32_t* _
         for (int z = -1; z <= 1; z++) {
             double vz = v + (double)z * (double)Ms;
             if (fabs(vz) <= (double)m) {
-                double r2 = (double)m * m - vz * vz;
-                acc += (r2 > 0.0 ? sinh(b * sqrt(r2)) / sqrt(r2) : b) / kPi;
+                if (window == INFT_BSPLINE) {
+                    acc += bspline_centred(vz, 2 * m);  // w(x) = M_2m(M_sigma x)
+                } else {
+                    double r2 = (double)m * m - vz * vz;
+                    acc += (r2 > 0.0 ? sinh(b * sqrt(r2)) / sqrt(r2) : b) / kPi;
+                }
             }
         }
         val *= acc;
@@ -1101,7 +1124,7 @@ static void build_tables(Plan& p, int dim, Tables& T, double X, cudaStream_t st)
     const int64_t M = p.M[dim], Ms = p.Ms[dim];
     T.iw.alloc(sizeof(double) * (M / 2 + 1));
     k_inv_what<<<nblk(M / 2 + 1), 256, 0, st>>>(T.iw.as<double>(), M, Ms, p.m, p.sigma,
-                                                 p.window == INFT_DIRICHLET ? 1 : 0);
+                                                 (int)p.window);
     INFT_CHECK_LAUNCH();
     p.launches++;
     // piece width 2h with (pi M) h <= 1: |phase change| <= 1 rad per half piece
@@ -1394,7 +1417,7 @@ static void alg1(Plan& p, double tau, DevBuf& w64, cudaStream_t st) {
                                             xs.as<double>(), l0s.as<int32_t>());
     iw.alloc(sizeof(double) * (M / 2 + 1));
     k_inv_what<<<nblk(M / 2 + 1), 256, 0, st>>>(iw.as<double>(), M, Ms, p.m, p.sigma,
-                                                 p.window == INFT_DIRICHLET ? 1 : 0);
+                                                 (int)p.window);
     DevBuf ndrop;
     ndrop.alloc(sizeof(unsigned long long));
     INFT_CUDA(cudaMemsetAsync(ndrop.p, 0, sizeof(unsigned long long), st));
@@ -1428,8 +1451,8 @@ void precompute(Plan& p, inft_method method, inft_weights wt, double tau, cudaSt
     p.n_rank_deficient = p.n_empty_cols = p.max_col_size = 0;
     p.tau = tau;
     if (method == INFT_PLAIN_NFFT) {
-        if (p.window != INFT_KAISER_BESSEL) {
-            set_error("INFT_PLAIN_NFFT needs a window function in space (Kaiser-Bessel)");
+        if (p.window == INFT_DIRICHLET) {
+            set_error("INFT_PLAIN_NFFT needs a window function in space (Kaiser-Bessel or B-spline)");
             throw Fail{INFT_ERR_INVALID_ARG};
         }
         if (p.N > 0) {
@@ -1440,7 +1463,7 @@ void precompute(Plan& p, inft_method method, inft_weights wt, double tau, cudaSt
                                                       p.N, p.d, xs.as<double>(), l0s.as<int32_t>());
             k_window_weights<<<nblk(p.N * p.P), 256, 0, st>>>(xs.as<double>(), l0s.as<int32_t>(), p.N, p.d, p.Ms[0],
                                                               p.d == 2 ? p.Ms[1] : 1, p.m, p.sigma, p.P1,
-                                                              w64.as<double>());
+                                                              (int)p.window, w64.as<double>());
             INFT_CHECK_LAUNCH();
             p.launches += 2;
             INFT_CUDA(cudaStreamSynchronize(st));
