@@ -202,9 +202,10 @@ int64_t inft_kernel_launches(inft_plan_t plan);
  * a_l = prod_n sin(pi (x_l - y_n)), b_j = prod_{n != j} 1/sin(pi (y_j - y_n))
  * (eq. coeff_ab) in the log domain with counted signs and the
  * balancing shift s = (max ln|b| - max ln|a|)/2 (Remark P:431-449, reading A22).
- * The sums are evaluated directly on the GPU (O(N^2), exact; the paper's fast
- * summation P:386-428 is not used).  Complex128 only; RHS-major [R][N] data,
- * host or device pointers (host data staged synchronously).
+ * The sums run by the paper's NFFT-based fast summation (O(N log N),
+ * error ~1e-15 N relative) for N >= 512, by exact direct O(N^2) GPU sums below
+ * that or with INFT_QUAD_DIRECT=1 set at plan time.  Complex128 only; RHS-major
+ * [R][N] data, host or device pointers (host data staged synchronously).
  * ------------------------------------------------------------------------- */
 typedef struct inft_quad_s* inft_quad_t; /* opaque quadratic-case plan */
 

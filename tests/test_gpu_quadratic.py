@@ -96,3 +96,26 @@ def test_quadratic_errors(P):
         P.QuadPlan(np.sort(y))
     with pytest.raises(P.InftError):
         P.QuadPlan(np.array([0.1, 0.1, 0.2, 0.3]))  # repeated node
+
+
+@pytest.mark.parametrize("N,kind", [(512, "jittered"), (4096, "jittered"), (1500, "iid"), (1 << 15, "jittered")])
+def test_fast_summation_equals_direct(P, torch, N, kind):
+    """The fast summation (default for N >= 512) against the direct GPU sums (INFT_QUAD_DIRECT=1)
+    on the same nodes: coefficients a, b and both applies."""
+    import os
+    y = _nodes(kind, N, 7)
+    qf = P.QuadPlan(y)
+    os.environ["INFT_QUAD_DIRECT"] = "1"
+    try:
+        qd = P.QuadPlan(y)
+    finally:
+        del os.environ["INFT_QUAD_DIRECT"]
+    _, af, bf, _ = qf.coeffs()
+    _, ad, bd, _ = qd.coeffs()
+    assert np.abs(af / ad - 1).max() < 1e-9 and np.abs(bf / bd - 1).max() < 1e-9
+    R = 3
+    f = torch.from_numpy(S.normal_complex(R, N, 8)).cuda()
+    h = torch.from_numpy(S.normal_complex(R, N, 9)).cuda()
+    tol = 1e-9 if kind == "jittered" else 1e-7
+    assert O.rel_l2(qf.apply(f).cpu().numpy(), qd.apply(f).cpu().numpy()) < tol
+    assert O.rel_l2(qf.adjoint_apply(h).cpu().numpy(), qd.adjoint_apply(h).cpu().numpy()) < tol
