@@ -1010,10 +1010,32 @@ static void run(Plan& p, const void* in, size_t in_rhs_bytes, void* out, size_t 
     INFT_CUDA(cudaEventRecord(p.ev_entry, st));
     INFT_CUDA(cudaStreamWaitEvent(p.s_h2d, p.ev_entry, 0));
     INFT_CUDA(cudaStreamWaitEvent(p.s_d2h, p.ev_entry, 0));
-    const int64_t nchunk = ceil_div(R, Rh);
+    // chunk schedule: a quarter-size first and last chunk shorten the pipeline fill (first
+    // H2D alone) and drain (last D2H alone); full chunks in between (INFT_STAGE_RAMP=0: uniform)
+    static const bool ramp = [] {
+        const char* e = getenv("INFT_STAGE_RAMP");
+        return !(e && atoi(e) == 0);
+    }();
+    std::vector<int64_t> starts;
+    {
+        const int64_t q = std::max<int64_t>(1, Rh / 4);
+        if (ramp && R >= 2 * q + Rh) {
+            starts.push_back(0);
+            int64_t r = q;
+            while (R - q - r > 0) {
+                starts.push_back(r);
+                r += std::min(Rh, R - q - r);
+            }
+            starts.push_back(R - q);
+        } else {
+            for (int64_t r = 0; r < R; r += Rh) starts.push_back(r);
+        }
+        starts.push_back(R);
+    }
+    const int64_t nchunk = (int64_t)starts.size() - 1;
     for (int64_t c = 0; c < nchunk; c++) {
         const int b = (int)(c & 1);
-        const int64_t r0 = c * Rh, rc = std::min(Rh, R - r0);
+        const int64_t r0 = starts[c], rc = starts[c + 1] - starts[c];
         const void* src = in_dev ? (const void*)(ib + r0 * in_rhs_bytes) : p.stage_in[b].p;
         void* dst = out_dev ? (void*)(ob + r0 * out_rhs_bytes) : p.stage_out[b].p;
         if (!in_dev) {
