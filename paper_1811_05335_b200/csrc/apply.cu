@@ -214,21 +214,28 @@ __device__ __forceinline__ void row_dispatch(int c, T (&ax)[16], T (&ay)[16], co
 // weights (one contiguous run of kB2 * PP values) by one 1-D bulk copy, its f values (kB2 x 32
 // RHS) and slot bases by per-thread cp.async, all issued one batch ahead so that the warps
 // only ever read shared memory in the node loop.
-constexpr int kB2 = 48;
+// nodes per batch and CTAs per SM: complex128 24 nodes, 2 CTAs/SM (config 4 spread 1.44 ->
+// 1.34 ms against 48 nodes, 1 CTA/SM); complex64 48 nodes, 1 CTA/SM (0.93 vs 1.05 ms)
+template <typename T>
+constexpr int kB2T = sizeof(T) == 8 ? 24 : 48;
+template <typename T>
+constexpr int kMinB2d = sizeof(T) == 8 ? 2 : 1;
 
 template <typename T>
 __host__ __device__ constexpr size_t tile2d_stage_bytes(int PP) {
+    constexpr int kB2 = kB2T<T>;
     return ((sizeof(C2<T>) * kB2 * 32 + sizeof(int2) * kB2 + sizeof(T) * (size_t)kB2 * PP) + 127) / 128 * 128;
 }
 
 template <typename T, int MC>
-__global__ void __launch_bounds__(256) k_spread_2d_tile(const int4* __restrict__ work,
+__global__ void __launch_bounds__(256, kMinB2d<T>) k_spread_2d_tile(const int4* __restrict__ work,
                                                         const int32_t* __restrict__ seg_start,
                                                         const int32_t* __restrict__ n0s, const T* __restrict__ w,
                                                         int PP, const C2<T>* __restrict__ fT, C2<T>* __restrict__ grid,
                                                         C2<T>* __restrict__ part, int Ms1, int Ms2, int nseg1,
                                                         int nseg2, int R, int64_t GS) {
     constexpr int P1 = 2 * MC + 1;
+    constexpr int kB2 = kB2T<T>;
     extern __shared__ __align__(128) unsigned char sm2[];
     __shared__ uint64_t full[2];
     __shared__ int tlo[4], thi[4], tnb[5];  // candidate tile ranges, batch prefix counts
@@ -396,6 +403,7 @@ static void ensure_spread2d_work(Plan& p, cudaStream_t st) {
     INFT_CUDA(cudaMemcpyAsync(ss.data(), p.seg_start.p, sizeof(int32_t) * ss.size(), cudaMemcpyDeviceToHost, st));
     INFT_CUDA(cudaStreamSynchronize(st));
     const int n1 = (int)p.nseg[0], n2 = (int)p.nseg[1];
+    const int kB2 = p.prec == INFT_C128 ? kB2T<double> : kB2T<float>;
     std::vector<int4> work, comb;
     int slots = 0;
     for (int t = 0; t < n1 * n2; ++t) {
