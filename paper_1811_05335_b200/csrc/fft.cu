@@ -202,13 +202,22 @@ constexpr int kRB = INFT_FFT_RADIX;
 #define INFT_FFT_TILE 4096
 #endif
 constexpr int kTileElems = INFT_FFT_TILE;
+// complex64 tiles (elements): 8192 = 64 KB like a complex128 tile, 512 threads at <= 128
+// registers (config 5 c64: 4096 -> 3.55 ms/step, 8192 -> 3.06)
+#ifndef INFT_FFT_TILE_F
+#define INFT_FFT_TILE_F 8192
+#endif
+constexpr int kTileElemsF = INFT_FFT_TILE_F;
+template <typename T>
+constexpr int tile_elems() { return sizeof(T) == 8 ? kTileElems : kTileElemsF; }
 constexpr int kLgRB = kRB == 16 ? 4 : (kRB == 8 ? 3 : 2);
 // TF independent length-L transforms per tile (compile-time: ~64 KB of shared memory, at
 // most 256 threads = TF L / 16, at most 8), thread t -> (f = t % TF, butterfly j = t / TF).
 // Static radix plan for L = 2^K: a first stage of radix 2^(K mod 4) (if any), then radix-16.
 template <typename T, int L>
 struct Geo {
-    static constexpr int TF = L >= kTileElems / 8 ? (kTileElems / L > 0 ? kTileElems / L : 1) : 8;
+    static constexpr int TE = tile_elems<T>();
+    static constexpr int TF = L >= TE / 8 ? (TE / L > 0 ? TE / L : 1) : 8;
     static constexpr int NT = TF * L / kRB < 32 ? 32 : TF * L / kRB;  // threads per CTA
     // row padding of the [f][L + PAD] layout: the lanes of one 128-byte shared wavefront cover
     // TF transforms x (wavefront / TF) consecutive positions
@@ -422,7 +431,10 @@ template <typename T, int SIGN, int MODE, int L>
 __global__ void __launch_bounds__(Geo<T, L>::NT, 1)
     k_pass_b(const __grid_constant__ CUtensorMap dmap, const __grid_constant__ CUtensorMap omap, Args<T> A, int BRd,
              int BRo, int ntiles) {
-    constexpr bool kStageB = sizeof(T) == 8;  // see the store lambda
+#ifndef INFT_STAGE_B_F
+#define INFT_STAGE_B_F 0
+#endif
+    constexpr bool kStageB = sizeof(T) == 8 || INFT_STAGE_B_F;  // see the store lambda
     extern __shared__ __align__(128) unsigned char smraw[];
     using G = Geo<T, L>;
     constexpr int TB = G::TF, S = G::ST, SW = G::SW;
@@ -602,7 +614,8 @@ bool fused_fft_available(const Plan& p) {
     // pass A of the adjoint stages d (2B rows x >= 16 bytes) in the tile's unused middle rows
     {
         const int N1 = split_n1(N);
-        const int TF = N1 >= fft::kTileElems / 8 ? std::max(1, fft::kTileElems / N1) : 8;
+        const int TE = p.prec == INFT_C128 ? fft::tile_elems<double>() : fft::tile_elems<float>();
+        const int TF = N1 >= TE / 8 ? std::max(1, TE / N1) : 8;
         const size_t cs = p.prec == INFT_C128 ? 16 : 8, ds = cs / 2;
         const size_t dw = std::max<size_t>((size_t)TF, 16 / ds);
         if ((size_t)(N1 - 2 * B) * TF * cs < (size_t)2 * B * dw * ds) return false;
@@ -613,7 +626,8 @@ bool fused_fft_available(const Plan& p) {
     {
         const int64_t B2 = half / split_n1(N);
         const size_t ds = p.prec == INFT_C128 ? 8 : 4;
-        const int TF = N2 >= fft::kTileElems / 8 ? std::max(1, (int)(fft::kTileElems / N2)) : 8;
+        const int TE = p.prec == INFT_C128 ? fft::tile_elems<double>() : fft::tile_elems<float>();
+        const int TF = N2 >= TE / 8 ? std::max(1, (int)(TE / N2)) : 8;
         const size_t dw = std::max<size_t>((size_t)TF, 16 / ds);
         const size_t smem = p.prec == INFT_C128 ? pass_b_smem<double>((int)N2, split_n1(N), p.M[0], 0)
                                                 : pass_b_smem<float>((int)N2, split_n1(N), p.M[0], 0);
