@@ -893,11 +893,186 @@ struct StageTimer {
     }
 };
 
+// ====================================================================== small 1-D problems
+// Configs 1-2 are launch-latency bound: for tiny batches (R M_sigma <= 8192, a
+// power-of-two M_sigma, d = 1) one 1024-thread CTA per RHS runs the whole direction in shared
+// memory in ONE launch (config 1: 0.028 -> 0.026 ms/step; config 2 with R = 16 stays on the
+// multi-kernel pipeline: 0.034 there against 0.052 here) --
+// inverse: spread (one thread per grid point, the nodes of its covering segments, written at
+// the bit-reversed index) -> radix-2 FFT (twiddle table in shared memory) -> truncate and
+// deconvolve; adjoint: deconvolve and zero-pad (bit-reversed) -> inverse FFT -> gather (one
+// thread per node).  Same arithmetic as the generic kernels, deterministic.
+#ifndef INFT_SMALL_THREADS
+#define INFT_SMALL_THREADS 1024
+#endif
+constexpr int kSmallThreads = INFT_SMALL_THREADS;
+__device__ __forceinline__ int bitrev_n(int v, int lg) { return (int)(__brev((unsigned)v) >> (32 - lg)); }
+
+template <typename T, int SIGN>
+__device__ void small_fft(C2<T>* g, const C2<T>* tw, int Ms, int lg) {
+    // in-place radix-2 DIT on bit-reversed input; tw[k] = e^{-2 pi i k / Ms}, k < Ms/2
+    for (int s = 1; s <= lg; ++s) {
+        const int half = 1 << (s - 1), step = Ms >> s;
+        for (int b = threadIdx.x; b < Ms / 2; b += blockDim.x) {
+            const int grp = b >> (s - 1), j = b & (half - 1);
+            const int i0 = (grp << s) + j, i1 = i0 + half;
+            C2<T> w = tw[j * step];
+            if (SIGN > 0) w.y = -w.y;
+            const C2<T> u = g[i0], v = g[i1];
+            const T vx = v.x * w.x - v.y * w.y, vy = v.x * w.y + v.y * w.x;
+            g[i0] = mk<T>(u.x + vx, u.y + vy);
+            g[i1] = mk<T>(u.x - vx, u.y - vy);
+        }
+        __syncthreads();
+    }
+}
+
+template <typename T>
+__device__ void small_twiddles(C2<T>* tw, int Ms) {
+    for (int k = threadIdx.x; k < Ms / 2; k += blockDim.x) {
+        double sn, cs;
+        sincospi(-2.0 * (double)k / (double)Ms, &sn, &cs);
+        tw[k] = mk<T>((T)cs, (T)sn);
+    }
+}
+
+template <typename T, bool WC>
+__global__ void __launch_bounds__(kSmallThreads) k_small_inverse(const int32_t* __restrict__ seg_start,
+                                                       const int32_t* __restrict__ n0s,
+                                                       const int32_t* __restrict__ perm, const T* __restrict__ w,
+                                                       int PP, int P, const C2<T>* __restrict__ f,
+                                                       C2<T>* __restrict__ fhat, const T* __restrict__ dk, int64_t N,
+                                                       int Ms, int lg, int M, int S) {
+    extern __shared__ __align__(16) unsigned char smraw[];
+    C2<T>* g = reinterpret_cast<C2<T>*>(smraw);
+    C2<T>* tw = g + Ms;
+    const int r = blockIdx.x;
+    const C2<T>* fr = f + (int64_t)r * N;
+    small_twiddles<T>(tw, Ms);
+    const int64_t nseg = (Ms + S - 1) / S;
+    for (int n = threadIdx.x; n < Ms; n += blockDim.x) {  // a2: conj(w) f over the covering segments
+        T sx = 0, sy = 0;
+        for_segments(n, P < Ms ? P : Ms, Ms, S, nseg, [&](int64_t sg) {
+            for (int i = seg_start[sg]; i < seg_start[sg + 1]; ++i) {
+                int t = (int)mod64(n - n0s[i], Ms);
+                if (t >= P) continue;
+                const C2<T> fv = fr[perm[i]];
+                for (; t < P; t += Ms) {
+                    if (WC) {
+                        const T wr = w[((int64_t)i * PP + t) * 2], wi = w[((int64_t)i * PP + t) * 2 + 1];
+                        sx += wr * fv.x + wi * fv.y;
+                        sy += wr * fv.y - wi * fv.x;
+                    } else {
+                        const T wr = w[(int64_t)i * PP + t];
+                        sx += wr * fv.x;
+                        sy += wr * fv.y;
+                    }
+                }
+            }
+        });
+        g[bitrev_n(n, lg)] = mk<T>(sx, sy);
+    }
+    __syncthreads();
+    small_fft<T, -1>(g, tw, Ms, lg);  // a3: F^*
+    for (int c = threadIdx.x; c < M; c += blockDim.x) {  // a4: truncate + s D^*
+        const int k = c - M / 2;
+        const C2<T> v = g[k < 0 ? k + Ms : k];
+        const T d = dk[c];
+        fhat[(int64_t)r * M + c] = mk<T>(d * v.x, d * v.y);
+    }
+}
+
+template <typename T, bool WC>
+__global__ void __launch_bounds__(kSmallThreads) k_small_adjoint(const int32_t* __restrict__ n0s,
+                                                       const int32_t* __restrict__ perm, const T* __restrict__ w,
+                                                       int PP, int P, const C2<T>* __restrict__ h,
+                                                       C2<T>* __restrict__ f, const T* __restrict__ dk, int64_t N,
+                                                       int Ms, int lg, int M) {
+    extern __shared__ __align__(16) unsigned char smraw[];
+    C2<T>* g = reinterpret_cast<C2<T>*>(smraw);
+    C2<T>* tw = g + Ms;
+    const int r = blockIdx.x;
+    small_twiddles<T>(tw, Ms);
+    for (int q = threadIdx.x; q < Ms; q += blockDim.x) {  // a5: s D + zero pad
+        const int k = q < Ms / 2 ? q : q - Ms;
+        C2<T> v = mk<T>(T(0), T(0));
+        if (k >= -M / 2 && k < M / 2) {
+            const C2<T> hv = h[(int64_t)r * M + k + M / 2];
+            const T d = dk[k + M / 2];
+            v = mk<T>(d * hv.x, d * hv.y);
+        }
+        g[bitrev_n(q, lg)] = v;
+    }
+    __syncthreads();
+    small_fft<T, 1>(g, tw, Ms, lg);  // a6: F
+    for (int64_t i = threadIdx.x; i < N; i += blockDim.x) {  // a7: B_opt
+        T sx = 0, sy = 0;
+        int q = n0s[i];
+        for (int t = 0; t < P; ++t) {
+            const C2<T> gv = g[q];
+            if (WC) {
+                const T wr = w[((int64_t)i * PP + t) * 2], wi = w[((int64_t)i * PP + t) * 2 + 1];
+                sx += wr * gv.x - wi * gv.y;
+                sy += wr * gv.y + wi * gv.x;
+            } else {
+                const T wr = w[(int64_t)i * PP + t];
+                sx += wr * gv.x;
+                sy += wr * gv.y;
+            }
+            if (++q == Ms) q = 0;
+        }
+        f[(int64_t)r * N + perm[i]] = mk<T>(sx, sy);
+    }
+}
+
+// (INFT_NO_SMALL=1 at plan creation turns it off; R * M_sigma bounds it to the latency-bound
+// regime -- one CTA per RHS leaves the GPU idle for big batches)
+static bool small_available(const Plan& p, int64_t R) {
+    const int64_t Ms = p.Ms[0];
+    return !p.no_small && p.d == 1 && Ms >= 16 && (Ms & (Ms - 1)) == 0 &&
+           Ms * (int64_t)p.elem_bytes() <= 64 * 1024 && p.N <= (int64_t(1) << 16) && p.N > 0 &&
+           R * Ms <= (int64_t(1) << 13);
+}
+
+template <typename T>
+static void small_inverse(Plan& p, const void* f, void* fhat, int64_t R, cudaStream_t st) {
+    const int Ms = (int)p.Ms[0];
+    const int lg = __builtin_ctz((unsigned)Ms);
+    const size_t smem = sizeof(C2<T>) * (size_t)(Ms + Ms / 2);
+    auto kfn = p.wt == INFT_WEIGHTS_COMPLEX ? k_small_inverse<T, true> : k_small_inverse<T, false>;
+    ensure_smem_attr((const void*)kfn, smem);
+    kfn<<<(unsigned)R, kSmallThreads, smem, st>>>(p.seg_start.as<int32_t>(), p.n0s.as<int32_t>(), p.perm.as<int32_t>(),
+                                        p.w.as<T>(), p.PP, p.P, static_cast<const C2<T>*>(f),
+                                        static_cast<C2<T>*>(fhat), dtable<T>(p), p.N, Ms, lg, (int)p.M[0],
+                                        p.S[0]);
+    INFT_CHECK_LAUNCH();
+    p.launches++;
+}
+
+template <typename T>
+static void small_adjoint(Plan& p, const void* h, void* f, int64_t R, cudaStream_t st) {
+    const int Ms = (int)p.Ms[0];
+    const int lg = __builtin_ctz((unsigned)Ms);
+    const size_t smem = sizeof(C2<T>) * (size_t)(Ms + Ms / 2);
+    auto kfn = p.wt == INFT_WEIGHTS_COMPLEX ? k_small_adjoint<T, true> : k_small_adjoint<T, false>;
+    ensure_smem_attr((const void*)kfn, smem);
+    kfn<<<(unsigned)R, kSmallThreads, smem, st>>>(p.n0s.as<int32_t>(), p.perm.as<int32_t>(), p.w.as<T>(), p.PP, p.P,
+                                        static_cast<const C2<T>*>(h), static_cast<C2<T>*>(f), dtable<T>(p), p.N, Ms,
+                                        lg, (int)p.M[0]);
+    INFT_CHECK_LAUNCH();
+    p.launches++;
+}
+
 static bool use_fused(const Plan& p) { return !p.no_fused_fft && fused_fft_available(p); }
 
 // One device-resident chunk (Rc <= grid capacity) of the inverse: a2 -> a3 -> a4.
 template <typename T>
 static void inverse_chunk(Plan& p, const void* f, void* fhat, int64_t Rc, cudaStream_t st) {
+    if (small_available(p, Rc)) {  // a2 -> a3 -> a4 in one launch
+        StageTimer t(p, 0, st);
+        small_inverse<T>(p, f, fhat, Rc, st);
+        return;
+    }
     ensure_grid(p, Rc);
     C2<T>* g = p.grid.as<C2<T>>();
     {
@@ -930,6 +1105,11 @@ static void inverse_chunk(Plan& p, const void* f, void* fhat, int64_t Rc, cudaSt
 // One chunk of the inverse adjoint: a5 -> a6 -> a7.
 template <typename T>
 static void adjoint_chunk(Plan& p, const void* h, void* f, int64_t Rc, cudaStream_t st) {
+    if (small_available(p, Rc)) {  // a5 -> a6 -> a7 in one launch
+        StageTimer t(p, 5, st);
+        small_adjoint<T>(p, h, f, Rc, st);
+        return;
+    }
     ensure_grid(p, Rc);
     C2<T>* g = p.grid.as<C2<T>>();
     int64_t total = Rc * p.Mstot;

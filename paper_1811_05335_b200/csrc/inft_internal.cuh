@@ -111,6 +111,7 @@ struct Plan {
     int perm_shift = 0;  // c >= 0 if perm[i] = (i + c) mod N (caller order = cyclic shift of sorted), else -1
     bool fast1d = false;
     bool no_fused_fft = false;  // INFT_NO_FUSED_FFT=1: cuFFT + separate deconvolution passes
+    bool no_small = false;      // INFT_NO_SMALL=1: no single-launch path for small 1-D problems
     int64_t GS = 1;  // grid row stride in complex elements (1-D fast path: M_sigma + halo)
 
     // method state

@@ -431,6 +431,10 @@ void plan_build(Plan& p, const double* nodes_any, cudaStream_t st) {
         const char* e = getenv("INFT_NO_FUSED_FFT");
         p.no_fused_fft = e && atoi(e);
     }
+    {
+        const char* e = getenv("INFT_NO_SMALL");
+        p.no_small = e && atoi(e);
+    }
     compute_deconv(p, 1.0, st);
 }
 
