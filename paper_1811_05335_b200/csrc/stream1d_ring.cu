@@ -116,8 +116,11 @@ __global__ void __launch_bounds__(128, INFT_RING_MINB) k_spread_ring(const __gri
     // node ranges whose windows go to side slots (kSidePart); a run next to a heavy segment
     // skips the prologue (kSideNoPro) and/or parks its spill into segment s1 (kSideCarry);
     // k_spread_ring_fix adds the side slots in a fixed order
-    const int* ce = chunks + 6 * blockIdx.x;
-    const int s0 = chunks ? __ldg(ce) : (int)blockIdx.x * Q;
+    // grid (row groups, chunks): the row groups of one chunk run side by side, so the second
+    // reads the chunk's node records from L2
+    const int cid = (int)blockIdx.y;
+    const int* ce = chunks + 6 * cid;
+    const int s0 = chunks ? __ldg(ce) : cid * Q;
     const int s1 = chunks ? __ldg(ce + 1) : min(s0 + Q, nseg);
     const int mode = chunks ? __ldg(ce + 4) : 0;
     const int slot = chunks ? __ldg(ce + 5) : 0;
@@ -142,7 +145,7 @@ __global__ void __launch_bounds__(128, INFT_RING_MINB) k_spread_ring(const __gri
         pos = s + (b - base) * kNB;
         cnt = min(kNB, e - pos);
     };
-    const int row0 = blockIdx.y * WPB * 32;
+    const int row0 = (int)blockIdx.x * WPB * 32;
     auto issue = [&](int b, int stage) {
         int pos, cnt;
         bool pro;
@@ -379,7 +382,7 @@ __global__ void __launch_bounds__(128, INFT_RING_MINB) k_gather_ring(const __gri
     const int WPB = blockDim.x >> 5;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const uint32_t sw = ((uint32_t)lane << 7) | ((uint32_t)(lane & 7) << 4);
-    const int row0 = blockIdx.y * WPB * 32;
+    const int row0 = (int)blockIdx.x * WPB * 32;
     const int r = row0 + threadIdx.x;
     const bool active = r < R;
 
@@ -398,11 +401,12 @@ __global__ void __launch_bounds__(128, INFT_RING_MINB) k_gather_ring(const __gri
     // chunk = Q segments, or a node-balanced run of segments from the chunk table
     // chunk = Q segments, or an entry (s0, s1, first node, end node) of the gather's chunk
     // table: node-balanced runs of segments, and heavy segments split into node ranges
-    const int s0 = chunks ? __ldg(chunks + 4 * blockIdx.x) : (int)blockIdx.x * Q;
-    const int s1 = chunks ? __ldg(chunks + 4 * blockIdx.x + 1) : min(s0 + Q, nseg);
+    const int cid = (int)blockIdx.y;  // grid (row groups, chunks), as the spread
+    const int s0 = chunks ? __ldg(chunks + 4 * cid) : cid * Q;
+    const int s1 = chunks ? __ldg(chunks + 4 * cid + 1) : min(s0 + Q, nseg);
     const int nbox = s1 - s0 + 1;  // box L = grid points of segment s0 + L (halo covers L = nseg)
-    const int b0 = chunks ? __ldg(chunks + 4 * blockIdx.x + 2) : __ldg(seg_start + s0);
-    const int b1 = chunks ? __ldg(chunks + 4 * blockIdx.x + 3) : __ldg(seg_start + s1);
+    const int b0 = chunks ? __ldg(chunks + 4 * cid + 2) : __ldg(seg_start + s0);
+    const int b1 = chunks ? __ldg(chunks + 4 * cid + 3) : __ldg(seg_start + s1);
     const int wrap = N - cshift;
     const int bw = (cshift > 0 && b0 < wrap && wrap < b1) ? wrap : b1;
     const int c1 = (bw - b0 + kNB - 1) / kNB;
@@ -679,6 +683,8 @@ bool ring_available(const Plan& p) {
         return false;
     if (p.S[0] != 2 * p.m) return false;
     if (p.prec == INFT_C64 && !ring_c64_spread_enabled()) return false;
+    // chunks are gridDim.y (<= 65535): at most nseg / kQ + the node-balanced / split ones
+    if (p.nseg[0] / ring::kQ + 2 * 148 * 64 > 65535) return false;
     // the f / output tensor maps need a row stride (N elements) that is a multiple of 16 bytes
     if ((p.N * (int64_t)p.elem_bytes()) % 16) return false;
     return p.prec == INFT_C128 ? ring_fns<double>(p.m).spread != nullptr : ring_fns<float>(p.m).spread != nullptr;
@@ -727,7 +733,7 @@ static int ring_cps() {
     static const int v = [] {
         const char* e = getenv("INFT_RING_CPS");
         const int x = e ? atoi(e) : 0;
-        return x >= 1 && x <= 256 ? x : 16;
+        return x >= 1 && x <= 64 ? x : 16;  // <= 64: chunk counts stay below gridDim.y's limit
     }();
     return v;
 }
@@ -915,7 +921,7 @@ static void ring_spread_t(Plan& p, const void* f, void* grid, int64_t R, cudaStr
     tmap_or_throw(&gm, grid, (uint64_t)p.GS * ce, (uint64_t)R, sizeof(C2<T>) * (uint64_t)p.GS, 32u, "spread grid");
     size_t smem = ring_spread_smem<T>(wpb, p.PP, p.S[0]);
     ensure_smem_attr((const void*)F.spread, smem);
-    dim3 g((unsigned)nchunks, (unsigned)ceil_div(R, 32 * wpb));
+    dim3 g((unsigned)ceil_div(R, 32 * wpb), (unsigned)nchunks);
     F.spread<<<g, 32 * wpb, smem, st>>>(fm, gm, p.seg_start.as<int32_t>(), chunks, p.w.as<T>(), p.PP, nseg, 0,
                                         (int)p.N, p.perm_shift, p.ring_side.as<C2<T>>(), (int)R);
     INFT_CHECK_LAUNCH();
@@ -958,7 +964,7 @@ static void ring_gather_t(Plan& p, const void* grid, void* f, int64_t R, cudaStr
     tmap_or_throw(&om, f, (uint64_t)p.N * ce, (uint64_t)R, sizeof(C2<T>) * (uint64_t)p.N, 32u, "gather f");
     size_t smem = ring_gather_smem<T>(wpb, p.PP, p.S[0]);
     ensure_smem_attr((const void*)F.gather, smem);
-    dim3 g((unsigned)nchunks, (unsigned)ceil_div(R, 32 * wpb));
+    dim3 g((unsigned)ceil_div(R, 32 * wpb), (unsigned)nchunks);
     F.gather<<<g, 32 * wpb, smem, st>>>(gm, om, p.seg_start.as<int32_t>(), chunks, p.w.as<T>(), p.PP,
                                         static_cast<C2<T>*>(f), p.N, nseg, 0, (int)R, p.perm_shift);
     INFT_CHECK_LAUNCH();
