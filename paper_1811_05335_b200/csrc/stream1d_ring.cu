@@ -47,6 +47,12 @@ constexpr int kStages = INFT_RING_STAGES;  // spread load pipeline depth (2: mor
 #define INFT_RING_STAGES_G 3
 #endif
 constexpr int kStagesG = INFT_RING_STAGES_G;  // gather window pipeline depth (config 5: 3 -> 0.993 ms, 2 -> 1.018)
+#ifndef INFT_RING_STAGES_GR
+#define INFT_RING_STAGES_GR 2
+#endif
+// gather node-record pipeline depth: 2 keeps a CTA at <= 37 KB of shared memory (6 CTAs per SM
+// instead of 5 with 3 record stages)
+constexpr int kStagesGR = INFT_RING_STAGES_GR;
 
 #define INFT_CASES_64(X)                                                                                      \
     X(0) X(1) X(2) X(3) X(4) X(5) X(6) X(7) X(8) X(9) X(10) X(11) X(12) X(13) X(14) X(15) X(16) X(17) X(18)   \
@@ -392,10 +398,10 @@ __global__ void __launch_bounds__(128, INFT_RING_MINB) k_gather_ring(const __gri
     unsigned char* wbuf = smem;
     unsigned char* stg = smem + kStagesG * wstage;  // [WPB][OBOX][32][128]
     unsigned char* rbuf = stg + (size_t)WPB * OBOX * 4096u;
-    uint64_t* fullW = reinterpret_cast<uint64_t*>(rbuf + kStagesG * rstage);
+    uint64_t* fullW = reinterpret_cast<uint64_t*>(rbuf + kStagesGR * rstage);
     uint64_t* emptyW = fullW + kStagesG;
     uint64_t* fullR = emptyW + kStagesG;
-    uint64_t* emptyR = fullR + kStagesG;
+    uint64_t* emptyR = fullR + kStagesGR;
     unsigned char* my_stg = stg + (size_t)warp * OBOX * 4096u;
 
     // chunk = Q segments, or a node-balanced run of segments from the chunk table
@@ -443,6 +449,8 @@ __global__ void __launch_bounds__(128, INFT_RING_MINB) k_gather_ring(const __gri
         for (int i = 0; i < kStagesG; ++i) {
             mbar_init(&fullW[i], 1);
             mbar_init(&emptyW[i], WPB);
+        }
+        for (int i = 0; i < kStagesGR; ++i) {
             mbar_init(&fullR[i], 1);
             mbar_init(&emptyR[i], WPB);
         }
@@ -451,7 +459,7 @@ __global__ void __launch_bounds__(128, INFT_RING_MINB) k_gather_ring(const __gri
     __syncthreads();
     if (threadIdx.x == 0) {
         for (int L = 0; L < min(kStagesG, nbox); ++L) issueW(L, L);
-        for (int b = 0; b < min(kStagesG, nbat); ++b) issueR(b, b);
+        for (int b = 0; b < min(kStagesGR, nbat); ++b) issueR(b, b);
     }
 
     T wx[K], wy[K];
@@ -491,8 +499,8 @@ __global__ void __launch_bounds__(128, INFT_RING_MINB) k_gather_ring(const __gri
     C2<T>* __restrict__ fr = f + (int64_t)(active ? r : 0) * N;
     const int rstore = row0 + warp * 32;
     for (int b = 0; b < nbat; ++b) {
-        const int stage = b % kStagesG;
-        const uint32_t parity = (uint32_t)((b / kStagesG) & 1);
+        const int stage = b % kStagesGR;
+        const uint32_t parity = (uint32_t)((b / kStagesGR) & 1);
         int pos, cnt;
         batch_pos(b, pos, cnt);
         mbar_wait(&fullR[stage], parity);
@@ -612,9 +620,9 @@ __global__ void __launch_bounds__(128, INFT_RING_MINB) k_gather_ring(const __gri
         fence_proxy_async();
         __syncwarp();
         if (lane == 0) mbar_arrive(&emptyR[stage]);
-        if (threadIdx.x == 0 && b + kStagesG < nbat) {
+        if (threadIdx.x == 0 && b + kStagesGR < nbat) {
             mbar_wait(&emptyR[stage], parity);
-            issueR(b + kStagesG, stage);
+            issueR(b + kStagesGR, stage);
         }
     }
     while (nextL < nbox) consume_box();  // no copy may be in flight at exit
@@ -715,8 +723,8 @@ static size_t ring_gather_smem(int wpb, int PP, int SEG) {
     const int EB = 128 / (int)sizeof(C2<T>);
     size_t wsz = (size_t)ring::kStagesG * (SEG / EB) * wpb * 4096;
     size_t st = (size_t)wpb * (ring::kNB / EB) * 4096;
-    size_t r = (size_t)ring::kStagesG * ((ring::kNB * PP * (int)sizeof(T) + 127) & ~127);
-    return wsz + st + r + 4 * ring::kStagesG * sizeof(uint64_t);
+    size_t r = (size_t)ring::kStagesGR * ((ring::kNB * PP * (int)sizeof(T) + 127) & ~127);
+    return wsz + st + r + 2 * (ring::kStagesG + ring::kStagesGR) * sizeof(uint64_t);
 }
 
 static void tmap_or_throw(CUtensorMap* m, const void* base, uint64_t inner, uint64_t rows, uint64_t stride,
