@@ -530,19 +530,25 @@ __global__ void __launch_bounds__(128, INFT_RING_MINB) k_gather_ring(const __gri
                 for (int q = 0; q < kNB; ++q) {
                     T wv[P];
                     WeightLoader<T, P>::load_smem(rec + q * PP, wv);
-                    T sx0 = 0, sy0 = 0, sx1 = 0, sy1 = 0;  // two chains: halve the FMA latency chain
+#ifndef INFT_GATHER_CHAINS
+#define INFT_GATHER_CHAINS 2
+#endif
+                    constexpr int NCH = INFT_GATHER_CHAINS;  // independent FMA chains per output
+                    T sx[NCH], sy[NCH];
+#pragma unroll
+                    for (int c = 0; c < NCH; ++c) sx[c] = sy[c] = T(0);
 #pragma unroll
                     for (int t = 0; t < P; ++t) {
                         const int rg = (q + t + SEG * PH) % K;
-                        if (t & 1) {
-                            sx1 = fma(wv[t], wx[rg], sx1);
-                            sy1 = fma(wv[t], wy[rg], sy1);
-                        } else {
-                            sx0 = fma(wv[t], wx[rg], sx0);
-                            sy0 = fma(wv[t], wy[rg], sy0);
-                        }
+                        sx[t % NCH] = fma(wv[t], wx[rg], sx[t % NCH]);
+                        sy[t % NCH] = fma(wv[t], wy[rg], sy[t % NCH]);
                     }
-                    *reinterpret_cast<C2<T>*>(my_stg + cofs<T>(q, sw)) = mk<T>(sx0 + sx1, sy0 + sy1);
+#pragma unroll
+                    for (int c = 1; c < NCH; ++c) {
+                        sx[0] += sx[c];
+                        sy[0] += sy[c];
+                    }
+                    *reinterpret_cast<C2<T>*>(my_stg + cofs<T>(q, sw)) = mk<T>(sx[0], sy[0]);
                 }
             };
             if (cur_i & 1)
