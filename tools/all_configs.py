@@ -3,7 +3,6 @@ one table for DESIGN.md / profiles.  Step = one inverse + one inverse adjoint ap
 import numpy as np
 import torch
 
-import oracle as O
 import paper_1811_05335_b200 as P
 import synth as S
 
@@ -14,12 +13,8 @@ for cid in (1, 2, 3, 4, 5):
     M = c["M"][0] if c["d"] == 1 else c["M"]
     sigma, m = c["sigma"], c["m"]
     R = c["R"] if cid != 5 else 64
-    if c["d"] == 1:
-        live = O.slot_live(x, O.msigma(M, sigma), m)
-    else:
-        l1 = O.slot_live(x[:, 0], O.msigma(M[0], sigma), m)
-        l2 = O.slot_live(x[:, 1], O.msigma(M[1], sigma), m)
-        live = (l1[:, :, None] & l2[:, None, :]).reshape(x.shape[0], -1)
+    # live slots = the support of the window matrix B (positive Kaiser-Bessel weights)
+    live = P.Plan(x, M, sigma, m).precompute("plain").get_bopt() != 0
     w = np.random.default_rng(cid).standard_normal(live.shape) * live
     for prec in ("c128", "c64"):
         plan = P.Plan(x, M, sigma, m, precision=prec).set_bopt(w, "alg2")

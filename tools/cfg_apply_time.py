@@ -4,7 +4,6 @@ import sys
 import numpy as np
 import torch
 
-import oracle as O
 import paper_1811_05335_b200 as P
 import synth as S
 
@@ -15,12 +14,8 @@ x = S.make_nodes(c)
 M = c["M"][0] if c["d"] == 1 else c["M"]
 sigma, m, R = c["sigma"], c["m"], c["R"] if cid != 5 else 64
 rng = np.random.default_rng(0)
-if c["d"] == 1:
-    live = O.slot_live(x, O.msigma(M, sigma), m)
-else:
-    l1 = O.slot_live(x[:, 0], O.msigma(M[0], sigma), m)
-    l2 = O.slot_live(x[:, 1], O.msigma(M[1], sigma), m)
-    live = (l1[:, :, None] & l2[:, None, :]).reshape(x.shape[0], -1)
+# live slots = the support of the window matrix B (positive Kaiser-Bessel weights)
+live = P.Plan(x, M, sigma, m).precompute("plain").get_bopt() != 0
 w = rng.standard_normal(live.shape) * live
 plan = P.Plan(x, M, sigma, m, precision=prec).set_bopt(w, "alg2")
 dt = torch.complex128 if prec == "c128" else torch.complex64
