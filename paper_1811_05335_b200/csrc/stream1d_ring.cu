@@ -255,8 +255,11 @@ __global__ void __launch_bounds__(128, INFT_RING_MINB) k_spread_ring(const __gri
         bool dense = false;
         if constexpr (SEG == kNB) {
             if (cnt == kNB) {
-                const unsigned fa = (unsigned)rec_n0(rec, P), fz = (unsigned)rec_n0(rec + (kNB - 1) * PP, P);
-                dense = (fa % SEG == 0) && (fz == fa + SEG - 1);
+                // node q of the batch at offset q of one segment: every slot base checked (first
+                // and last alone do not exclude a repeated offset beside a skipped one)
+                const unsigned fa = (unsigned)rec_n0(rec, P);
+                const unsigned nq = (unsigned)rec_n0(rec + (lane & (kNB - 1)) * PP, P);
+                dense = __all_sync(0xffffffffu, (fa % SEG == 0) && nq == fa + (unsigned)(lane & (kNB - 1)));
             }
         }
         if (dense) {
@@ -513,8 +516,10 @@ __global__ void __launch_bounds__(128, INFT_RING_MINB) k_gather_ring(const __gri
         bool dense = false;
         if constexpr (SEG == kNB) {
             if (full_tile) {
-                const unsigned fa = (unsigned)rec_n0(rec, P), fz = (unsigned)rec_n0(rec + (kNB - 1) * PP, P);
-                dense = (fa % SEG == 0) && (fz == fa + SEG - 1);
+                // as the spread: every node's slot base checked
+                const unsigned fa = (unsigned)rec_n0(rec, P);
+                const unsigned nq = (unsigned)rec_n0(rec + (lane & (kNB - 1)) * PP, P);
+                dense = __all_sync(0xffffffffu, (fa % SEG == 0) && nq == fa + (unsigned)(lane & (kNB - 1)));
             }
         }
         int ncnt = cnt;
