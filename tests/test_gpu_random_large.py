@@ -1,6 +1,8 @@
 """GPU: seeded random problems at sizes where the hot-path kernels run with many chunks and
 tiles (M up to 2^17, ring kernels m in {4, 8, 16}, fused four-step FFT passes, multiple row
 groups, CUDA-graph replay), element-wise against the oracle's C apply."""
+import os
+
 import numpy as np
 import pytest
 
@@ -48,7 +50,8 @@ def _case(seed):
     return M, m, x, R, prec, kind
 
 
-@pytest.mark.parametrize("seed", range(24))
+# INFT_RANDOM_LARGE=n widens the sweep
+@pytest.mark.parametrize("seed", range(int(os.environ.get("INFT_RANDOM_LARGE", "24"))))
 def test_random_large(P, torch, seed):
     M, m, x, R, prec, kind = _case(seed)
     sigma = 2.0
@@ -74,7 +77,7 @@ def test_random_large(P, torch, seed):
         assert O.rel_l2(c(oa), ref_a) <= tol, (seed, M, m, kind, R, prec)
 
 
-@pytest.mark.parametrize("seed", range(4))
+@pytest.mark.parametrize("seed", range(max(4, int(os.environ.get("INFT_RANDOM_LARGE", "24")) // 6)))
 def test_random_large_2d(P, torch, seed):
     """2-D tile kernels (heavy tiles split, partial sums combined) at larger sizes."""
     rng = np.random.default_rng(8000 + seed)
