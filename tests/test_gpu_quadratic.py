@@ -119,3 +119,25 @@ def test_fast_summation_equals_direct(P, torch, N, kind):
     tol = 1e-9 if kind == "jittered" else 1e-7
     assert O.rel_l2(qf.apply(f).cpu().numpy(), qd.apply(f).cpu().numpy()) < tol
     assert O.rel_l2(qf.adjoint_apply(h).cpu().numpy(), qd.adjoint_apply(h).cpu().numpy()) < tol
+
+
+@pytest.mark.parametrize("seed", range(8))
+def test_fast_summation_random(P, torch, seed):
+    """Random even N (not powers of two) and jitter levels: fast summation = direct sums."""
+    import os
+    rng = np.random.default_rng(900 + seed)
+    N = 2 * int(rng.integers(256, 15000))
+    y = S.jittered(N, seed, jitter=float(rng.choice([0.05, 0.25, 0.45])))
+    delta = float(rng.choice([0.0, 0.3 / N, 0.7 / N]))
+    qf = P.QuadPlan(y, delta=delta)
+    os.environ["INFT_QUAD_DIRECT"] = "1"
+    try:
+        qd = P.QuadPlan(y, delta=delta)
+    finally:
+        del os.environ["INFT_QUAD_DIRECT"]
+    np.testing.assert_array_equal(qf.coeffs()[0], qd.coeffs()[0])
+    R = int(rng.choice([1, 5, 20]))
+    f = torch.from_numpy(S.normal_complex(R, N, seed)).cuda()
+    h = torch.from_numpy(S.normal_complex(R, N, seed + 1)).cuda()
+    assert O.rel_l2(qf.apply(f).cpu().numpy(), qd.apply(f).cpu().numpy()) < 1e-9, (N, seed)
+    assert O.rel_l2(qf.adjoint_apply(h).cpu().numpy(), qd.adjoint_apply(h).cpu().numpy()) < 1e-9, (N, seed)
