@@ -108,3 +108,45 @@ def test_alg2_gpu_setup_large_columns(P, cid):
         assert abs(rg - ro) <= 1e-6, (n, len(js), ro, rg)
     print(f"config {cid}: GPU Alg. 2 setup {dt:.2f} s, {len(big)} large columns, "
           f"max |I(l)| {info['max_col_size']}, max rank {info['max_lowrank_rank']}")
+
+
+@pytest.mark.parametrize("seed", range(6))
+def test_alg2_random_large_columns(P, seed):
+    """Seeded random 1-D node clusters whose grid columns hold more than 64 unknowns (the
+    pivoted-Cholesky low-rank solver) next to ordinary ones: sampled columns, including the
+    largest, reach the oracle's per-column optimum."""
+    rng = np.random.default_rng(4000 + seed)
+    M = int(rng.choice([512, 1024, 2048]))
+    sigma = float(rng.choice([1.5, 2.0]))
+    if (sigma * M) % 2:
+        sigma = 2.0
+    m = int(rng.integers(2, 9))
+    N = int(rng.choice([8192, 16384]))
+    width = float(rng.choice([0.002, 0.01, 0.03]))
+    x = np.sort(np.clip(np.concatenate([rng.normal(rng.uniform(-0.4, 0.4), width, N // 2),
+                                        rng.random(N - N // 2) - 0.5]), -0.5, 0.5 - 1e-12))
+    window = "dirichlet" if seed % 3 == 2 else "kb"
+    plan = P.Plan(x, M, sigma, m, window=window).precompute("alg2")
+    w = plan.get_bopt()
+    assert np.all(np.isfinite(w))
+    Ms = O.msigma(M, sigma)
+    sets = _columns_1d(x, Ms, m)
+    big = [n for n in sets if len(sets[n]) > 64]
+    assert big, "the cluster should produce low-rank columns"
+    by_size = sorted((n for n in sets if 0 < len(sets[n]) <= 400), key=lambda n: -len(sets[n]))
+    small = [n for n in sets if 0 < len(sets[n]) <= 64]
+    sample = by_size[:2] + list(rng.choice(big, min(3, len(big)), replace=False)) + \
+        list(rng.choice(small, 4, replace=False))
+    for n in sample:
+        if len(sets[n]) > 400:
+            continue
+        js = [j for j, _ in sets[n]]
+        ts = [t for _, t in sets[n]]
+        xs = x[js]
+        l = n - Ms if n >= Ms // 2 else n
+        G = np.real(_kernel_rows(lambda d, M_, s_, m_: O.G_kernel(d, M_, s_, m_, window),
+                                 O.wrap_diff(xs[:, None] - xs[None, :]), M, sigma, m))
+        y = np.real(O.Kplus_kernel(O.wrap_diff(xs - l / Ms), M, sigma, m, window))
+        bo, _ = O.solve_minnorm_gram(G, y)
+        ro, rg = _resid(G, y, bo), _resid(G, y, w[js, ts])
+        assert abs(rg - ro) <= 1e-6, (seed, n, len(js), ro, rg)
