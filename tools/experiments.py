@@ -181,7 +181,7 @@ def err_table(title, cases, method):
 
 
 def e7(cs):
-    print("## E7  quadratic case M = N (Lagrange inverse, direct GPU sums): errors per node, jittered, fhat in [1,100]")
+    print("## E7  quadratic case M = N (Lagrange inverse; fast summation for N >= 512, direct sums below): errors per node, jittered, fhat in [1,100]")
     print(f"{'N':>6} {'e2abs/N':>9} {'e2rel/N':>9} {'einf/N':>9} {'einfrel/N':>9} {'ms':>8}")
     for c in cs:
         N = 1 << c
