@@ -7,7 +7,7 @@ figures' PDFs are not in the container, so the output is tables of the same quan
   E4  Alg. 2 setup time, B-spline vs Dirichlet, m = 2, sigma = 1, M = 128     (Fig. P:1425-1431)
   E5  Alg. 1 errors per node, inverse and inverse adjoint                     (Ex. P:1052-1143)
   E6  Alg. 2 errors per node, inverse and inverse adjoint                     (Ex. P:1467-1552)
-  E7  quadratic case errors per node (direct-sum Lagrange inverse)           (Ex. P:501-544)
+  E7  quadratic case errors per node (Lagrange inverse, fast summation)      (Ex. P:501-544)
 
 Every setup and apply runs in the library (libinft.so); the dense matrices of the metrics
 (A, F, D, B from the plan's own weights and deconvolution table) are formed with torch on
