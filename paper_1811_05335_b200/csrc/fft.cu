@@ -309,6 +309,64 @@ __device__ __forceinline__ void cta_fft(const C2<T>* tw, C2<T>* sm, Load&& load,
     fft_stages<T, SIGN, Geo<T, L>, 0, 1>(tw, sm, load, store);
 }
 
+// In-place variant (experiment, INFT_FFT_IP): the tile buffer is also the work buffer, so a
+// CTA needs one ~80 KB buffer and two CTAs share an SM; stage 0 reads the landed tile, waits
+// for every thread, then writes the skewed work layout into the same buffer; after the last
+// stage has read the buffer, on_free() (thread 0) issues the next tile's copy into it.
+template <typename T, int SIGN, typename G, int R, int NS, int SI, typename Load, typename Store, typename Free>
+__device__ __forceinline__ void run_stage_ip(const C2<T>* tw, C2<T>* sm, Load&& load, Store&& store, Free&& on_free) {
+    constexpr int L = G::ST - G::PAD;
+    constexpr int TF = G::TF;
+    constexpr int nbut = L / R;
+    constexpr int total = nbut * TF;
+    constexpr int per = (total + G::NT - 1) / G::NT;
+    constexpr bool last = SI == G::NST - 1;
+    C2<T> a[per][R];
+#pragma unroll
+    for (int p = 0; p < per; ++p) {
+        const int t = threadIdx.x + p * G::NT;
+        if (total % G::NT != 0 && t >= total) break;
+        const int f = t % TF, j = t / TF;
+#pragma unroll
+        for (int m = 0; m < R; ++m) {
+            const int n = j + m * nbut;
+            if constexpr (SI == 0)
+                a[p][m] = load(f, n, p, m);
+            else
+                a[p][m] = sm[sidx<G>(f, n)];
+        }
+    }
+    if constexpr (last) fence_proxy_async();  // generic reads before the next tile's TMA
+    __syncthreads();  // every read of the shared buffer done (the writes below reuse it)
+    if constexpr (last) on_free();
+#pragma unroll
+    for (int p = 0; p < per; ++p) {
+        const int t = threadIdx.x + p * G::NT;
+        if (total % G::NT != 0 && t >= total) break;
+        const int f = t % TF, j = t / TF;
+        stage_regs<T, SIGN, R, L, NS>(a[p], j, tw);
+        const int base = (j / NS) * NS * R + (j % NS);
+#pragma unroll
+        for (int m = 0; m < R; ++m) {
+            const int k = base + m * NS;
+            if constexpr (last)
+                store(f, k, a[p][m], m);
+            else
+                sm[sidx<G>(f, k)] = a[p][m];
+        }
+    }
+    if constexpr (!last) __syncthreads();
+}
+
+template <typename T, int SIGN, typename G, int SI, int NS, typename Load, typename Store, typename Free>
+__device__ __forceinline__ void fft_stages_ip(const C2<T>* tw, C2<T>* sm, Load&& load, Store&& store, Free&& on_free) {
+    if constexpr (SI < G::NST) {
+        constexpr int R = (SI == 0) ? G::RF : kRB;
+        run_stage_ip<T, SIGN, G, R, NS, SI>(tw, sm, load, store, on_free);
+        fft_stages_ip<T, SIGN, G, SI + 1, NS * R>(tw, sm, load, store, on_free);
+    }
+}
+
 // byte offset of pass B's deconvolution tile: after tile[2] | work | twiddles, 128-aligned
 template <typename T>
 __host__ __device__ constexpr size_t d_offset(int L, int ST, int SW, int TB) {
@@ -421,6 +479,90 @@ __global__ void __launch_bounds__(Geo<T, L>::NT, 1)
         cta_fft<T, SIGN, L>(tws, work, load, store);
         fence_proxy_async();  // this thread's reads of tile[b] precede the next TMA into it
         __syncthreads();      // tile[b] and work free for the next iteration
+    }
+}
+
+// Pass A in place (MODE 0 inverse, MODE 1 adjoint; same data flow as k_pass_a): one buffer
+// of max(L TA, SW TA) elements per CTA, two CTAs per SM (config 5 pass A MODE 0: 0.886 ->
+// 0.826 ms against the double-buffered one-CTA kernel).
+template <typename T, int SIGN, int MODE, int L>
+__global__ void __launch_bounds__(Geo<T, L>::NT, 2)
+    k_pass_a_ip(const __grid_constant__ CUtensorMap map, const __grid_constant__ CUtensorMap dmap, Args<T> A, int BR,
+                int ntiles) {
+    extern __shared__ __align__(128) unsigned char smraw[];
+    constexpr int CE = (int)(sizeof(C2<T>) / 8);
+    using G = Geo<T, L>;
+    constexpr int TA = G::TF, S = G::SW;
+    constexpr int BUF = (L * TA > S * TA ? L * TA : S * TA);
+    C2<T>* buf = reinterpret_cast<C2<T>*>(smraw);
+    C2<T>* tws = buf + BUF;
+    uint64_t* bar = reinterpret_cast<uint64_t*>(tws + L / kRB);
+    const int N2 = A.N2;
+    const int tiles_per_rhs = N2 / TA;
+    const int B = (int)(A.M / 2 / N2);  // band rows on each side (MODE 1)
+    constexpr int DW = (int)(16 / sizeof(T)) > TA ? (int)(16 / sizeof(T)) : TA;
+    const uint32_t tile_bytes = (uint32_t)(MODE == 0 ? sizeof(C2<T>) * TA * L
+                                                     : sizeof(C2<T>) * TA * 2 * B + sizeof(T) * DW * 2 * B);
+    if (threadIdx.x == 0) {
+        prefetch_tmap(&map);
+        if (MODE == 1) prefetch_tmap(&dmap);
+        mbar_init(bar, 1);
+        fence_barrier_init();
+    }
+    for (int i = threadIdx.x; i < L / kRB; i += blockDim.x) tws[i] = A.tw1[i];
+    __syncthreads();
+    auto issue = [&](int id) {
+        const int r = id / tiles_per_rhs, c0 = (id % tiles_per_rhs) * TA * CE;
+        mbar_arrive_expect_tx(bar, tile_bytes);
+        if (MODE == 0) {
+            for (int q = 0; q < L; q += BR) tma_load_3d(buf + q * TA, &map, c0, q, r, bar);
+        } else {
+            T* dsm = reinterpret_cast<T*>(buf + B * TA);
+            const int dc0 = ((id % tiles_per_rhs) * TA) & ~(DW - 1);
+            for (int q = 0; q < B; q += BR) {
+                tma_load_3d(buf + q * TA, &map, c0, B + q, r, bar);
+                tma_load_3d(buf + (L - B + q) * TA, &map, c0, q, r, bar);
+                tma_load_3d(dsm + q * DW, &dmap, dc0, B + q, 0, bar);
+                tma_load_3d(dsm + (B + q) * DW, &dmap, dc0, q, 0, bar);
+            }
+        }
+    };
+    const int fl = threadIdx.x % TA, jl = threadIdx.x < TA * (L / kRB) ? threadIdx.x / TA : 0;
+    const int lmask = (1 << A.LB) - 1;
+    int it = 0;
+    if (threadIdx.x == 0 && (int)blockIdx.x < ntiles) issue(blockIdx.x);
+    for (int id = blockIdx.x; id < ntiles; id += gridDim.x, ++it) {
+        const int64_t r = id / tiles_per_rhs;
+        const int col0 = (id % tiles_per_rhs) * TA;
+        const int n2l = col0 + fl;
+        const int e0 = n2l * jl, eq = n2l * (L / kRB);
+        const C2<T> t0a = twid_g<T, SIGN>(A.tlo, e0 & lmask), t0b = twid_g<T, SIGN>(A.thi, e0 >> A.LB);
+        const C2<T> tqa = twid_g<T, SIGN>(A.tlo, eq & lmask), tqb = twid_g<T, SIGN>(A.thi, eq >> A.LB);
+        mbar_wait(bar, it & 1);
+        const T* dsm = reinterpret_cast<const T*>(buf + B * TA);
+        auto load = [&](int f, int n1, int, int) -> C2<T> {
+            if (MODE == 0) return buf[n1 * TA + f];
+            if (n1 >= B && n1 < L - B) return mk<T>(T(0), T(0));
+            const C2<T> v = buf[n1 * TA + f];
+            const T d = dsm[(n1 < B ? n1 : n1 - (L - 2 * B)) * DW + (col0 & (DW - 1)) + f];
+            return mk<T>(d * v.x, d * v.y);
+        };
+        C2<T> wq, wcur;
+        C2<T>* orow = (MODE == 0) ? A.grid + r * A.GS : A.ybuf + r * A.N;
+        auto store = [&](int f, int k1, C2<T> v, int m) {
+            if (m == 0) {
+                wq = cmul<T>(tqa, tqb);
+                wcur = cmul<T>(t0a, t0b);
+            } else {
+                wcur = cmul<T>(wcur, wq);
+            }
+            orow[(int64_t)k1 * N2 + col0 + f] = cmul<T>(v, wcur);
+        };
+        const int nxt = id + (int)gridDim.x;
+        auto on_free = [&]() {
+            if (threadIdx.x == 0 && nxt < ntiles) issue(nxt);
+        };
+        fft_stages_ip<T, SIGN, G, 0, 1>(tws, buf, load, store, on_free);
     }
 }
 
@@ -784,8 +926,32 @@ static void launch_pass_a(Plan& p, fft::Args<T>& A, int mode, const void* src, i
         set_error("cuTensorMapEncodeTiled failed (fused FFT pass A)");
         throw Fail{INFT_ERR_CUDA};
     }
-    const size_t smem = cs * (size_t)(2 * L * TA + SW * TA + L / fft::kRB) + 16;
     const int ntiles = (int)(R * (A.N2 / TA));
+    // in-place pass A (two CTAs per SM) unless INFT_FFT_IP=0
+    static const bool ip = [] {
+        const char* e = getenv("INFT_FFT_IP");
+        return !(e && atoi(e) == 0);
+    }();
+    if (ip && sizeof(T) == 8) {  // complex64 (512-thread tiles) would spill at 64 registers
+        PassAFn<T> kf = nullptr;
+        switch (L) {
+            case 512: kf = mode == 0 ? fft::k_pass_a_ip<T, -1, 0, 512> : fft::k_pass_a_ip<T, 1, 1, 512>; break;
+            case 1024: kf = mode == 0 ? fft::k_pass_a_ip<T, -1, 0, 1024> : fft::k_pass_a_ip<T, 1, 1, 1024>; break;
+            case 2048: kf = mode == 0 ? fft::k_pass_a_ip<T, -1, 0, 2048> : fft::k_pass_a_ip<T, 1, 1, 2048>; break;
+            default: break;
+        }
+        if (kf) {
+            const size_t smem_ip = cs * (size_t)(std::max(L * TA, SW * TA) + L / fft::kRB) + 16;
+            ensure_smem_attr((const void*)kf, smem_ip);
+            const int occ = occupancy_cached((const void*)kf, threads, smem_ip);
+            kf<<<(unsigned)std::min(ntiles, num_sms() * std::max(1, occ)), threads, smem_ip, st>>>(map, dmap, A, BR,
+                                                                                                    ntiles);
+            INFT_CHECK_LAUNCH();
+            p.launches++;
+            return;
+        }
+    }
+    const size_t smem = cs * (size_t)(2 * L * TA + SW * TA + L / fft::kRB) + 16;
     ensure_smem_attr((const void*)ka, smem);
     const int occ = occupancy_cached((const void*)ka, threads, smem);
     ka<<<(unsigned)std::min(ntiles, num_sms() * std::max(1, occ)), threads, smem, st>>>(map, dmap, A, BR, ntiles);
