@@ -706,6 +706,102 @@ __global__ void __launch_bounds__(Geo<T, L>::NT, 1)
     if (kStageB && threadIdx.x == 0) bulk_wait<0>();
 }
 
+// Pass B in place (complex128): one buffer of max(ST TB, SW TB) elements plus the d side
+// buffer (MODE 0), two CTAs per SM, plain stores from registers (the staged TMA stores of
+// k_pass_b would hold the buffer the next tile lands in).
+template <typename T, int SIGN, int MODE, int L>
+__global__ void __launch_bounds__(Geo<T, L>::NT, 2)
+    k_pass_b_ip(const __grid_constant__ CUtensorMap dmap, const __grid_constant__ CUtensorMap omap, Args<T> A,
+                int BRd, int BRo, int ntiles) {
+    extern __shared__ __align__(128) unsigned char smraw[];
+    using G = Geo<T, L>;
+    constexpr int TB = G::TF, S = G::ST, SW = G::SW;
+    constexpr int BUF = (S * TB > SW * TB ? S * TB : SW * TB);
+    constexpr int DW = (int)(16 / sizeof(T)) > TB ? (int)(16 / sizeof(T)) : TB;
+    const int N1 = A.N1;
+    const int64_t half = A.M / 2;
+    const int B2 = (int)(half / N1);
+    C2<T>* buf = reinterpret_cast<C2<T>*>(smraw);
+    C2<T>* tws = buf + BUF;
+    T* dsm = reinterpret_cast<T*>(smraw + ((sizeof(C2<T>) * (size_t)(BUF + L / kRB) + 127) / 128 * 128));
+    uint64_t* bars = reinterpret_cast<uint64_t*>(dsm + (MODE == 0 ? 2 * B2 * DW : 0));
+    const int tiles_per_rhs = N1 / TB;
+    const C2<T>* src = (MODE == 0) ? A.grid : A.ybuf;
+    const int64_t src_stride = (MODE == 0) ? A.GS : A.N;
+    if (threadIdx.x == 0) {
+        if (MODE == 0) prefetch_tmap(&dmap);
+        mbar_init(&bars[0], 1);
+        mbar_init(&bars[1], 1);
+        fence_barrier_init();
+    }
+    for (int i = threadIdx.x; i < L / kRB; i += blockDim.x) tws[i] = A.tw2[i];
+    __syncthreads();
+    auto issue = [&](int id) {
+        const int64_t r = id / tiles_per_rhs;
+        const int row0 = (id % tiles_per_rhs) * TB;
+        mbar_arrive_expect_tx(&bars[0], (uint32_t)(sizeof(C2<T>) * L * TB));
+        for (int f = 0; f < TB; ++f)
+            bulk_g2s(buf + f * S, src + r * src_stride + (int64_t)(row0 + f) * L, (uint32_t)(sizeof(C2<T>) * L),
+                     &bars[0]);
+    };
+    int it = 0;
+    if (threadIdx.x == 0 && (int)blockIdx.x < ntiles) issue(blockIdx.x);
+    for (int id = blockIdx.x; id < ntiles; id += gridDim.x, ++it) {
+        const int64_t r = id / tiles_per_rhs;
+        const int row0 = (id % tiles_per_rhs) * TB;
+        if (MODE == 0 && threadIdx.x == 0) {  // this tile's d factors (the previous tile is done)
+            const int dc0 = row0 & ~(DW - 1);
+            mbar_arrive_expect_tx(&bars[1], (uint32_t)(sizeof(T) * DW * 2 * B2));
+            for (int q = 0; q < B2; q += BRd) {
+                tma_load_3d(dsm + q * DW, &dmap, dc0, B2 + q, 0, &bars[1]);
+                tma_load_3d(dsm + (B2 + q) * DW, &dmap, dc0, q, 0, &bars[1]);
+            }
+        }
+        mbar_wait(&bars[0], it & 1);
+        C2<T>* grow = A.grid + r * A.GS;
+        C2<T>* frow = A.fhat + r * A.M;
+        auto load = [&](int f, int n2, int, int) -> C2<T> { return buf[f * S + n2]; };
+        constexpr int NsL = L / kRB;
+        const bool fastband = (B2 % NsL) == 0;
+        const int mlo = B2 / NsL;
+        const int jl = threadIdx.x / TB, fl = threadIdx.x - (threadIdx.x / TB) * TB;
+        const int doff = (row0 & (DW - 1)) + fl;
+        auto store = [&](int f, int k2, C2<T> v, int m) {
+            const int64_t k = (int64_t)(row0 + f) + (int64_t)N1 * k2;
+            if (MODE == 0) {
+                if (m == 0) mbar_wait(&bars[1], it & 1);
+                int sr;
+                if (fastband) {
+                    if (m < mlo)
+                        sr = jl + m * NsL;
+                    else if (m >= kRB - mlo)
+                        sr = jl + m * NsL - (L - 2 * B2);
+                    else
+                        return;
+                } else if (k2 < B2) {
+                    sr = k2;
+                } else if (k2 >= L - B2) {
+                    sr = k2 - (L - 2 * B2);
+                } else {
+                    return;
+                }
+                const T d = dsm[sr * DW + doff];
+                const int64_t c = (int64_t)(sr < B2 ? sr + B2 : sr - B2) * N1 + row0 + f;
+                frow[c] = mk<T>(d * v.x, d * v.y);
+            } else {
+                grow[k] = v;
+                if (k < A.H) grow[A.N + k] = v;  // the gather's halo copy of the first cells
+            }
+        };
+        const int nxt = id + (int)gridDim.x;
+        auto on_free = [&]() {
+            if (threadIdx.x == 0 && nxt < ntiles) issue(nxt);
+        };
+        fft_stages_ip<T, SIGN, G, 0, 1>(tws, buf, load, store, on_free);
+        if (MODE == 0) __syncthreads();  // every d read of this tile before the next tile's d copy
+    }
+}
+
 }  // namespace fft
 
 // =========================================================================== host
@@ -1000,6 +1096,37 @@ static void launch_pass_b(Plan& p, fft::Args<T>& A, int mode, int64_t R, cudaStr
         throw Fail{INFT_ERR_CUDA};
     }
     const int ntiles = (int)(R * (A.N1 / TB));
+    // in-place pass B for the inverse (MODE 0: plain stores of the kept half; two CTAs per SM,
+    // complex128) unless INFT_FFT_IP_B=0.  Config 5: 0.854 -> 0.766 ms.  MODE 1 writes the whole
+    // grid + halo and keeps the staged TMA stores of k_pass_b (in place with plain stores:
+    // 0.885 -> 0.917 ms).
+    static const bool ipb = [] {
+        const char* e = getenv("INFT_FFT_IP_B");
+        return !(e && atoi(e) == 0);
+    }();
+    if (ipb && sizeof(T) == 8 && mode == 0) {
+        PassBFn<T> kf = nullptr;
+        switch (L) {
+            case 512: kf = mode == 0 ? fft::k_pass_b_ip<T, -1, 0, 512> : fft::k_pass_b_ip<T, 1, 1, 512>; break;
+            case 1024: kf = mode == 0 ? fft::k_pass_b_ip<T, -1, 0, 1024> : fft::k_pass_b_ip<T, 1, 1, 1024>; break;
+            case 2048: kf = mode == 0 ? fft::k_pass_b_ip<T, -1, 0, 2048> : fft::k_pass_b_ip<T, 1, 1, 2048>; break;
+            case 4096: kf = mode == 0 ? fft::k_pass_b_ip<T, -1, 0, 4096> : fft::k_pass_b_ip<T, 1, 1, 4096>; break;
+            default: break;
+        }
+        if (kf) {
+            const size_t head = (cs * (size_t)(std::max(ST * TB, SW * TB) + L / fft::kRB) + 127) / 128 * 128;
+            const size_t smem_ip = head + (mode == 0 ? sizeof(T) * (size_t)(2 * B2 * DW) : 0) + 32;
+            if (smem_ip <= 227 * 1024) {
+                ensure_smem_attr((const void*)kf, smem_ip);
+                const int occ = occupancy_cached((const void*)kf, threads, smem_ip);
+                kf<<<(unsigned)std::min(ntiles, num_sms() * std::max(1, occ)), threads, smem_ip, st>>>(
+                    dmap, omap, A, BRd, BRo, ntiles);
+                INFT_CHECK_LAUNCH();
+                p.launches++;
+                return;
+            }
+        }
+    }
     ensure_smem_attr((const void*)kb, smem);
     const int occ = occupancy_cached((const void*)kb, threads, smem);
     kb<<<(unsigned)std::min(ntiles, num_sms() * std::max(1, occ)), threads, smem, st>>>(dmap, omap, A, BRd, BRo,
