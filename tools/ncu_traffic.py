@@ -14,10 +14,10 @@ import sys
 # kernel-name pattern -> bench stage (fused 1-D path, see include/inft.h stage list)
 STAGES = [
     (r"k_spread", "spread"),
-    (r"k_pass_a<(double|float), \(int\)-1, 0,", "fft_forward"),
-    (r"k_pass_b<(double|float), \(int\)-1, 0,", "trunc_deconv"),
-    (r"k_pass_a<(double|float), 1, 1,", "deconv_pad"),
-    (r"k_pass_b<(double|float), 1, 1,", "fft_inverse"),
+    (r"k_pass_a(_ip)?<(double|float), \(int\)-1, 0,", "fft_forward"),
+    (r"k_pass_b(_ip)?<(double|float), \(int\)-1, 0,", "trunc_deconv"),
+    (r"k_pass_a(_ip)?<(double|float), 1, 1,", "deconv_pad"),
+    (r"k_pass_b(_ip)?<(double|float), 1, 1,", "fft_inverse"),
     (r"k_gather", "gather"),
 ]
 
