@@ -789,17 +789,32 @@ __global__ void __launch_bounds__(Geo<T, L>::NT, 2)
                 const int64_t c = (int64_t)(sr < B2 ? sr + B2 : sr - B2) * N1 + row0 + f;
                 frow[c] = mk<T>(d * v.x, d * v.y);
             } else {
-                grow[k] = v;
-                if (k < A.H) grow[A.N + k] = v;  // the gather's halo copy of the first cells
+                // staged in the buffer the last stage has just read, [k2][TB], left by TMA store
+                // boxes below; the halo copy of the first cells goes straight out
+                buf[k2 * TB + f] = v;
+                if (k < A.H) grow[A.N + k] = v;
             }
         };
         const int nxt = id + (int)gridDim.x;
         auto on_free = [&]() {
-            if (threadIdx.x == 0 && nxt < ntiles) issue(nxt);
+            if (MODE == 0 && threadIdx.x == 0 && nxt < ntiles) issue(nxt);
         };
         fft_stages_ip<T, SIGN, G, 0, 1>(tws, buf, load, store, on_free);
-        if (MODE == 0) __syncthreads();  // every d read of this tile before the next tile's d copy
+        if (MODE == 0) {
+            __syncthreads();  // every d read of this tile before the next tile's d copy
+        } else {
+            fence_proxy_async();  // staged outputs before the TMA store
+            __syncthreads();
+            if (threadIdx.x == 0) {
+                for (int q = 0; q < L; q += BRo) tma_store_3d(&omap, row0 * (int)(sizeof(C2<T>) / 8), q, (int)r,
+                                                              buf + q * TB);
+                bulk_commit();
+                bulk_wait_read<0>();  // the store has read the buffer: the next tile may land
+                if (nxt < ntiles) issue(nxt);
+            }
+        }
     }
+    if (MODE == 1 && threadIdx.x == 0) bulk_wait<0>();
 }
 
 }  // namespace fft
@@ -1104,7 +1119,11 @@ static void launch_pass_b(Plan& p, fft::Args<T>& A, int mode, int64_t R, cudaStr
         const char* e = getenv("INFT_FFT_IP_B");
         return !(e && atoi(e) == 0);
     }();
-    if (ipb && sizeof(T) == 8 && mode == 0) {
+    static const bool ipb1 = [] {
+        const char* e = getenv("INFT_FFT_IP_B1");
+        return e && atoi(e);
+    }();
+    if (ipb && sizeof(T) == 8 && (mode == 0 || ipb1)) {
         PassBFn<T> kf = nullptr;
         switch (L) {
             case 512: kf = mode == 0 ? fft::k_pass_b_ip<T, -1, 0, 512> : fft::k_pass_b_ip<T, 1, 1, 512>; break;
