@@ -208,15 +208,18 @@ constexpr int kTileElems = INFT_FFT_TILE;
 #define INFT_FFT_TILE_F 8192
 #endif
 constexpr int kTileElemsF = INFT_FFT_TILE_F;
+// in-place kernels: 4096-element tiles at both precisions (256 threads, <= 128 registers at two
+// CTAs per SM; complex64's 8192-element tiles would need 512 threads at 64 registers)
+constexpr int kTileIP = 4096;
 template <typename T>
 constexpr int tile_elems() { return sizeof(T) == 8 ? kTileElems : kTileElemsF; }
 constexpr int kLgRB = kRB == 16 ? 4 : (kRB == 8 ? 3 : 2);
 // TF independent length-L transforms per tile (compile-time: ~64 KB of shared memory, at
 // most 256 threads = TF L / 16, at most 8), thread t -> (f = t % TF, butterfly j = t / TF).
 // Static radix plan for L = 2^K: a first stage of radix 2^(K mod 4) (if any), then radix-16.
-template <typename T, int L>
+template <typename T, int L, int TE_ = 0>
 struct Geo {
-    static constexpr int TE = tile_elems<T>();
+    static constexpr int TE = TE_ > 0 ? TE_ : tile_elems<T>();
     static constexpr int TF = L >= TE / 8 ? (TE / L > 0 ? TE / L : 1) : 8;
     static constexpr int NT = TF * L / kRB < 32 ? 32 : TF * L / kRB;  // threads per CTA
     // row padding of the [f][L + PAD] layout: the lanes of one 128-byte shared wavefront cover
@@ -486,12 +489,12 @@ __global__ void __launch_bounds__(Geo<T, L>::NT, 1)
 // of max(L TA, SW TA) elements per CTA, two CTAs per SM (config 5 pass A MODE 0: 0.886 ->
 // 0.826 ms against the double-buffered one-CTA kernel).
 template <typename T, int SIGN, int MODE, int L>
-__global__ void __launch_bounds__(Geo<T, L>::NT, 2)
+__global__ void __launch_bounds__(Geo<T, L, kTileIP>::NT, 2)
     k_pass_a_ip(const __grid_constant__ CUtensorMap map, const __grid_constant__ CUtensorMap dmap, Args<T> A, int BR,
                 int ntiles) {
     extern __shared__ __align__(128) unsigned char smraw[];
     constexpr int CE = (int)(sizeof(C2<T>) / 8);
-    using G = Geo<T, L>;
+    using G = Geo<T, L, kTileIP>;
     constexpr int TA = G::TF, S = G::SW;
     constexpr int BUF = (L * TA > S * TA ? L * TA : S * TA);
     C2<T>* buf = reinterpret_cast<C2<T>*>(smraw);
@@ -710,11 +713,11 @@ __global__ void __launch_bounds__(Geo<T, L>::NT, 1)
 // buffer (MODE 0), two CTAs per SM, plain stores from registers (the staged TMA stores of
 // k_pass_b would hold the buffer the next tile lands in).
 template <typename T, int SIGN, int MODE, int L>
-__global__ void __launch_bounds__(Geo<T, L>::NT, 2)
+__global__ void __launch_bounds__(Geo<T, L, kTileIP>::NT, 2)
     k_pass_b_ip(const __grid_constant__ CUtensorMap dmap, const __grid_constant__ CUtensorMap omap, Args<T> A,
                 int BRd, int BRo, int ntiles) {
     extern __shared__ __align__(128) unsigned char smraw[];
-    using G = Geo<T, L>;
+    using G = Geo<T, L, kTileIP>;
     constexpr int TB = G::TF, S = G::ST, SW = G::SW;
     constexpr int BUF = (S * TB > SW * TB ? S * TB : SW * TB);
     constexpr int DW = (int)(16 / sizeof(T)) > TB ? (int)(16 / sizeof(T)) : TB;
@@ -1002,6 +1005,25 @@ static size_t pass_b_smem(int L, int N1, int64_t M, int mode) {
     return fft::d_offset<T>(L, ST, SW, TB) + (mode == 0 ? sizeof(T) * (size_t)(2 * B2 * DW) : 0) + 32;
 }
 
+// in-place kernels and their geometry (Geo<T, L, kTileIP>) for the supported lengths
+template <typename T>
+static bool pick_ip(int mode, int L, bool pass_a, PassAFn<T>& a, PassBFn<T>& b, int& TF, int& ST, int& SW, int& NT) {
+#define INFT_IPG(LL)                                                                                          \
+    TF = fft::Geo<T, LL, fft::kTileIP>::TF, ST = fft::Geo<T, LL, fft::kTileIP>::ST,                           \
+    SW = fft::Geo<T, LL, fft::kTileIP>::SW, NT = fft::Geo<T, LL, fft::kTileIP>::NT;                           \
+    if (pass_a) a = mode == 0 ? fft::k_pass_a_ip<T, -1, 0, LL> : fft::k_pass_a_ip<T, 1, 1, LL>;                \
+    else b = mode == 0 ? fft::k_pass_b_ip<T, -1, 0, LL> : fft::k_pass_b_ip<T, 1, 1, LL>;                        \
+    return true;
+    switch (L) {
+        case 512: { INFT_IPG(512) }
+        case 1024: { INFT_IPG(1024) }
+        case 2048: { INFT_IPG(2048) }
+        case 4096: { INFT_IPG(4096) }
+        default: return false;
+    }
+#undef INFT_IPG
+}
+
 // pass A over `src` (MODE 0: the grid, rows GS; MODE 1: h, rows M)
 template <typename T>
 static void launch_pass_a(Plan& p, fft::Args<T>& A, int mode, const void* src, int64_t R, cudaStream_t st) {
@@ -1014,6 +1036,23 @@ static void launch_pass_a(Plan& p, fft::Args<T>& A, int mode, const void* src, i
     if (!pick_kernels<T>(mode, L, ka, kb, TA, ST, SW, threads)) {
         set_error("fused FFT: unsupported factor length");
         throw Fail{INFT_ERR_UNSUPPORTED};
+    }
+    // in-place pass A (two CTAs per SM) unless INFT_FFT_IP=0: its own tile geometry
+    static const bool ip = [] {
+        const char* e = getenv("INFT_FFT_IP");
+        return !(e && atoi(e) == 0);
+    }();
+    PassAFn<T> kip = nullptr;
+    PassBFn<T> kunused = nullptr;
+    // complex128 only: complex64's double-buffered 8192-element tiles are faster (config 5 c64
+    // 3.06 ms/step against 3.21 in place with 4096-element tiles)
+    if (ip && sizeof(T) == 8) {
+        int tf, st_, sw, nt;
+        if (pick_ip<T>(mode, L, true, kip, kunused, tf, st_, sw, nt)) {
+            TA = tf, ST = st_, SW = sw, threads = nt;
+        } else {
+            kip = nullptr;
+        }
     }
     CUtensorMap map, dmap;
     int BR;
@@ -1038,29 +1077,15 @@ static void launch_pass_a(Plan& p, fft::Args<T>& A, int mode, const void* src, i
         throw Fail{INFT_ERR_CUDA};
     }
     const int ntiles = (int)(R * (A.N2 / TA));
-    // in-place pass A (two CTAs per SM) unless INFT_FFT_IP=0
-    static const bool ip = [] {
-        const char* e = getenv("INFT_FFT_IP");
-        return !(e && atoi(e) == 0);
-    }();
-    if (ip && sizeof(T) == 8) {  // complex64 (512-thread tiles) would spill at 64 registers
-        PassAFn<T> kf = nullptr;
-        switch (L) {
-            case 512: kf = mode == 0 ? fft::k_pass_a_ip<T, -1, 0, 512> : fft::k_pass_a_ip<T, 1, 1, 512>; break;
-            case 1024: kf = mode == 0 ? fft::k_pass_a_ip<T, -1, 0, 1024> : fft::k_pass_a_ip<T, 1, 1, 1024>; break;
-            case 2048: kf = mode == 0 ? fft::k_pass_a_ip<T, -1, 0, 2048> : fft::k_pass_a_ip<T, 1, 1, 2048>; break;
-            default: break;
-        }
-        if (kf) {
-            const size_t smem_ip = cs * (size_t)(std::max(L * TA, SW * TA) + L / fft::kRB) + 16;
-            ensure_smem_attr((const void*)kf, smem_ip);
-            const int occ = occupancy_cached((const void*)kf, threads, smem_ip);
-            kf<<<(unsigned)std::min(ntiles, num_sms() * std::max(1, occ)), threads, smem_ip, st>>>(map, dmap, A, BR,
-                                                                                                    ntiles);
-            INFT_CHECK_LAUNCH();
-            p.launches++;
-            return;
-        }
+    if (kip) {
+        const size_t smem_ip = cs * (size_t)(std::max(L * TA, SW * TA) + L / fft::kRB) + 16;
+        ensure_smem_attr((const void*)kip, smem_ip);
+        const int occ = occupancy_cached((const void*)kip, threads, smem_ip);
+        kip<<<(unsigned)std::min(ntiles, num_sms() * std::max(1, occ)), threads, smem_ip, st>>>(map, dmap, A, BR,
+                                                                                                 ntiles);
+        INFT_CHECK_LAUNCH();
+        p.launches++;
+        return;
     }
     const size_t smem = cs * (size_t)(2 * L * TA + SW * TA + L / fft::kRB) + 16;
     ensure_smem_attr((const void*)ka, smem);
@@ -1080,6 +1105,28 @@ static void launch_pass_b(Plan& p, fft::Args<T>& A, int mode, int64_t R, cudaStr
     if (!pick_kernels<T>(mode, L, ka, kb, TB, ST, SW, threads)) {
         set_error("fused FFT: unsupported factor length");
         throw Fail{INFT_ERR_UNSUPPORTED};
+    }
+    // in-place pass B for the inverse (MODE 0: plain stores of the kept half; two CTAs per SM)
+    // unless INFT_FFT_IP_B=0.  Config 5: 0.854 -> 0.766 ms.  MODE 1 writes the whole grid + halo
+    // and keeps the staged TMA stores of k_pass_b (in place with plain stores: 0.885 -> 0.917
+    // ms; with staged stores, INFT_FFT_IP_B1=1: 1.00 ms).
+    static const bool ipb = [] {
+        const char* e = getenv("INFT_FFT_IP_B");
+        return !(e && atoi(e) == 0);
+    }();
+    static const bool ipb1 = [] {
+        const char* e = getenv("INFT_FFT_IP_B1");
+        return e && atoi(e);
+    }();
+    PassBFn<T> kip = nullptr;
+    if (ipb && sizeof(T) == 8 && (mode == 0 || ipb1)) {
+        PassAFn<T> unused = nullptr;
+        int tf, st_, sw, nt;
+        if (pick_ip<T>(mode, L, false, unused, kip, tf, st_, sw, nt)) {
+            TB = tf, ST = st_, SW = sw, threads = nt;
+        } else {
+            kip = nullptr;
+        }
     }
     const int B2 = (int)(A.M / 2 / A.N1);
     const int DW = std::max<int>(TB, (int)(16 / sizeof(T)));
@@ -1111,40 +1158,16 @@ static void launch_pass_b(Plan& p, fft::Args<T>& A, int mode, int64_t R, cudaStr
         throw Fail{INFT_ERR_CUDA};
     }
     const int ntiles = (int)(R * (A.N1 / TB));
-    // in-place pass B for the inverse (MODE 0: plain stores of the kept half; two CTAs per SM,
-    // complex128) unless INFT_FFT_IP_B=0.  Config 5: 0.854 -> 0.766 ms.  MODE 1 writes the whole
-    // grid + halo and keeps the staged TMA stores of k_pass_b (in place with plain stores:
-    // 0.885 -> 0.917 ms).
-    static const bool ipb = [] {
-        const char* e = getenv("INFT_FFT_IP_B");
-        return !(e && atoi(e) == 0);
-    }();
-    static const bool ipb1 = [] {
-        const char* e = getenv("INFT_FFT_IP_B1");
-        return e && atoi(e);
-    }();
-    if (ipb && sizeof(T) == 8 && (mode == 0 || ipb1)) {
-        PassBFn<T> kf = nullptr;
-        switch (L) {
-            case 512: kf = mode == 0 ? fft::k_pass_b_ip<T, -1, 0, 512> : fft::k_pass_b_ip<T, 1, 1, 512>; break;
-            case 1024: kf = mode == 0 ? fft::k_pass_b_ip<T, -1, 0, 1024> : fft::k_pass_b_ip<T, 1, 1, 1024>; break;
-            case 2048: kf = mode == 0 ? fft::k_pass_b_ip<T, -1, 0, 2048> : fft::k_pass_b_ip<T, 1, 1, 2048>; break;
-            case 4096: kf = mode == 0 ? fft::k_pass_b_ip<T, -1, 0, 4096> : fft::k_pass_b_ip<T, 1, 1, 4096>; break;
-            default: break;
-        }
-        if (kf) {
-            const size_t head = (cs * (size_t)(std::max(ST * TB, SW * TB) + L / fft::kRB) + 127) / 128 * 128;
-            const size_t smem_ip = head + (mode == 0 ? sizeof(T) * (size_t)(2 * B2 * DW) : 0) + 32;
-            if (smem_ip <= 227 * 1024) {
-                ensure_smem_attr((const void*)kf, smem_ip);
-                const int occ = occupancy_cached((const void*)kf, threads, smem_ip);
-                kf<<<(unsigned)std::min(ntiles, num_sms() * std::max(1, occ)), threads, smem_ip, st>>>(
-                    dmap, omap, A, BRd, BRo, ntiles);
-                INFT_CHECK_LAUNCH();
-                p.launches++;
-                return;
-            }
-        }
+    if (kip) {
+        const size_t head = (cs * (size_t)(std::max(ST * TB, SW * TB) + L / fft::kRB) + 127) / 128 * 128;
+        const size_t smem_ip = head + (mode == 0 ? sizeof(T) * (size_t)(2 * B2 * DW) : 0) + 32;
+        ensure_smem_attr((const void*)kip, smem_ip);  // <= ~150 KB for L <= 4096
+        const int occ = occupancy_cached((const void*)kip, threads, smem_ip);
+        kip<<<(unsigned)std::min(ntiles, num_sms() * std::max(1, occ)), threads, smem_ip, st>>>(dmap, omap, A, BRd,
+                                                                                                 BRo, ntiles);
+        INFT_CHECK_LAUNCH();
+        p.launches++;
+        return;
     }
     ensure_smem_attr((const void*)kb, smem);
     const int occ = occupancy_cached((const void*)kb, threads, smem);
