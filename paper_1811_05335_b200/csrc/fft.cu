@@ -1015,6 +1015,8 @@ static bool pick_ip(int mode, int L, bool pass_a, PassAFn<T>& a, PassBFn<T>& b, 
     else b = mode == 0 ? fft::k_pass_b_ip<T, -1, 0, LL> : fft::k_pass_b_ip<T, 1, 1, LL>;                        \
     return true;
     switch (L) {
+        case 128: { INFT_IPG(128) }
+        case 256: { INFT_IPG(256) }
         case 512: { INFT_IPG(512) }
         case 1024: { INFT_IPG(1024) }
         case 2048: { INFT_IPG(2048) }
