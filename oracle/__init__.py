@@ -641,6 +641,8 @@ def _clib():
             fn.argtypes = [I64, P, P, P, P, P, P, P, P, P, P, I64, ctypes.c_int]
             fn.restype = ctypes.c_int
         lib.oracle_dft.argtypes = [P, I64, ctypes.c_int]
+        lib.oracle_trig_sum.argtypes = [I64, I64, P, I64, P, P, ctypes.c_int]
+        lib.oracle_trig_sum.restype = ctypes.c_int
         lib.oracle_num_threads.restype = ctypes.c_int
         _lib = lib
     return _lib
@@ -659,6 +661,43 @@ def dft(x, sign):
     a = np.ascontiguousarray(np.asarray(x, dtype=np.complex128).copy())
     _clib().oracle_dft(_ptr(a), a.size, int(sign))
     return a
+
+
+def trig_sum(c, x, nthreads=0):
+    """out[r][i] = sum_{k=-M/2}^{M/2-1} c[r][k + M/2] e^{2 pi i k x_i}: the plain direct sum in C
+    (oracle_trig_sum; angle-addition steps restarted from an exactly reduced phase every 32
+    terms).  c [M] or [R][M] complex; returns [n] or [R][n]."""
+    c = np.asarray(c, dtype=np.complex128)
+    one = c.ndim == 1
+    c = np.ascontiguousarray(np.atleast_2d(c))
+    R, M = c.shape
+    xs = np.ascontiguousarray(np.asarray(x, dtype=np.float64).ravel())
+    out = np.zeros((R, xs.size), dtype=np.complex128)
+    if xs.size and R:
+        _clib().oracle_trig_sum(M, R, _ptr(c), xs.size, _ptr(xs), _ptr(out), nthreads)
+    shape = np.asarray(x).shape
+    return out[0].reshape(shape) if one else out.reshape((R,) + shape)
+
+
+def G_kernel_c(dx, M, sigma, m, window="kb"):
+    """G(x) of G_kernel by the C direct sum (same sum, for large test samples)."""
+    Ms = msigma(M, sigma)
+    c = (1.0 / window_hat_vector(M, sigma, m) ** 2 / Ms if window == "kb"
+         else inv_what_vector(M, sigma, m, window) ** 2 / Ms)
+    return trig_sum(c, dx)
+
+
+def Kplus_kernel_c(dx, M, sigma, m, window="kb"):
+    """K+(x) of Kplus_kernel by the C direct sum."""
+    Ms = msigma(M, sigma)
+    c = (1.0 / window_hat_vector(M, sigma, m) / Ms if window == "kb"
+         else inv_what_vector(M, sigma, m, window) / Ms)
+    return trig_sum(c, dx)
+
+
+def ndft_c(x, fhat, M):
+    """f = A fhat (eq. nfft) by the C direct sum; 1-D, fhat [R][M] centered."""
+    return trig_sum(np.atleast_2d(fhat), x)
 
 
 def _split_w(w):

@@ -326,3 +326,95 @@ int oracle_dft(double* x, int64_t n, int sign) {
     free(scratch);
     return 0;
 }
+
+/* ------------------------------------------------------ trigonometric sums ---- */
+
+/* e^{2 pi i k x} from the exactly reduced phase frac(k x): the product k x is split into
+ * p + e by one fma (two-product), so |k| up to 2^21 keeps ~1e-16 phase accuracy. */
+static void unit_phase(double k, double x, double* c, double* s) {
+    double p = k * x;
+    double e = fma(k, x, -p);
+    double fr = p - floor(p);
+    fr += e;
+    fr -= floor(fr);
+    *c = cos(TWO_PI * fr);
+    *s = sin(TWO_PI * fr);
+}
+
+/* out[r][i] = sum_{k=-M/2}^{M/2-1} c[r][k + M/2] e^{2 pi i k x_i}, r < R, i < n (direct sum;
+ * c and out interleaved complex).  Used for the kernels G(x), K+(x) of the Gram form of
+ * Alg. "Fast optimization of the matrix B" (coefficients 1/(M_sigma what(k)^2), 1/(M_sigma
+ * what(k)); reading A6) and for the NDFT f = A fhat (eq. nfft).
+ * e^{2 pi i k x} is stepped by the angle-addition recurrence z_{k+1} = z_k e^{2 pi i x} and
+ * restarted from unit_phase() every 32 terms (<= 32 roundings between restarts). */
+/* One coefficient vector, eight x at a time (eight independent recurrences). */
+static void trig_sum_x8(int64_t M, const double* c, const double* x, int nb, double* out) {
+    enum { BLK = 32, XB = 8 };
+    double sc[XB], ss[XB], zr[XB], zi[XB], ar[XB], ai[XB];
+    for (int b = 0; b < XB; b++) {
+        unit_phase(1.0, x[b < nb ? b : 0], &sc[b], &ss[b]);
+        ar[b] = ai[b] = 0.0;
+    }
+    for (int64_t k0 = -M / 2; k0 < M / 2; k0 += BLK) {
+        for (int b = 0; b < XB; b++) unit_phase((double)k0, x[b < nb ? b : 0], &zr[b], &zi[b]);
+        const int64_t k1 = k0 + BLK < M / 2 ? k0 + BLK : M / 2;
+        for (int64_t k = k0; k < k1; k++) {
+            const double cr = c[2 * (k + M / 2)], ci = c[2 * (k + M / 2) + 1];
+            for (int b = 0; b < XB; b++) {
+                ar[b] += cr * zr[b] - ci * zi[b];
+                ai[b] += cr * zi[b] + ci * zr[b];
+                const double t = zr[b] * sc[b] - zi[b] * ss[b];
+                zi[b] = zr[b] * ss[b] + zi[b] * sc[b];
+                zr[b] = t;
+            }
+        }
+    }
+    for (int b = 0; b < nb; b++) {
+        out[2 * b] = ar[b];
+        out[2 * b + 1] = ai[b];
+    }
+}
+
+int oracle_trig_sum(int64_t M, int64_t R, const double* c, int64_t n, const double* x, double* out,
+                    int nthreads) {
+    enum { BLK = 32 };
+    if (R == 1) {
+#ifdef _OPENMP
+        if (nthreads > 0) omp_set_num_threads(nthreads);
+#pragma omp parallel for schedule(dynamic, 4)
+#endif
+        for (int64_t i = 0; i < n; i += 8) trig_sum_x8(M, c, x + i, (int)(n - i < 8 ? n - i : 8), out + 2 * i);
+        return 0;
+    }
+#ifdef _OPENMP
+    if (nthreads > 0) omp_set_num_threads(nthreads);
+#pragma omp parallel for schedule(dynamic, 16)
+#endif
+    for (int64_t i = 0; i < n; i++) {
+        double sc, ss;
+        unit_phase(1.0, x[i], &sc, &ss);
+        double* acc = (double*)calloc((size_t)(2 * (R > 0 ? R : 1)), sizeof(double));
+        for (int64_t k0 = -M / 2; k0 < M / 2; k0 += BLK) {
+            double zr, zi;
+            unit_phase((double)k0, x[i], &zr, &zi);
+            const int64_t k1 = k0 + BLK < M / 2 ? k0 + BLK : M / 2;
+            for (int64_t k = k0; k < k1; k++) {
+                const double* ck = c + 2 * (k + M / 2);
+                for (int64_t r = 0; r < R; r++) {
+                    const double cr = ck[2 * r * M], ci = ck[2 * r * M + 1];
+                    acc[2 * r] += cr * zr - ci * zi;
+                    acc[2 * r + 1] += cr * zi + ci * zr;
+                }
+                const double t = zr * sc - zi * ss;
+                zi = zr * ss + zi * sc;
+                zr = t;
+            }
+        }
+        for (int64_t r = 0; r < R; r++) {
+            out[2 * (r * n + i)] = acc[2 * r];
+            out[2 * (r * n + i) + 1] = acc[2 * r + 1];
+        }
+        free(acc);
+    }
+    return 0;
+}

@@ -126,6 +126,15 @@ def _stream_ptr(stream):
     return int(stream)
 
 
+def _check_nodes_shape(nd, d):
+    """Nodes are float64 [N] (1-D) or [N][2] (2-D); the C side reads N*d doubles."""
+    ok = (nd.ndim == 1) if d == 1 else (nd.ndim == 2 and nd.shape[1] == d)
+    if d == 1 and nd.ndim == 2 and nd.shape[1] == 1:
+        ok = True
+    if not ok:
+        raise ValueError(f"nodes: shape {tuple(nd.shape)}, expected [N]" + ("" if d == 1 else f"[{d}]"))
+
+
 class Plan:
     """A plan for fixed nodes: nodes [N] or [N][2] float64 in [-1/2, 1/2)."""
 
@@ -134,16 +143,16 @@ class Plan:
             M = (M,)
         self.d = len(M)
         self.M = tuple(int(v) for v in M)
-        nodes_np = None
         if hasattr(nodes, "data_ptr"):
-            nd = nodes.contiguous()
+            import torch
+            nd = nodes.to(torch.float64).contiguous()
             self._nodes_ref = nd
-            N = nd.shape[0]
-            nptr = nd.data_ptr()
         else:
-            nodes_np = np.ascontiguousarray(np.asarray(nodes, dtype=np.float64))
-            N = nodes_np.shape[0]
-            nptr = nodes_np.ctypes.data if N > 0 else None
+            nd = np.ascontiguousarray(np.asarray(nodes, dtype=np.float64))
+            self._nodes_ref = nd
+        _check_nodes_shape(nd, self.d)
+        N = nd.shape[0]
+        nptr = (nd.data_ptr() if hasattr(nd, "data_ptr") else nd.ctypes.data) if N > 0 else None
         self.N = int(N)
         self.prec = INFT_C128 if precision in ("c128", INFT_C128) else INFT_C64
         Marr = (ctypes.c_int64 * self.d)(*self.M)
@@ -242,19 +251,41 @@ class Plan:
             return torch.empty(shape, dtype=dt, device=like.device, pin_memory=False)
         return np.empty(shape, dtype=np.complex128 if self.prec == INFT_C128 else np.complex64)
 
+    def _dtype_ok(self, a):
+        want = "complex128" if self.prec == INFT_C128 else "complex64"
+        return str(a.dtype).replace("torch.", "") == want
+
+    def _check_buf(self, a, width, what, R=None):
+        """dtype = the plan's precision, trailing size = width, [R][width] or [width], and
+        CUDA tensors on the plan's device: the C side trusts these sizes."""
+        if not self._dtype_ok(a):
+            raise TypeError(f"{what}: dtype {a.dtype} does not match the plan's precision "
+                            f"({'complex128' if self.prec == INFT_C128 else 'complex64'})")
+        if a.ndim not in (1, 2) or a.shape[-1] != width:
+            raise ValueError(f"{what}: shape {tuple(a.shape)}, expected [R][{width}]")
+        if R is not None and (a.shape[0] if a.ndim == 2 else 1) != R:
+            raise ValueError(f"{what}: {a.shape[0] if a.ndim == 2 else 1} rows, expected {R}")
+        dev = getattr(a, "device", None)
+        if getattr(dev, "type", None) == "cuda" and dev.index != self.device:
+            raise ValueError(f"{what}: tensor on {dev}, the plan on cuda:{self.device}")
+
     def apply(self, f, out=None, stream=None):
         """Inverse NFFT (problem (1)): fhat = s D^* F^* B_opt^* f; f [R][N] -> [R][prod M]."""
+        self._check_buf(f, self.N, "apply input f")
         R = f.shape[0] if f.ndim == 2 else 1
         if out is None:
             out = self._out(f, (R, self.Mtot))
+        self._check_buf(out, self.Mtot, "apply output fhat", R)
         _check(inft_apply(self._h, _ptr(f), _ptr(out), R, _stream_ptr(stream)), "inft_apply")
         return out
 
     def adjoint_apply(self, h, out=None, stream=None):
         """Inverse adjoint NFFT (problem (2)): f = s B_opt F D h; h [R][prod M] -> [R][N]."""
+        self._check_buf(h, self.Mtot, "adjoint_apply input h")
         R = h.shape[0] if h.ndim == 2 else 1
         if out is None:
             out = self._out(h, (R, self.N))
+        self._check_buf(out, self.N, "adjoint_apply output f", R)
         _check(inft_adjoint_apply(self._h, _ptr(h), _ptr(out), R, _stream_ptr(stream)), "inft_adjoint_apply")
         return out
 
@@ -265,12 +296,14 @@ class QuadPlan:
 
     def __init__(self, nodes, delta=0.0, device=0, stream=None):
         if hasattr(nodes, "data_ptr"):
-            nd = nodes.contiguous()
-            self._nodes_ref = nd
+            import torch
+            nd = nodes.to(torch.float64).contiguous()
             N, nptr = nd.shape[0], nd.data_ptr()
         else:
             nd = np.ascontiguousarray(np.asarray(nodes, dtype=np.float64))
             N, nptr = nd.shape[0], nd.ctypes.data
+        _check_nodes_shape(nd, 1)
+        self._nodes_ref = nd
         self.N = int(N)
         self.device = int(device)
         h = ctypes.c_void_p()
@@ -308,19 +341,34 @@ class QuadPlan:
             return torch.empty(shape, dtype=torch.complex128, device=like.device)
         return np.empty(shape, dtype=np.complex128)
 
+    def _check_buf(self, a, what, R=None):
+        if str(a.dtype).replace("torch.", "") != "complex128":
+            raise TypeError(f"{what}: dtype {a.dtype}, the quadratic case is complex128")
+        if a.ndim not in (1, 2) or a.shape[-1] != self.N:
+            raise ValueError(f"{what}: shape {tuple(a.shape)}, expected [R][{self.N}]")
+        if R is not None and (a.shape[0] if a.ndim == 2 else 1) != R:
+            raise ValueError(f"{what}: row count does not match the input")
+        dev = getattr(a, "device", None)
+        if getattr(dev, "type", None) == "cuda" and dev.index != self.device:
+            raise ValueError(f"{what}: tensor on {dev}, the plan on cuda:{self.device}")
+
     def apply(self, f, out=None, stream=None):
         """Inverse NFFT, quadratic case: f [R][N] -> fhat [R][N] (k = -N/2..N/2-1)."""
+        self._check_buf(f, "quad apply input")
         R = f.shape[0] if f.ndim == 2 else 1
         if out is None:
             out = self._out(f, (R, self.N))
+        self._check_buf(out, "quad apply output", R)
         _check(inft_quad_apply(self._h, _ptr(f), _ptr(out), R, _stream_ptr(stream)), "inft_quad_apply")
         return out
 
     def adjoint_apply(self, h, out=None, stream=None):
         """Inverse adjoint NFFT, quadratic case: h [R][N] -> f [R][N]."""
+        self._check_buf(h, "quad adjoint input")
         R = h.shape[0] if h.ndim == 2 else 1
         if out is None:
             out = self._out(h, (R, self.N))
+        self._check_buf(out, "quad adjoint output", R)
         _check(inft_quad_adjoint_apply(self._h, _ptr(h), _ptr(out), R, _stream_ptr(stream)),
                "inft_quad_adjoint_apply")
         return out

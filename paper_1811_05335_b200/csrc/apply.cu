@@ -1159,13 +1159,25 @@ static void ensure_streams(Plan& p) {
     INFT_CUDA(cudaEventCreateWithFlags(&p.ev_exit, cudaEventDisableTiming));
 }
 
+// Device pointer on the plan's device -> true; host memory -> false; a device pointer on
+// another GPU is an argument error (the kernels would fault with an illegal address).
+static bool plan_device_ptr(const Plan& p, const void* ptr) {
+    const int d = pointer_device(ptr);
+    if (d >= 0 && d != p.device) {
+        set_error("apply: buffer lives on cuda:" + std::to_string(d) + ", the plan on cuda:" +
+                  std::to_string(p.device));
+        throw Fail{INFT_ERR_INVALID_ARG};
+    }
+    return d >= 0;
+}
+
 // Device-resident path: chunks of the grid capacity.  Host path: double-buffered
 // staging; H2D of chunk c+1 (stream s_h2d) and D2H of chunk c-1 (stream s_d2h)
 // overlap the compute of chunk c on the caller's stream.
 static void run(Plan& p, const void* in, size_t in_rhs_bytes, void* out, size_t out_rhs_bytes, int64_t R,
                 cudaStream_t st, ChunkFn fn) {
-    const bool in_dev = in_rhs_bytes == 0 || is_device_pointer(in);
-    const bool out_dev = out_rhs_bytes == 0 || is_device_pointer(out);
+    const bool in_dev = in_rhs_bytes == 0 || plan_device_ptr(p, in);
+    const bool out_dev = out_rhs_bytes == 0 || plan_device_ptr(p, out);
     const char* ib = static_cast<const char*>(in);
     char* ob = static_cast<char*>(out);
     if (in_dev && out_dev) {
@@ -1268,12 +1280,31 @@ static bool graphs_enabled() {
 
 static void run_graphed(Plan& p, int dir, const void* in, size_t in_rhs_bytes, void* out, size_t out_rhs_bytes,
                         int64_t R, cudaStream_t st, ChunkFn fn) {
-    const bool dev = (in_rhs_bytes == 0 || is_device_pointer(in)) && (out_rhs_bytes == 0 || is_device_pointer(out));
+    const bool dev = (in_rhs_bytes == 0 || plan_device_ptr(p, in)) && (out_rhs_bytes == 0 || plan_device_ptr(p, out));
     if (!graphs_enabled() || p.profiling || !dev) {
         run(p, in, in_rhs_bytes, out, out_rhs_bytes, R, st, fn);
         return;
     }
-    Plan::GraphEntry& e = p.graphs[Plan::GraphKey{dir, in, out, R, p.state_version}];
+    // drop graphs captured on an older plan state (stale buffers) and cap the cache: callers
+    // whose buffer addresses rotate would otherwise accumulate one exec per address pair
+    for (auto it = p.graphs.begin(); it != p.graphs.end();) {
+        if (it->first.version < p.state_version) {
+            if (it->second.exec) cudaGraphExecDestroy(it->second.exec);
+            it = p.graphs.erase(it);
+        } else {
+            ++it;
+        }
+    }
+    const Plan::GraphKey key{dir, in, out, R, p.state_version};
+    if (p.graphs.size() >= Plan::kMaxGraphs && !p.graphs.count(key)) {
+        auto lru = p.graphs.begin();
+        for (auto it = p.graphs.begin(); it != p.graphs.end(); ++it)
+            if (it->second.last_use < lru->second.last_use) lru = it;
+        if (lru->second.exec) cudaGraphExecDestroy(lru->second.exec);
+        p.graphs.erase(lru);
+    }
+    Plan::GraphEntry& e = p.graphs[key];
+    e.last_use = ++p.graph_clock;
     if (!e.exec && e.seen++ == 0) {  // first call: plain launches (allocations, one-time tables)
         run(p, in, in_rhs_bytes, out, out_rhs_bytes, R, st, fn);
         return;

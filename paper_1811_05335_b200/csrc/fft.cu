@@ -17,6 +17,8 @@
 #include <algorithm>
 #include <cstdio>
 #include <cstring>
+#include <map>
+#include <mutex>
 #include <vector>
 
 #include "common.cuh"
@@ -842,6 +844,9 @@ struct FftState {
     int64_t y_rhs = 0;
 };
 
+// Per-plan FFT tables; one plan per GPU may be driven from its own host thread, so the map is
+// guarded (the state itself belongs to one plan, which the ABI does not share across threads).
+static std::mutex g_fft_mu;
 static std::map<const Plan*, FftState*>& fft_states() {
     static std::map<const Plan*, FftState*> m;
     return m;
@@ -899,9 +904,14 @@ bool fused_fft_available(const Plan& p) {
 
 template <typename T>
 static FftState& fft_state(Plan& p, cudaStream_t st) {
-    auto& m = fft_states();
-    FftState*& s = m[&p];
-    if (!s) s = new FftState();
+    FftState* sp;
+    {
+        std::lock_guard<std::mutex> g(g_fft_mu);
+        FftState*& slot = fft_states()[&p];
+        if (!slot) slot = new FftState();
+        sp = slot;
+    }
+    FftState* s = sp;
     if (s->ready) return *s;
     const int64_t N = p.Ms[0];
     int lg = 0;
@@ -927,6 +937,7 @@ static FftState& fft_state(Plan& p, cudaStream_t st) {
 }
 
 void release_fft_state(const Plan* p) {
+    std::lock_guard<std::mutex> g(g_fft_mu);
     auto& m = fft_states();
     auto it = m.find(p);
     if (it != m.end()) {

@@ -166,8 +166,11 @@ struct Plan {
         int seen = 0;
         cudaGraphExec_t exec = nullptr;
         int64_t launches = 0;
+        int64_t last_use = 0;
     };
+    static constexpr size_t kMaxGraphs = 16;  // LRU cap on captured graphs per plan
     std::map<GraphKey, GraphEntry> graphs;
+    int64_t graph_clock = 0;
     // ring kernels: node-balanced chunk tables (segment boundaries), per target node count
     struct ChunkTable {
         DevBuf buf;
@@ -244,6 +247,7 @@ void release_fft_state(const Plan* p);
 void precompute(Plan& p, inft_method method, inft_weights wt, double tau, cudaStream_t st);
 
 bool is_device_pointer(const void* ptr);
+int pointer_device(const void* ptr);  // device ordinal, -1 for host memory
 
 inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
 

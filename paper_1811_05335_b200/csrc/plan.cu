@@ -24,20 +24,31 @@ namespace inft {
 static thread_local std::string g_last_error;
 // Dynamic shared-memory attribute set once per (kernel, largest size so far) and occupancy
 // queried once per (kernel, threads, smem): both are driver calls on every apply otherwise.
+// Keyed by (device, kernel): the attribute is per device context, so a second plan on another
+// GPU in the same process must set it again.
 static std::mutex g_attr_mu;
+static int current_device() {
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) {
+        cudaGetLastError();
+        dev = 0;
+    }
+    return dev;
+}
 void ensure_smem_attr(const void* fn, size_t smem) {
-    static std::unordered_map<const void*, size_t> done;
+    static std::map<std::pair<int, const void*>, size_t> done;
+    const auto key = std::make_pair(current_device(), fn);
     std::lock_guard<std::mutex> g(g_attr_mu);
-    auto it = done.find(fn);
+    auto it = done.find(key);
     if (it != done.end() && it->second >= smem) return;
     INFT_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    done[fn] = smem;
+    done[key] = smem;
 }
 
 int occupancy_cached(const void* fn, int threads, size_t smem) {
-    static std::map<std::tuple<const void*, int, size_t>, int> done;
+    static std::map<std::tuple<int, const void*, int, size_t>, int> done;
+    auto key = std::make_tuple(current_device(), fn, threads, smem);
     std::lock_guard<std::mutex> g(g_attr_mu);
-    auto key = std::make_tuple(fn, threads, smem);
     auto it = done.find(key);
     if (it != done.end()) return it->second;
     int occ = 1;
@@ -144,14 +155,21 @@ Plan::~Plan() {
 }
 
 bool is_device_pointer(const void* ptr) {
-    if (!ptr) return false;
+    return pointer_device(ptr) >= 0;
+}
+
+// Device ordinal of a device (or managed) pointer, -1 for host memory (pageable or pinned).
+int pointer_device(const void* ptr) {
+    if (!ptr) return -1;
     cudaPointerAttributes a;
     cudaError_t e = cudaPointerGetAttributes(&a, ptr);
     if (e != cudaSuccess) {
         cudaGetLastError();
-        return false;
+        return -1;
     }
-    return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
+    if (a.type == cudaMemoryTypeDevice) return a.device;
+    if (a.type == cudaMemoryTypeManaged) return a.device < 0 ? 0 : a.device;
+    return -1;
 }
 
 // ------------------------------------------------------------------ kernels
@@ -322,9 +340,8 @@ void plan_build(Plan& p, const double* nodes_any, cudaStream_t st) {
     const int d = p.d;
     p.nodes.alloc(sizeof(double) * std::max<int64_t>(1, p.N * d));
     if (p.N > 0) {
-        bool dev = is_device_pointer(nodes_any);
-        INFT_CUDA(cudaMemcpyAsync(p.nodes.p, nodes_any, sizeof(double) * p.N * d,
-                                  dev ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, st));
+        // cudaMemcpyDefault (UVA): host, this device or a peer device's buffer
+        INFT_CUDA(cudaMemcpyAsync(p.nodes.p, nodes_any, sizeof(double) * p.N * d, cudaMemcpyDefault, st));
     }
     // tiles
     if (d == 1) {
@@ -498,9 +515,7 @@ void upload_weights(Plan& p, const double* w_host, inft_method method, inft_weig
     DevBuf tmp;
     tmp.alloc(sizeof(double) * std::max<int64_t>(1, n));
     if (n > 0) {
-        bool dev = is_device_pointer(w_host);
-        INFT_CUDA(cudaMemcpyAsync(tmp.p, w_host, sizeof(double) * n,
-                                  dev ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, st));
+        INFT_CUDA(cudaMemcpyAsync(tmp.p, w_host, sizeof(double) * n, cudaMemcpyDefault, st));
     }
     size_t es = p.prec == INFT_C128 ? sizeof(double) : sizeof(float);
     p.w.alloc(es * std::max<int64_t>(1, p.N * p.PP * cp));

@@ -364,3 +364,26 @@ def test_gpu_adjointness_and_batch_invariance(P, torch):
         assert abs(a - b) <= 1e-12 * abs(a)
     one = plan.apply(_dev(torch, f[7:8])).cpu().numpy()
     assert O.rel_l2(one, A[7:8]) <= 1e-15
+
+
+def test_binding_rejects_mismatched_buffers(P, torch):
+    """The C side trusts R*N / R*M elements at the plan's precision: the binding checks dtype,
+    trailing size, output size and device before passing raw pointers (no silent overrun)."""
+    M, sigma, m = 64, 2.0, 4
+    x = S.jittered(100, 3)
+    plan = P.Plan(torch.from_numpy(x).to(torch.float32).cuda(), M, sigma, m)  # float32 nodes: converted
+    np.testing.assert_array_equal(plan.get_bins()[0], O.node_base(x.astype(np.float32).astype(np.float64), 128, m))
+    plan = P.Plan(x, M, sigma, m).set_bopt(_live_random_weights(x, M, sigma, m, 1), "alg2")
+    f = torch.zeros(2, 100, dtype=torch.complex128, device="cuda")
+    with pytest.raises(TypeError):
+        plan.apply(f.to(torch.complex64))
+    with pytest.raises(ValueError):
+        plan.apply(torch.zeros(2, 99, dtype=torch.complex128, device="cuda"))
+    with pytest.raises(ValueError):
+        plan.apply(f, out=torch.zeros(1, M, dtype=torch.complex128, device="cuda"))
+    with pytest.raises(ValueError):  # config-5-like trap: adjoint output sized [R][M] with N > M
+        plan.adjoint_apply(torch.zeros(2, M, dtype=torch.complex128, device="cuda"),
+                           out=torch.zeros(2, M, dtype=torch.complex128, device="cuda"))
+    with pytest.raises(ValueError):
+        P.Plan(np.zeros((10, 2)), M, sigma, m)  # 2-D nodes for a 1-D plan
+    assert plan.apply(f).shape == (2, M)
