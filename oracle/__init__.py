@@ -679,20 +679,30 @@ def trig_sum(c, x, nthreads=0):
     return out[0].reshape(shape) if one else out.reshape((R,) + shape)
 
 
+_COEF_CACHE = {}
+
+
+def _kernel_coefs(M, sigma, m, window, power):
+    """1/(M_sigma what(k)^power), k = -M/2..M/2-1 (cached: the I0 series over 2^20 k is slow)."""
+    key = (M, sigma, m, window, power)
+    if key not in _COEF_CACHE:
+        Ms = msigma(M, sigma)
+        c = (1.0 / window_hat_vector(M, sigma, m) ** power / Ms if window == "kb"
+             else inv_what_vector(M, sigma, m, window) ** power / Ms)
+        if len(_COEF_CACHE) > 16:
+            _COEF_CACHE.clear()
+        _COEF_CACHE[key] = np.ascontiguousarray(c, dtype=np.complex128)
+    return _COEF_CACHE[key]
+
+
 def G_kernel_c(dx, M, sigma, m, window="kb"):
     """G(x) of G_kernel by the C direct sum (same sum, for large test samples)."""
-    Ms = msigma(M, sigma)
-    c = (1.0 / window_hat_vector(M, sigma, m) ** 2 / Ms if window == "kb"
-         else inv_what_vector(M, sigma, m, window) ** 2 / Ms)
-    return trig_sum(c, dx)
+    return trig_sum(_kernel_coefs(M, sigma, m, window, 2), dx)
 
 
 def Kplus_kernel_c(dx, M, sigma, m, window="kb"):
     """K+(x) of Kplus_kernel by the C direct sum."""
-    Ms = msigma(M, sigma)
-    c = (1.0 / window_hat_vector(M, sigma, m) / Ms if window == "kb"
-         else inv_what_vector(M, sigma, m, window) / Ms)
-    return trig_sum(c, dx)
+    return trig_sum(_kernel_coefs(M, sigma, m, window, 1), dx)
 
 
 def ndft_c(x, fhat, M):

@@ -165,6 +165,7 @@ def test_cfg5_gpu_bopt_sampled_rows(P, torch, prec):
 # ------------------------------------------------------------------ setup parity, 512 columns
 def _check_columns(w, x, members, largest, M, sigma, m, d, label):
     worst = 0.0
+    ratios = []
     t0 = time.perf_counter()
     for n, mem in members.items():
         if not mem:
@@ -173,12 +174,16 @@ def _check_columns(w, x, members, largest, M, sigma, m, d, label):
         ts = [t for _, t in mem]
         G, y = (gram_1d if d == 1 else gram_2d)(x, js, n, M, sigma, m)
         bo, _ = O.solve_minnorm_gram(G, y)
-        ro, rg = residual(G, y, bo), residual(G, y, w[js, ts])
+        bg = w[js, ts]
+        ro, rg = residual(G, y, bo), residual(G, y, bg)
         assert abs(rg - ro) <= 1e-6, (label, n, len(js), ro, rg)
         worst = max(worst, abs(rg - ro))
+        ratios.append(np.linalg.norm(bg) / max(np.linalg.norm(bo), 1e-300))
     sizes = [len(members[n]) for n in largest]
+    ratios = np.array(ratios)
     print(f"{label}: {len(members)} columns (32 largest |I(l)| {max(sizes)}..{min(sizes)}), "
-          f"max |res_gpu - res_oracle| {worst:.2e}, {time.perf_counter() - t0:.1f} s")
+          f"max |res_gpu - res_oracle| {worst:.2e}, ||b_gpu||/||b_oracle|| median {np.median(ratios):.3g} "
+          f"max {ratios.max():.3g} (>2: {(ratios > 2).sum()}), {time.perf_counter() - t0:.1f} s")
 
 
 @pytest.mark.parametrize("cid", [3, 5])
