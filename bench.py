@@ -31,6 +31,25 @@ RLOC = 64
 CFG_ID = 5
 
 
+def workload_config(R, ws, prec):
+    """The `config` object of the bench line -- identical for our arm and the reference arm."""
+    return {"workload": "cfg5: 1-D M=2^20, N=2^21 jittered (seed 4), sigma=2, m=8, Kaiser-Bessel, "
+                        "Alg. 2 B_opt; step = inverse NFFT + inverse adjoint NFFT",
+            "rhs_per_gpu": R, "global_batch": R * ws, "parallelism": f"rhs-sharded x{ws}",
+            "l2": "inputs larger than L2 (no flush needed)", "precision": prec}
+
+
+def cpu_model():
+    try:
+        with open("/proc/cpuinfo") as fh:
+            for line in fh:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return None
+
+
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -46,6 +65,10 @@ def parse():
                     help="N > 1: skip the scatter/apply/gather timing through rank 0")
     ap.add_argument("--e2e-one-plan", action="store_true",
                     help="e2e: inverse and adjoint on one plan/stream (serialised) instead of two")
+    ap.add_argument("--no-configs", action="store_true",
+                    help="skip the per-config record (configs 1-4 c128, config 5 c64)")
+    ap.add_argument("--config", default="c5", choices=["c1", "c2", "c3", "c4", "c5"],
+                    help="print only the per-config record line of this BASELINE config (c5: the headline)")
     return ap.parse_args()
 
 
@@ -56,14 +79,96 @@ def dist_env():
     return ws, rank, local
 
 
-def model_bytes_per_rhs(N, M, Ms, P, e, ew, R):
+def model_bytes_per_rhs(N, M, Ms, P, e, ew, R, d=1):
     """SURVEY 8(d) algorithmic bytes: each factor streamed once, FFT = 1 read + 1 write
-    of the grid, B_opt (P weights + one int32 slot base per node) once per batch."""
-    inv = e * (N + 3 * Ms + 2 * M) + (P * ew + 4) * N / R
-    adj = e * (M + 4 * Ms + N) + (P * ew + 4) * N / R
-    spread = e * (N + Ms) + (P * ew + 4) * N / R
-    gather = e * (Ms + N) + (P * ew + 4) * N / R
+    of the grid, B_opt (P weights + one int32 slot base per node and dimension) once per batch."""
+    inv = e * (N + 3 * Ms + 2 * M) + (P * ew + 4 * d) * N / R
+    adj = e * (M + 4 * Ms + N) + (P * ew + 4 * d) * N / R
+    spread = e * (N + Ms) + (P * ew + 4 * d) * N / R
+    gather = e * (Ms + N) + (P * ew + 4 * d) * N / R
     return inv, adj, spread, gather
+
+
+# measured FMA peaks of this B200 (tools/fp_peak.cu, profiles/r01_fp_peaks.txt; 2 flops per FMA)
+FP_PEAK_TFLOPS = {"c128": 34.1, "c64": 72.3}
+CONFIG_BOUND = {1: "latency", 2: "latency", 3: "hbm", 4: "fp64", 5: "hbm"}
+
+
+def time_config(cid, prec, steps, warmup, dev, torch, P, S, R=None):
+    """One BASELINE config on its own batch and direction(s), GPU setup by the config's algorithm
+    (SURVEY D1), random device inputs; CUDA events over `steps` steps (graph replay), then a
+    profiled pass for the stage times.  Returns the per-config record."""
+    c = S.config(cid)
+    x = S.make_nodes(c)
+    d = c["d"]
+    M = c["M"][0] if d == 1 else tuple(c["M"])
+    sigma, m = c["sigma"], c["m"]
+    R = R or (c["R"] if cid != 5 else RLOC)
+    Mtot = int(np.prod(c["M"]))
+    Ms = int(np.prod([v * sigma for v in c["M"]]))
+    N = x.shape[0]
+    Pn = (2 * m + 1) ** d
+    e, ew = (16, 8) if prec == "c128" else (8, 4)
+    cdt = torch.complex128 if prec == "c128" else torch.complex64
+    plan = P.Plan(x, M, sigma, m, precision=prec, device=dev)
+    t0 = time.perf_counter()
+    plan.precompute("alg1" if c["alg"] == 1 else "alg2")
+    torch.cuda.synchronize()
+    setup_s = time.perf_counter() - t0
+    g = torch.Generator(device=f"cuda:{dev}").manual_seed(77 + cid)
+    f = torch.randn(R, N, dtype=cdt, device=f"cuda:{dev}", generator=g)
+    h = torch.randn(R, Mtot, dtype=cdt, device=f"cuda:{dev}", generator=g)
+    fo = torch.empty(R, Mtot, dtype=cdt, device=f"cuda:{dev}")
+    ho = torch.empty(R, N, dtype=cdt, device=f"cuda:{dev}")
+    dirs = c["dirs"]
+    stream = torch.cuda.current_stream()
+
+    def step():
+        if "inverse" in dirs:
+            plan.apply(f, out=fo, stream=stream)
+        if "adjoint" in dirs:
+            plan.adjoint_apply(h, out=ho, stream=stream)
+
+    for _ in range(max(3, warmup)):
+        step()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    l0 = plan.kernel_launches()
+    e0.record(stream)
+    for _ in range(steps):
+        step()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    launches = (plan.kernel_launches() - l0) / steps
+    ms = e0.elapsed_time(e1) / steps
+    plan.set_profiling(True)
+    plan.get_profile(reset=True)
+    for _ in range(steps):
+        step()
+    torch.cuda.synchronize()
+    prof = plan.get_profile(reset=True)
+    plan.set_profiling(False)
+    inv_b, adj_b, spread_b, gather_b = model_bytes_per_rhs(N, Mtot, Ms, Pn, e, ew, R, d)
+    byts = R * ((inv_b if "inverse" in dirs else 0) + (adj_b if "adjoint" in dirs else 0))
+    peak, _ = measured_peak_hbm()
+    gbs = byts / (ms / 1e3) / 1e9
+    stages = {k: round(v[0] / v[1], 5) for k, v in prof.items() if v[1]}
+    rec = {"cfg": cid, "prec": prec, "rhs": R, "dirs": list(dirs), "ms_per_step": ms,
+           "solves_per_s": R * len(dirs) / (ms / 1e3), "model_gbs": gbs, "hbm_frac": gbs / peak,
+           "bound": CONFIG_BOUND[cid], "stages_ms": stages, "launches_per_step": launches,
+           "setup_s": setup_s, "fast_path": plan.info()["fast_path"], "fused_fft": plan.info()["fused_fft"]}
+    if CONFIG_BOUND[cid] == "latency":
+        rec["us_per_step"] = ms * 1e3
+    if CONFIG_BOUND[cid] == "fp64":
+        # spread / gather: P taps x (2 FMA = 4 flops, real weights) per node and RHS
+        flops = 4.0 * N * Pn * R
+        for k in ("spread", "gather"):
+            if k in stages:
+                tf = flops / (stages[k] / 1e3) / 1e12
+                rec[f"{k}_tflops"] = tf
+                rec[f"{k}_fp_frac"] = tf / FP_PEAK_TFLOPS[prec]
+        rec["fp_peak_tflops"] = FP_PEAK_TFLOPS[prec]
+    return rec
 
 
 def ncu_traffic(stage, prec, R):
@@ -161,6 +266,7 @@ def cpu_baseline(x, M, sigma, m, w, R_sample, target_s=10.0):
             break
     cores = min(O.num_threads(), R_sample)
     return {"value": 2 * R_sample * batches / dt, "unit": "solves/s", "cores": cores, "kind": "oracle",
+            "cpu_model": cpu_model(), "host_threads": os.cpu_count(),
             "sample": f"config 5, {batches} x {R_sample} RHS x (inverse + inverse adjoint), same B_opt, "
                       f"{dt:.1f} s wall"}
 
@@ -195,10 +301,12 @@ def run_reference(args):
             "impl": "reference", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": 1e3 * dt / args.steps, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
             "dtype": "f64", "data": "synthetic",
-            "config": {"workload": "cfg5: 1-D M=2^20, N=2^21 jittered (seed 4), sigma=2, m=8, KB; "
-                                   "inverse + inverse adjoint", "rhs_per_step": R_s},
+            "config": workload_config(args.rhs, args.gpus, "c128"),
             "cpu_baseline": {"value": val, "unit": "solves/s", "cores": cores, "kind": "oracle",
-                             "sample": f"{R_s} RHS per direction per step (bounded sample of the 64-RHS batch)"},
+                             "cpu_model": cpu_model(), "host_threads": os.cpu_count(),
+                             "sample": f"{R_s} RHS per direction per step (bounded sample of the {args.rhs}-RHS "
+                                       "batch); weights = the window matrix B on the same sparsity (the apply's "
+                                       "cost does not depend on the values)"},
             "e2e": {"value": val, "unit": "solves/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
@@ -245,21 +353,28 @@ def run_e2e(args, plan, f, h, R, N, M, e, cdt, ws, dev, stream, torch, dist, pla
                     + ("; inverse and adjoint on two plans/streams" if plan2 is not None else "")}
 
 
-def run_dist_e2e(plan, R, N, M, cdt, ws, rank, dev, steps, torch, dist):
+def run_dist_e2e(plan, R, N, M, cdt, ws, rank, dev, steps, torch, dist, comm_dev=None, return_outputs=False):
     """SURVEY 8(e) with-communication time: rank 0 owns the whole batch (R per rank), scatters
-    the inputs f and h over NCCL, every rank applies to its shard, and the outputs are gathered
-    back to rank 0; per step, max over ranks.  Reported next to the rank-resident weak-scaling
-    `value` (the efficiency measure).  Complex tensors travel as float views."""
+    the inputs f and h, every rank applies to its shard, and the outputs are gathered back to
+    rank 0; per step, max over ranks.  Reported next to the rank-resident weak-scaling `value`
+    (the efficiency measure).  Complex tensors travel as float views.  comm_dev: where the
+    collectives' buffers live (the plan's device for NCCL; the CPU for gloo in tests, with
+    copies to and from the plan's device around the apply)."""
+    comm_dev = comm_dev if comm_dev is not None else dev
+    staged = torch.device(comm_dev) != torch.device(dev)
     Rg = R * ws
-    g = torch.Generator(device=dev).manual_seed(7)
-    F = torch.randn(Rg, N, dtype=cdt, device=dev, generator=g) if rank == 0 else None
-    H = torch.randn(Rg, M, dtype=cdt, device=dev, generator=g) if rank == 0 else None
-    fo = torch.empty(Rg, M, dtype=cdt, device=dev) if rank == 0 else None
-    ho = torch.empty(Rg, N, dtype=cdt, device=dev) if rank == 0 else None
-    f_loc = torch.empty(R, N, dtype=cdt, device=dev)
-    h_loc = torch.empty(R, M, dtype=cdt, device=dev)
-    oi = torch.empty(R, M, dtype=cdt, device=dev)
-    oa = torch.empty(R, N, dtype=cdt, device=dev)
+    g = torch.Generator(device=comm_dev).manual_seed(7)
+    F = torch.randn(Rg, N, dtype=cdt, device=comm_dev, generator=g) if rank == 0 else None
+    H = torch.randn(Rg, M, dtype=cdt, device=comm_dev, generator=g) if rank == 0 else None
+    fo = torch.empty(Rg, M, dtype=cdt, device=comm_dev) if rank == 0 else None
+    ho = torch.empty(Rg, N, dtype=cdt, device=comm_dev) if rank == 0 else None
+    f_loc = torch.empty(R, N, dtype=cdt, device=comm_dev)
+    h_loc = torch.empty(R, M, dtype=cdt, device=comm_dev)
+    oi = torch.empty(R, M, dtype=cdt, device=comm_dev)
+    oa = torch.empty(R, N, dtype=cdt, device=comm_dev)
+    if staged:
+        f_d, h_d = torch.empty(R, N, dtype=cdt, device=dev), torch.empty(R, M, dtype=cdt, device=dev)
+        oi_d, oa_d = torch.empty(R, M, dtype=cdt, device=dev), torch.empty(R, N, dtype=cdt, device=dev)
     real = torch.view_as_real
 
     def chunks(t):
@@ -268,14 +383,23 @@ def run_dist_e2e(plan, R, N, M, cdt, ws, rank, dev, steps, torch, dist):
     def step():
         dist.scatter(real(f_loc), chunks(F), src=0)
         dist.scatter(real(h_loc), chunks(H), src=0)
-        plan.apply(f_loc, out=oi)
-        plan.adjoint_apply(h_loc, out=oa)
+        if staged:
+            f_d.copy_(f_loc)
+            h_d.copy_(h_loc)
+            plan.apply(f_d, out=oi_d)
+            plan.adjoint_apply(h_d, out=oa_d)
+            oi.copy_(oi_d)
+            oa.copy_(oa_d)
+        else:
+            plan.apply(f_loc, out=oi)
+            plan.adjoint_apply(h_loc, out=oa)
         dist.gather(real(oi), chunks(fo), dst=0)
         dist.gather(real(oa), chunks(ho), dst=0)
 
     step()
     dist.barrier()
-    if torch.cuda.is_available():
+    on_gpu = torch.device(comm_dev).type == "cuda"
+    if on_gpu:
         torch.cuda.synchronize()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
@@ -289,13 +413,16 @@ def run_dist_e2e(plan, R, N, M, cdt, ws, rank, dev, steps, torch, dist):
         for _ in range(steps):
             step()
         ms = (time.perf_counter() - t0) * 1e3 / steps
-    t = torch.tensor([ms], dtype=torch.float64, device=dev)
+    t = torch.tensor([ms], dtype=torch.float64, device=comm_dev)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms = float(t.item())
     bytes_moved = int((Rg * (N + M) * 2) * (16 if cdt == torch.complex128 else 8))
-    return {"value": 2 * Rg / (ms / 1e3), "unit": "solves/s", "ms_per_step": ms,
-            "collective_bytes_per_step": bytes_moved,
-            "note": "rank 0 scatters f, h and gathers fhat, f over NCCL each step (SURVEY 8(e))"}
+    res = {"value": 2 * Rg / (ms / 1e3), "unit": "solves/s", "ms_per_step": ms,
+           "collective_bytes_per_step": bytes_moved,
+           "note": "rank 0 scatters f, h and gathers fhat, f each step (SURVEY 8(e))"}
+    if return_outputs:
+        res["outputs"] = (F, H, fo, ho)
+    return res
 
 
 def main():
@@ -308,6 +435,9 @@ def main():
 
     ws, rank, local = dist_env()
     if ws > 1:
+        # NCCL's communicator set-up lines (transport, NVLS/NVLink paths) go to stderr
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
         torch.cuda.set_device(local)
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     dev = local if ws > 1 else 0
@@ -316,6 +446,22 @@ def main():
     import synth as S
     import paper_1811_05335_b200 as P
     from paper_1811_05335_b200 import dist as D
+
+    if args.config != "c5":
+        cid = int(args.config[1:])
+        rec = time_config(cid, args.prec, args.steps, args.warmup, dev, torch, P, S)
+        if rank == 0:
+            print(json.dumps({"metric": "iNFFT solves/s (complex double, batched)" if args.prec == "c128"
+                              else "iNFFT solves/s (complex float, batched)", "value": rec["solves_per_s"] * ws,
+                              "unit": "solves/s", "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
+                              "ms_per_step": rec["ms_per_step"], "higher_is_better": True, "scaling": "weak",
+                              "vs_baseline": None, "dtype": "f64" if args.prec == "c128" else "f32",
+                              "data": "synthetic", "config": {"workload": f"BASELINE config {cid}",
+                                                              "rhs_per_gpu": rec["rhs"], "precision": args.prec},
+                              "record": rec}), flush=True)
+        if ws > 1:
+            dist.destroy_process_group()
+        return
 
     c = S.config(CFG_ID)
     x = S.make_nodes(c)
@@ -355,9 +501,8 @@ def main():
     torch.cuda.synchronize()
 
     # ---------------------------------------------------------------- timed region
+    # the path users get: profiling off, so repeated applies replay their CUDA graphs
     sampler = ClockSampler(dev)
-    plan.set_profiling(True)
-    plan.get_profile(reset=True)
     launches0 = plan.kernel_launches()
     if ws > 1:
         dist.barrier()
@@ -376,12 +521,27 @@ def main():
     clocks = sampler.stop()
     launches = plan.kernel_launches() - launches0
     ms_total = ev0.elapsed_time(ev1)
-    prof = plan.get_profile(reset=True)
-    plan.set_profiling(False)
     ms_total = D.max_over_ranks(ms_total, dist if ws > 1 else None, device=torch.device("cuda", dev))
     ms_step = ms_total / args.steps
     solves = 2 * R * ws * args.steps
     value = solves / (ms_total / 1e3)
+
+    # ---------------------------------------------------------------- per-kernel times (second pass)
+    # the same K steps again with the library's per-stage CUDA events on the launching stream
+    # (plain launches, no graph replay): the roofline's kernel durations and stage shares
+    plan.set_profiling(True)
+    plan.get_profile(reset=True)
+    torch.cuda.synchronize()
+    p0 = torch.cuda.Event(enable_timing=True)
+    p1 = torch.cuda.Event(enable_timing=True)
+    p0.record(stream)
+    for _ in range(args.steps):
+        step()
+    p1.record(stream)
+    torch.cuda.synchronize()
+    ms_prof = p0.elapsed_time(p1)
+    prof = plan.get_profile(reset=True)
+    plan.set_profiling(False)
 
     # ---------------------------------------------------------------- roofline of the dominant kernel
     inv_b, adj_b, spread_b, gather_b = model_bytes_per_rhs(N, M, Ms, info["P"], e, ew, R)
@@ -404,7 +564,9 @@ def main():
                 "traffic_source": traffic_src, "fused_fft": fused}
     stages = {k: {"ms_per_launch": stage_ms[k], "launches": prof[k][1],
                   "gbs": (stage_bytes[k] / (stage_ms[k] / 1e3) / 1e9) if stage_ms[k] else None,
-                  "share_of_step": (prof[k][0] / ms_total) if ms_total else None} for k in stage_ms}
+                  "share_of_step": (prof[k][0] / ms_prof) if ms_prof else None} for k in stage_ms}
+    roofline["timing"] = (f"per-stage CUDA events on the launching stream over a second pass of "
+                          f"{args.steps} steps ({ms_prof / args.steps:.3f} ms/step with events, plain launches)")
 
     # ---------------------------------------------------------------- e2e through the C ABI with host buffers
     e2e = None
@@ -434,6 +596,16 @@ def main():
         except Exception as ex:  # the baseline must never break the bench line
             cpu = {"value": None, "unit": "solves/s", "cores": None, "kind": "oracle", "sample": f"failed: {ex}"}
 
+    # ---------------------------------------------------------------- per-config record (rank 0, N = 1)
+    configs = None
+    if rank == 0 and ws == 1 and not args.no_configs:
+        configs = {}
+        for cid, prec in ((1, "c128"), (2, "c128"), (3, "c128"), (4, "c128"), (5, "c64")):
+            try:
+                configs[f"c{cid}_{prec}"] = time_config(cid, prec, max(args.steps, 20), args.warmup, dev, torch, P, S)
+            except Exception as ex:
+                configs[f"c{cid}_{prec}"] = {"error": str(ex)[:300]}
+
     if rank == 0:
         line = {
             "metric": "iNFFT solves/s (complex double, batched)" if args.prec == "c128"
@@ -441,13 +613,10 @@ def main():
             "value": value, "unit": "solves/s", "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
             "dtype": "f64" if args.prec == "c128" else "f32", "data": "synthetic",
-            "config": {"workload": "cfg5: 1-D M=2^20, N=2^21 jittered (seed 4), sigma=2, m=8, Kaiser-Bessel, "
-                                   "Alg. 2 B_opt; step = inverse NFFT + inverse adjoint NFFT",
-                       "rhs_per_gpu": R, "global_batch": R * ws, "parallelism": f"rhs-sharded x{ws}",
-                       "l2": "inputs larger than L2 (no flush needed)", "precision": args.prec},
+            "config": workload_config(R, ws, args.prec),
             "apply_hbm_gbs": apply_gbs, "apply_hbm_frac": apply_gbs / peak,
             "roofline": roofline, "stages": stages, "cpu_baseline": cpu, "e2e": e2e, "dist_e2e": dist_e2e,
-            "gpu_launches": launches, "clocks": clocks,
+            "gpu_launches": launches, "clocks": clocks, "configs": configs,
             "setup": {"plan_s": t_plan, "precompute_s": t_setup, "n_rank_deficient": info["n_rank_deficient"],
                       "max_col_size": info["max_col_size"], "fast_path": info["fast_path"],
                       "workspace_bytes": info["workspace_bytes"]},

@@ -42,8 +42,19 @@ def _worker(rank, ws, port, q):
     import bench
     R, N, M = 3, 10, 6
     plan = FakePlan(N, M)
-    res = bench.run_dist_e2e(plan, R, N, M, torch.complex128, ws, rank, torch.device("cpu"), 2, torch, dist)
-    q.put((rank, res["value"] > 0, res["collective_bytes_per_step"]))
+    res = bench.run_dist_e2e(plan, R, N, M, torch.complex128, ws, rank, torch.device("cpu"), 2, torch, dist,
+                             return_outputs=True)
+    same = True
+    if rank == 0:
+        # every rank's shard came back to rank 0 in order: the gathered outputs equal the
+        # stand-in plan applied to the whole batch
+        F, H, fo, ho = res["outputs"]
+        ref_i = torch.empty_like(fo)
+        ref_a = torch.empty_like(ho)
+        plan.apply(F, out=ref_i)
+        plan.adjoint_apply(H, out=ref_a)
+        same = bool(torch.equal(fo, ref_i) and torch.equal(ho, ref_a))
+    q.put((rank, res["value"] > 0 and same, res["collective_bytes_per_step"]))
     dist.destroy_process_group()
 
 

@@ -37,10 +37,23 @@ def test_bench_line_contract():
     assert e["value"] < d["value"]  # host copies cannot be free
     assert d["gpu_launches"] >= 6 * 3
     assert {"sm_mhz", "sm_max_mhz", "reasons"} <= set(d["clocks"])
+    cf = d["configs"]
+    assert set(cf) == {"c1_c128", "c2_c128", "c3_c128", "c4_c128", "c5_c64"}, cf
+    for k, rec in cf.items():
+        assert "error" not in rec, (k, rec)
+        assert rec["ms_per_step"] > 0 and rec["solves_per_s"] > 0 and rec["bound"] in ("latency", "hbm", "fp64")
+    assert 0 < cf["c4_c128"]["spread_fp_frac"] < 1.2
+
+
+def test_bench_single_config_flag():
+    d = _run(["--config", "c3", "--steps", "3", "--warmup", "3"])
+    assert d["record"]["cfg"] == 3 and d["value"] > 0 and d["config"]["rhs_per_gpu"] == 256
 
 
 def test_bench_reference_arm_contract():
     d = _run(["--impl", "reference", "--steps", "1", "--warmup", "3"])
+    ours = _run(["--steps", "3", "--warmup", "3", "--no-cpu-baseline", "--no-e2e", "--no-configs"])
+    assert d["config"] == ours["config"]  # same workload description in both arms
     assert d["impl"] == "reference" and d["value"] > 0 and d["unit"] == "solves/s"
     assert d["cpu_baseline"]["kind"] == "oracle" and d["cpu_baseline"]["cores"] >= 1
     assert d["e2e"]["h2d_bytes_per_step"] == 0 and d["e2e"]["d2h_bytes_per_step"] == 0
