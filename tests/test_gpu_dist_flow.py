@@ -3,7 +3,9 @@ one GPU per box; the ranks' kernels never wait on each other -- every collective
 collective): each rank builds its own plan replica and runs the GPU Alg. 2 setup, the ranks
 prove they hold bit-identical B_opt (SHA-256 digest all-gather), rank 0 scatters the batch,
 every rank applies its shard, rank 0 gathers -- and the gathered outputs must be bit-identical
-to ONE plan applied to the whole batch (the apply kernels are deterministic and per-RHS).
+to ONE plan applied shard by shard (the apply kernels are deterministic), and equal to one plan
+applied to the whole batch at once to rounding (the ring kernels' node chunks depend on the batch
+size, which changes the straight-line / general code path of some 16-node batches).
 Sharding basis: independent right-hand sides for fixed nodes."""
 import os
 import socket
@@ -51,11 +53,14 @@ def _worker(rank, ws, port, q):
         detail = ""
         if rank == 0:
             F, H, fo, ho = res["outputs"]
+            sh_i = torch.cat([plan.apply(F[i:i + R].cuda()).cpu() for i in range(0, ws * R, R)])
+            sh_a = torch.cat([plan.adjoint_apply(H[i:i + R].cuda()).cpu() for i in range(0, ws * R, R)])
+            same = bool(torch.equal(fo, sh_i) and torch.equal(ho, sh_a))
             one_i = plan.apply(F.cuda()).cpu()
             one_a = plan.adjoint_apply(H.cuda()).cpu()
-            same = bool(torch.equal(fo, one_i) and torch.equal(ho, one_a))
-            detail = f"max diff {float((fo - one_i).abs().max()):.3g} / {float((ho - one_a).abs().max()):.3g}"
-            ok = ok and same
+            rel = max(float((fo - one_i).norm() / one_i.norm()), float((ho - one_a).norm() / one_a.norm()))
+            detail = f"bit-identical to shard-wise apply: {same}; vs whole batch rel {rel:.2e}"
+            ok = ok and same and rel <= 1e-14
         q.put((rank, ok, detail))
         dist.destroy_process_group()
     except Exception as ex:  # report instead of hanging the other rank
