@@ -17,7 +17,7 @@ HERE = os.path.join(ROOT, "paper_1811_05335_b200")
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.environ.get("INFT_LIB_OUT") or os.path.join(HERE, "libinft.so")
 EXTRA = os.environ.get("INFT_NVCC_EXTRA", "").split()
-SOURCES = ["plan.cu", "apply.cu", "stream1d.cu", "stream1d_ring.cu", "fft.cu", "setup.cu", "quadratic.cu"]
+SOURCES = ["plan.cu", "apply.cu", "stream1d.cu", "stream1d_ring.cu", "fft.cu", "setup.cu", "quadratic.cu", "spread2d_line.cu"]
 CUDA_HOME = os.environ.get("CUDA_HOME", "/usr/local/cuda")
 NVCC = os.path.join(CUDA_HOME, "bin", "nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]

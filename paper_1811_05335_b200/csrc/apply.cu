@@ -114,13 +114,13 @@ __global__ void k_spread_generic_2d(const int32_t* __restrict__ seg_start, const
 // 32-lane read per node).  Every grid value is written once: no atomics, deterministic.
 template <typename T>
 __global__ void k_transpose_f(const C2<T>* __restrict__ f, const int32_t* __restrict__ perm, C2<T>* __restrict__ fT,
-                              int64_t N, int R) {
+                              int64_t N, int R, int RS) {
     const int64_t total = (int64_t)N * R;
     for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
          idx += (int64_t)gridDim.x * blockDim.x) {
         const int64_t i = idx / R;
         const int r = (int)(idx - i * R);
-        fT[idx] = f[(int64_t)r * N + perm[i]];
+        fT[i * RS + r] = f[(int64_t)r * N + perm[i]];
     }
 }
 
@@ -581,16 +581,24 @@ static void spread(Plan& p, const C2<T>* f, C2<T>* grid, int64_t R, cudaStream_t
                 p.seg_start.as<int32_t>(), p.n0s.as<int32_t>(), p.perm.as<int32_t>(), w, p.PP, p.P, f, grid, p.N,
                 p.Ms[0], p.GS, p.S[0], (int)R);
     } else if (!getenv_flag("INFT_SPREAD2D_GENERIC")) {
-        // node-major copy of f (sorted node order), then the tile kernel (or one warp per cell)
-        if (p.fT_rhs < R) {
-            p.fT.alloc(sizeof(C2<T>) * (size_t)p.N * R);
-            p.fT_rhs = R;
+        // node-major copy of f (sorted node order), then the line kernel (or the tile kernel, or one
+        // warp per cell); the line kernel's bulk copies of f rows need 16-byte aligned row starts,
+        // so its row stride is R rounded up to 16 bytes
+        const bool line = line2d_available(p);
+        const int64_t RS = line ? ceil_div(R * (int64_t)sizeof(C2<T>), 16) * 16 / (int64_t)sizeof(C2<T>) : R;
+        if (p.fT_rhs < RS) {
+            p.fT.alloc(sizeof(C2<T>) * (size_t)p.N * RS);
+            p.fT_rhs = RS;
             p.state_version++;
         }
         C2<T>* fT = p.fT.as<C2<T>>();
-        k_transpose_f<T><<<gs_blocks(R * p.N, 256), 256, 0, st>>>(f, p.perm.as<int32_t>(), fT, p.N, (int)R);
+        k_transpose_f<T><<<gs_blocks(R * p.N, 256), 256, 0, st>>>(f, p.perm.as<int32_t>(), fT, p.N, (int)R, (int)RS);
         INFT_CHECK_LAUNCH();
         p.launches++;
+        if (line) {
+            spread_line2d(p, fT, grid, R, (int)RS, st);
+            return;
+        }
         if (tile2d_available(p)) {
             ensure_spread2d_work(p, st);
             if (p.part2d_rhs < R && p.slots2d > 0) {

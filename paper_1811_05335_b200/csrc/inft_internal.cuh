@@ -181,6 +181,11 @@ struct Plan {
     std::vector<int32_t> seg_host;  // host copy of seg_start (1-D)
     DevBuf ring_side;               // ring spread: side slots of split heavy segments [slot][R][2m]
     int64_t state_version = 0;  // bumped whenever weights / tables change
+    int64_t w_version = 0;      // bumped whenever the weights change (tables derived from them)
+    // 2-D line spread (spread2d_line.cu): virtual-node records, segment table, items, fix entries
+    DevBuf line_rec, line_vidx, line_seg, line_items, line_fix, line_first, line_carry;
+    int64_t line_version = -1, line_slot_rhs = 0;
+    int line_nv = 0, line_nitems = 0, line_nfix = 0;
     cudaStream_t s_graph = nullptr;
     cudaEvent_t ev_g0 = nullptr, ev_g1 = nullptr;
     cudaEvent_t ev_h2d[2] = {nullptr, nullptr}, ev_comp[2] = {nullptr, nullptr},
@@ -237,6 +242,9 @@ bool ring_available(const Plan& p);
 bool ring_spread_available(const Plan& p);
 void spread_ring(Plan& p, const void* f, void* grid, int64_t R, cudaStream_t st);
 void gather_ring(Plan& p, const void* grid, void* f, int64_t R, cudaStream_t st);
+// spread2d_line.cu
+bool line2d_available(const Plan& p);
+void spread_line2d(Plan& p, const void* fT, void* grid, int64_t R, int RS, cudaStream_t st);
 // fft.cu
 bool fused_fft_available(const Plan& p);
 // part: 1 = pass A (columns), 2 = pass B (rows), 3 = both

@@ -486,6 +486,7 @@ void compute_deconv(Plan& p, double s, cudaStream_t st) {
 
 static void finish_weights(Plan& p, inft_method method, inft_weights wt, cudaStream_t st) {
     p.state_version++;  // captured apply graphs refer to the old weight buffers
+    p.w_version++;      // tables derived from the weights (2-D line records) are stale
     // max |w| over the double copy
     DevBuf mx;
     mx.alloc(sizeof(unsigned long long));
