@@ -950,7 +950,7 @@ __global__ void __launch_bounds__(kSmallThreads) k_small_inverse(const int32_t* 
                                                        const int32_t* __restrict__ perm, const T* __restrict__ w,
                                                        int PP, int P, const C2<T>* __restrict__ f,
                                                        C2<T>* __restrict__ fhat, const T* __restrict__ dk, int64_t N,
-                                                       int Ms, int lg, int M, int S) {
+                                                       int Ms, int lg, int M, int S, int stage_bytes) {
     extern __shared__ __align__(16) unsigned char smraw[];
     C2<T>* g = reinterpret_cast<C2<T>*>(smraw);
     C2<T>* tw = g + Ms;
@@ -958,26 +958,71 @@ __global__ void __launch_bounds__(kSmallThreads) k_small_inverse(const int32_t* 
     const C2<T>* fr = f + (int64_t)r * N;
     small_twiddles<T>(tw, Ms);
     const int64_t nseg = (Ms + S - 1) / S;
+    // staged (when the plan's tables fit): f in sorted node order, slot bases, segment table and
+    // weights copied to shared memory by coalesced loads first, so that the per-grid-point scan
+    // below reads shared memory instead of chains of dependent global loads (config 1: 19 us)
+    const bool staged = stage_bytes > 0;
+    C2<T>* fs = tw + Ms / 2;
+    int32_t* ns = reinterpret_cast<int32_t*>(fs + N);
+    int32_t* ss = ns + N;
+    T* ws = reinterpret_cast<T*>(smraw + ((((size_t)(Ms + Ms / 2 + N) * sizeof(C2<T>) + 4 * (N + nseg + 1)) + 15) & ~(size_t)15));
+    if (staged) {
+        for (int i = threadIdx.x; i < N; i += blockDim.x) {
+            fs[i] = fr[perm[i]];
+            ns[i] = n0s[i];
+        }
+        for (int i = threadIdx.x; i <= nseg; i += blockDim.x) ss[i] = seg_start[i];
+        const int64_t nw = (int64_t)N * PP * (WC ? 2 : 1);
+        for (int64_t e = threadIdx.x; e < nw; e += blockDim.x) ws[e] = w[e];
+        __syncthreads();
+    }
+    const int32_t* n0p = staged ? ns : n0s;
+    const int32_t* ssp = staged ? ss : seg_start;
+    const T* wp = staged ? ws : w;
+    // covering segments of grid point n in int32 arithmetic (S is a power of two); the generic
+    // int64 segment walk (for_segments) only when the span wraps onto itself
+    const int lgS = __ffs(S) - 1;
+    auto node_term = [&](int i, int t, T& sx, T& sy) {
+        const C2<T> fv = staged ? fs[i] : fr[perm[i]];
+        for (; t < P; t += Ms) {
+            if (WC) {
+                const T wr = wp[((int64_t)i * PP + t) * 2], wi = wp[((int64_t)i * PP + t) * 2 + 1];
+                sx += wr * fv.x + wi * fv.y;
+                sy += wr * fv.y - wi * fv.x;
+            } else {
+                const T wr = wp[(int64_t)i * PP + t];
+                sx += wr * fv.x;
+                sy += wr * fv.y;
+            }
+        }
+    };
     for (int n = threadIdx.x; n < Ms; n += blockDim.x) {  // a2: conj(w) f over the covering segments
         T sx = 0, sy = 0;
-        for_segments(n, P < Ms ? P : Ms, Ms, S, nseg, [&](int64_t sg) {
-            for (int i = seg_start[sg]; i < seg_start[sg + 1]; ++i) {
-                int t = (int)mod64(n - n0s[i], Ms);
-                if (t >= P) continue;
-                const C2<T> fv = fr[perm[i]];
-                for (; t < P; t += Ms) {
-                    if (WC) {
-                        const T wr = w[((int64_t)i * PP + t) * 2], wi = w[((int64_t)i * PP + t) * 2 + 1];
-                        sx += wr * fv.x + wi * fv.y;
-                        sy += wr * fv.y - wi * fv.x;
-                    } else {
-                        const T wr = w[(int64_t)i * PP + t];
-                        sx += wr * fv.x;
-                        sy += wr * fv.y;
-                    }
+        int lo = n - (P - 1);
+        if (lo < 0) lo += Ms;
+        const int s_lo = lo >> lgS, s_hi = n >> lgS;
+        int cnt = s_hi - s_lo;
+        if (cnt < 0) cnt += (int)nseg;
+        if (P < Ms && (1 << lgS) == S && cnt + 1 <= nseg && !(cnt == 0 && lo > n)) {
+            for (int k = 0; k <= cnt; ++k) {
+                int sg = s_lo + k;
+                if (sg >= nseg) sg -= (int)nseg;
+                const int e = ssp[sg + 1];
+                for (int i = ssp[sg]; i < e; ++i) {
+                    int t = n - n0p[i];
+                    if (t < 0) t += Ms;
+                    if (t < P) node_term(i, t, sx, sy);
                 }
             }
-        });
+        } else {
+            for_segments(n, P < Ms ? P : Ms, Ms, S, nseg, [&](int64_t sg) {
+                for (int i = ssp[sg]; i < ssp[sg + 1]; ++i) {
+                    int t = (int)mod64(n - n0p[i], Ms);
+                    if (t >= P) continue;
+                    node_term(i, t, sx, sy);
+                }
+            });
+        }
         g[bitrev_n(n, lg)] = mk<T>(sx, sy);
     }
     __syncthreads();
@@ -1019,11 +1064,11 @@ __global__ void __launch_bounds__(kSmallThreads) k_small_adjoint(const int32_t* 
         for (int t = 0; t < P; ++t) {
             const C2<T> gv = g[q];
             if (WC) {
-                const T wr = w[((int64_t)i * PP + t) * 2], wi = w[((int64_t)i * PP + t) * 2 + 1];
+                const T wr = __ldg(w + ((int64_t)i * PP + t) * 2), wi = __ldg(w + ((int64_t)i * PP + t) * 2 + 1);
                 sx += wr * gv.x - wi * gv.y;
                 sy += wr * gv.y + wi * gv.x;
             } else {
-                const T wr = w[(int64_t)i * PP + t];
+                const T wr = __ldg(w + (int64_t)i * PP + t);
                 sx += wr * gv.x;
                 sy += wr * gv.y;
             }
@@ -1046,13 +1091,19 @@ template <typename T>
 static void small_inverse(Plan& p, const void* f, void* fhat, int64_t R, cudaStream_t st) {
     const int Ms = (int)p.Ms[0];
     const int lg = __builtin_ctz((unsigned)Ms);
-    const size_t smem = sizeof(C2<T>) * (size_t)(Ms + Ms / 2);
+    const int64_t nseg = (Ms + p.S[0] - 1) / p.S[0];
+    const size_t base = sizeof(C2<T>) * (size_t)(Ms + Ms / 2);
+    // staged tables: f (sorted order), slot bases, segment table, weights
+    const size_t staged = ((base + sizeof(C2<T>) * p.N + 4 * (p.N + nseg + 1) + 15) & ~(size_t)15) +
+                          sizeof(T) * (size_t)p.N * p.PP * (p.wt == INFT_WEIGHTS_COMPLEX ? 2 : 1);
+    const bool stage = staged <= 160 * 1024 && !getenv_flag("INFT_SMALL_NOSTAGE");
+    const size_t smem = stage ? staged : base;
     auto kfn = p.wt == INFT_WEIGHTS_COMPLEX ? k_small_inverse<T, true> : k_small_inverse<T, false>;
     ensure_smem_attr((const void*)kfn, smem);
     kfn<<<(unsigned)R, kSmallThreads, smem, st>>>(p.seg_start.as<int32_t>(), p.n0s.as<int32_t>(), p.perm.as<int32_t>(),
                                         p.w.as<T>(), p.PP, p.P, static_cast<const C2<T>*>(f),
                                         static_cast<C2<T>*>(fhat), dtable<T>(p), p.N, Ms, lg, (int)p.M[0],
-                                        p.S[0]);
+                                        p.S[0], stage ? (int)staged : 0);
     INFT_CHECK_LAUNCH();
     p.launches++;
 }

@@ -714,12 +714,12 @@ __global__ void __launch_bounds__(Geo<T, L>::NT, 1)
 // Pass B in place (complex128): one buffer of max(ST TB, SW TB) elements plus the d side
 // buffer (MODE 0), two CTAs per SM, plain stores from registers (the staged TMA stores of
 // k_pass_b would hold the buffer the next tile lands in).
-template <typename T, int SIGN, int MODE, int L>
-__global__ void __launch_bounds__(Geo<T, L, kTileIP>::NT, 2)
+template <typename T, int SIGN, int MODE, int L, int TE = kTileIP>
+__global__ void __launch_bounds__(Geo<T, L, TE>::NT, TE == kTileIP ? 2 : 1)
     k_pass_b_ip(const __grid_constant__ CUtensorMap dmap, const __grid_constant__ CUtensorMap omap, Args<T> A,
                 int BRd, int BRo, int ntiles) {
     extern __shared__ __align__(128) unsigned char smraw[];
-    using G = Geo<T, L, kTileIP>;
+    using G = Geo<T, L, TE>;
     constexpr int TB = G::TF, S = G::ST, SW = G::SW;
     constexpr int BUF = (S * TB > SW * TB ? S * TB : SW * TB);
     constexpr int DW = (int)(16 / sizeof(T)) > TB ? (int)(16 / sizeof(T)) : TB;
@@ -858,7 +858,13 @@ static size_t pass_b_smem(int L, int N1, int64_t M, int mode);
 static int split_n1(int64_t N) {
     int lg = 0;
     while ((int64_t(1) << lg) < N) lg++;
-    return 1 << (lg / 2);
+    // INFT_FFT_N1_SHIFT=k: N1 = 2^(floor(lg/2) - k) (experiment: wider pass-A column tiles)
+    static const int shift = [] {
+        const char* e = getenv("INFT_FFT_N1_SHIFT");
+        return e ? atoi(e) : 0;
+    }();
+    const int l1 = std::max(1, lg / 2 - shift);
+    return 1 << l1;
 }
 
 bool fused_fft_available(const Plan& p) {
@@ -1016,6 +1022,23 @@ static size_t pass_b_smem(int L, int N1, int64_t M, int mode) {
     return fft::d_offset<T>(L, ST, SW, TB) + (mode == 0 ? sizeof(T) * (size_t)(2 * B2 * DW) : 0) + 32;
 }
 
+// pass B of the inverse in place with 8192-element tiles (INFT_FFT_TILE_B=8192): 4 rows of 2048,
+// so each kept output column leaves as a 64-byte run instead of 32 (one CTA per SM)
+template <typename T>
+static bool pick_ip_b8(int L, PassBFn<T>& b, int& TF, int& ST, int& SW, int& NT) {
+#define INFT_IPG8(LL)                                                                                    \
+    TF = fft::Geo<T, LL, 8192>::TF, ST = fft::Geo<T, LL, 8192>::ST, SW = fft::Geo<T, LL, 8192>::SW,      \
+    NT = fft::Geo<T, LL, 8192>::NT;                                                                      \
+    b = fft::k_pass_b_ip<T, -1, 0, LL, 8192>;                                                            \
+    return true;
+    switch (L) {
+        case 1024: { INFT_IPG8(1024) }
+        case 2048: { INFT_IPG8(2048) }
+        default: return false;
+    }
+#undef INFT_IPG8
+}
+
 // in-place kernels and their geometry (Geo<T, L, kTileIP>) for the supported lengths
 template <typename T>
 static bool pick_ip(int mode, int L, bool pass_a, PassAFn<T>& a, PassBFn<T>& b, int& TF, int& ST, int& SW, int& NT) {
@@ -1135,7 +1158,13 @@ static void launch_pass_b(Plan& p, fft::Args<T>& A, int mode, int64_t R, cudaStr
     if (ipb && sizeof(T) == 8 && (mode == 0 || ipb1)) {
         PassAFn<T> unused = nullptr;
         int tf, st_, sw, nt;
-        if (pick_ip<T>(mode, L, false, unused, kip, tf, st_, sw, nt)) {
+        static const int tile_b = [] {
+            const char* e = getenv("INFT_FFT_TILE_B");
+            return e ? atoi(e) : 4096;
+        }();
+        if (mode == 0 && tile_b == 8192 && pick_ip_b8<T>(L, kip, tf, st_, sw, nt)) {
+            TB = tf, ST = st_, SW = sw, threads = nt;
+        } else if (pick_ip<T>(mode, L, false, unused, kip, tf, st_, sw, nt)) {
             TB = tf, ST = st_, SW = sw, threads = nt;
         } else {
             kip = nullptr;
