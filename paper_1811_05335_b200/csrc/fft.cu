@@ -213,6 +213,17 @@ constexpr int kTileElemsF = INFT_FFT_TILE_F;
 // in-place kernels: 4096-element tiles at both precisions (256 threads, <= 128 registers at two
 // CTAs per SM; complex64's 8192-element tiles would need 512 threads at 64 registers)
 constexpr int kTileIP = 4096;
+// in-place kernels: L2 prefetch of the next tile at the start of the current one
+#ifndef INFT_FFT_PREFETCH
+#define INFT_FFT_PREFETCH 1
+#endif
+constexpr bool kPrefetch = INFT_FFT_PREFETCH != 0;
+// pass A: off -- prefetching its strided column boxes slowed it (config 5: 0.825 -> 0.97 ms)
+// while pass B's contiguous rows gain (0.760 -> 0.735 ms)
+#ifndef INFT_FFT_PREFETCH_A
+#define INFT_FFT_PREFETCH_A 0
+#endif
+constexpr bool kPrefetchA = INFT_FFT_PREFETCH_A != 0;
 template <typename T>
 constexpr int tile_elems() { return sizeof(T) == 8 ? kTileElems : kTileElemsF; }
 constexpr int kLgRB = kRB == 16 ? 4 : (kRB == 8 ? 3 : 2);
@@ -516,6 +527,19 @@ __global__ void __launch_bounds__(Geo<T, L, kTileIP>::NT, 2)
     }
     for (int i = threadIdx.x; i < L / kRB; i += blockDim.x) tws[i] = A.tw1[i];
     __syncthreads();
+    // L2 prefetch of a tile's boxes (INFT_FFT_PREFETCH_A, off: slower here, see kPrefetchA): the
+    // in-place buffer can only take the next tile after the last stage has read it
+    auto prefetch = [&](int id) {
+        const int r = id / tiles_per_rhs, c0 = (id % tiles_per_rhs) * TA * CE;
+        if (MODE == 0) {
+            for (int q = 0; q < L; q += BR) tma_prefetch_3d(&map, c0, q, r);
+        } else {
+            for (int q = 0; q < B; q += BR) {
+                tma_prefetch_3d(&map, c0, B + q, r);
+                tma_prefetch_3d(&map, c0, q, r);
+            }
+        }
+    };
     auto issue = [&](int id) {
         const int r = id / tiles_per_rhs, c0 = (id % tiles_per_rhs) * TA * CE;
         mbar_arrive_expect_tx(bar, tile_bytes);
@@ -543,6 +567,7 @@ __global__ void __launch_bounds__(Geo<T, L, kTileIP>::NT, 2)
         const int e0 = n2l * jl, eq = n2l * (L / kRB);
         const C2<T> t0a = twid_g<T, SIGN>(A.tlo, e0 & lmask), t0b = twid_g<T, SIGN>(A.thi, e0 >> A.LB);
         const C2<T> tqa = twid_g<T, SIGN>(A.tlo, eq & lmask), tqb = twid_g<T, SIGN>(A.thi, eq >> A.LB);
+        if (kPrefetchA && threadIdx.x == 0 && id + (int)gridDim.x < ntiles) prefetch(id + (int)gridDim.x);
         mbar_wait(bar, it & 1);
         const T* dsm = reinterpret_cast<const T*>(buf + B * TA);
         auto load = [&](int f, int n1, int, int) -> C2<T> {
@@ -749,6 +774,12 @@ __global__ void __launch_bounds__(Geo<T, L, TE>::NT, TE == kTileIP ? 2 : 1)
             bulk_g2s(buf + f * S, src + r * src_stride + (int64_t)(row0 + f) * L, (uint32_t)(sizeof(C2<T>) * L),
                      &bars[0]);
     };
+    auto prefetch = [&](int id) {
+        const int64_t r = id / tiles_per_rhs;
+        const int row0 = (id % tiles_per_rhs) * TB;
+        for (int f = 0; f < TB; ++f)
+            bulk_prefetch_l2(src + r * src_stride + (int64_t)(row0 + f) * L, (uint32_t)(sizeof(C2<T>) * L));
+    };
     int it = 0;
     if (threadIdx.x == 0 && (int)blockIdx.x < ntiles) issue(blockIdx.x);
     for (int id = blockIdx.x; id < ntiles; id += gridDim.x, ++it) {
@@ -762,6 +793,7 @@ __global__ void __launch_bounds__(Geo<T, L, TE>::NT, TE == kTileIP ? 2 : 1)
                 tma_load_3d(dsm + (B2 + q) * DW, &dmap, dc0, q, 0, &bars[1]);
             }
         }
+        if (kPrefetch && threadIdx.x == 0 && id + (int)gridDim.x < ntiles) prefetch(id + (int)gridDim.x);
         mbar_wait(&bars[0], it & 1);
         C2<T>* grow = A.grid + r * A.GS;
         C2<T>* frow = A.fhat + r * A.M;

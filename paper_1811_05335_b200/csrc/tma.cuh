@@ -77,6 +77,20 @@ __device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, i
         : "memory");
 }
 
+// L2 prefetch of a 3-D tensor-map box (no shared-memory destination, no completion tracking):
+// warms L2 for a later tma_load_3d of the same box.
+__device__ __forceinline__ void tma_prefetch_3d(const CUtensorMap* map, int c0, int c1, int c2) {
+    asm volatile("cp.async.bulk.prefetch.tensor.3d.L2.global.tile [%0, {%1, %2, %3}];" ::"l"(
+                     reinterpret_cast<uint64_t>(map)),
+                 "r"(c0), "r"(c1), "r"(c2)
+                 : "memory");
+}
+
+// L2 prefetch of a contiguous global range (16-byte multiple).
+__device__ __forceinline__ void bulk_prefetch_l2(const void* src, uint32_t bytes) {
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes) : "memory");
+}
+
 // Per-thread asynchronous copy global -> shared of BYTES (4, 8 or 16) with zero fill when
 // src_bytes = 0 (LDGSTS); completion by cp_async_commit / cp_async_wait<N>.
 template <int BYTES>
