@@ -44,9 +44,9 @@ constexpr int kSideCarry = 4;  // next segment heavy: spill into s1 to a side sl
 constexpr int kNB = INFT_RING_NB;          // nodes per staged batch
 constexpr int kStages = INFT_RING_STAGES;  // spread load pipeline depth (2: more CTAs per SM beat a deeper pipe)
 #ifndef INFT_RING_STAGES_G
-#define INFT_RING_STAGES_G 3
+#define INFT_RING_STAGES_G 2
 #endif
-constexpr int kStagesG = INFT_RING_STAGES_G;  // gather window pipeline depth (config 5: 3 -> 0.993 ms, 2 -> 1.018)
+constexpr int kStagesG = INFT_RING_STAGES_G;  // gather window pipeline depth (config 5, aligned output ring: 2 -> 0.894 ms at 6 CTAs/SM, 3 -> 0.938 at 5)
 #ifndef INFT_RING_STAGES_GR
 #define INFT_RING_STAGES_GR 2
 #endif
@@ -386,6 +386,14 @@ __global__ void __launch_bounds__(128, INFT_RING_MINB) k_gather_ring(const __gri
     constexpr int CE = (int)sizeof(C2<T>) / 8;
     constexpr int SBOX = SEG / EB;  // window boxes per segment
     constexpr int OBOX = kNB / EB;  // output boxes per batch
+    // output staging ring of NR boxes: output column c (caller node order) lives in ring slot
+    // c mod RS, and only whole, 128-byte-aligned boxes of f leave by TMA store.  The sorted
+    // node order is a cyclic shift of the caller's (perm_shift, odd for config 5), so batch-
+    // aligned boxes started mid-sector: every 128-byte box row touched 5 sectors with two
+    // partial ones (ncu: 1.25x the write sectors, L2 read-modify-writes).  The columns before a
+    // run's first aligned box and after its last one are stored from the ring by plain stores.
+    constexpr int NR = OBOX + 1;
+    constexpr int RS = NR * EB;
     static_assert(SEG % EB == 0 && kNB % EB == 0, "tile shapes");
     const int N = (int)Nl;
     const int WPB = blockDim.x >> 5;
@@ -399,13 +407,13 @@ __global__ void __launch_bounds__(128, INFT_RING_MINB) k_gather_ring(const __gri
     const uint32_t wstage = (uint32_t)SBOX * WPB * 4096u;
     const uint32_t rstage = (uint32_t)((kNB * PP * (int)sizeof(T) + 127) & ~127);
     unsigned char* wbuf = smem;
-    unsigned char* stg = smem + kStagesG * wstage;  // [WPB][OBOX][32][128]
-    unsigned char* rbuf = stg + (size_t)WPB * OBOX * 4096u;
+    unsigned char* stg = smem + kStagesG * wstage;  // [WPB][NR][32][128]
+    unsigned char* rbuf = stg + (size_t)WPB * NR * 4096u;
     uint64_t* fullW = reinterpret_cast<uint64_t*>(rbuf + kStagesGR * rstage);
     uint64_t* emptyW = fullW + kStagesG;
     uint64_t* fullR = emptyW + kStagesG;
     uint64_t* emptyR = fullR + kStagesGR;
-    unsigned char* my_stg = stg + (size_t)warp * OBOX * 4096u;
+    unsigned char* my_stg = stg + (size_t)warp * NR * 4096u;
 
     // chunk = Q segments, or a node-balanced run of segments from the chunk table
     // chunk = Q segments, or an entry (s0, s1, first node, end node) of the gather's chunk
@@ -468,24 +476,21 @@ __global__ void __launch_bounds__(128, INFT_RING_MINB) k_gather_ring(const __gri
     T wx[K], wy[K];
     int nextL = 0;
     const uint32_t wrow = (uint32_t)warp * SBOX * 4096u;
-    // box L -> registers of half (L & 1)
-    auto consume_box = [&]() {
+    // box L -> registers of half H = L & 1, H a compile-time constant (static register
+    // indices: a run-time half made ptxas select every window register with FSEL, 2K extra
+    // instructions per box)
+    auto consume_box_h = [&](auto HC) {
+        constexpr int H = decltype(HC)::value;
         const int L = nextL++;
         const int stage = L % kStagesG;
         const uint32_t parity = (uint32_t)((L / kStagesG) & 1);
         mbar_wait(&fullW[stage], parity);
         const unsigned char* wb = wbuf + stage * wstage + wrow;
-        const int half = L & 1;
 #pragma unroll
         for (int v = 0; v < SEG; ++v) {
             const C2<T> g = *reinterpret_cast<const C2<T>*>(wb + cofs<T>(v, sw));
-            if (half) {
-                wx[SEG + v] = g.x;
-                wy[SEG + v] = g.y;
-            } else {
-                wx[v] = g.x;
-                wy[v] = g.y;
-            }
+            wx[H * SEG + v] = g.x;
+            wy[H * SEG + v] = g.y;
         }
         fence_proxy_async();
         __syncwarp();
@@ -495,12 +500,30 @@ __global__ void __launch_bounds__(128, INFT_RING_MINB) k_gather_ring(const __gri
             issueW(L + kStagesG, stage);
         }
     };
+    auto consume_box = [&]() {
+        if (nextL & 1)
+            consume_box_h(std::integral_constant<int, 1>{});
+        else
+            consume_box_h(std::integral_constant<int, 0>{});
+    };
     consume_box();
     consume_box();
     int cur_i = 0;  // window for segment s0 + cur_i: phase cur_i & 1
 
     C2<T>* __restrict__ fr = f + (int64_t)(active ? r : 0) * N;
     const int rstore = row0 + warp * 32;
+    // output run state (warp-uniform): a run is a stretch of consecutive output columns
+    // [run_start, run_next); boxes below box_next are stored, columns [run_start, plain_lo) too
+    int run_next = -1, run_start = 0, lead_end = 0, plain_lo = 0, box_next = 0;
+    auto ring_ofs = [&](int c) { return cofs<T>(c % RS, sw); };
+    auto store_plain = [&](int c0, int c1) {  // this lane's row, its own ring slots
+        if (active)
+            for (int c = c0; c < c1; ++c) fr[c] = *reinterpret_cast<const C2<T>*>(my_stg + ring_ofs(c));
+    };
+    auto end_run = [&]() {
+        const int c0 = max(plain_lo, box_next * EB);
+        if (run_next >= 0 && c0 < run_next) store_plain(c0, run_next);
+    };
     for (int b = 0; b < nbat; ++b) {
         const int stage = b % kStagesGR;
         const uint32_t parity = (uint32_t)((b / kStagesGR) & 1);
@@ -509,10 +532,19 @@ __global__ void __launch_bounds__(128, INFT_RING_MINB) k_gather_ring(const __gri
         mbar_wait(&fullR[stage], parity);
         const T* rec = reinterpret_cast<const T*>(rbuf + stage * rstage);
         const bool full_tile = cnt == kNB;
-        if (full_tile) {
-            if (lane == 0) bulk_wait_read<0>();
-            __syncwarp();
+        int col = pos + cshift;
+        if (col >= N) col -= N;
+        if (col != run_next) {  // a new run (chunk start, the wrap of the node order)
+            end_run();
+            run_start = col;
+            plain_lo = col;
+            box_next = (col + EB - 1) / EB;
+            lead_end = box_next * EB;
         }
+        const int cm = col % RS;  // ring slot of the batch's first output
+        // ring slots free: every earlier TMA store has read its box
+        if (lane == 0) bulk_wait_read<0>();
+        __syncwarp();
         bool dense = false;
         if constexpr (SEG == kNB) {
             if (full_tile) {
@@ -525,41 +557,87 @@ __global__ void __launch_bounds__(128, INFT_RING_MINB) k_gather_ring(const __gri
         int ncnt = cnt;
         if (dense) {
             const int seg = (int)((unsigned)rec_n0(rec, P) / SEG);
-            while (cur_i < seg - s0) {
-                consume_box();
-                ++cur_i;
+            const bool step1 = seg - s0 == cur_i + 1;
+            if (!step1) {
+                while (cur_i < seg - s0) {
+                    consume_box();
+                    ++cur_i;
+                }
             }
+            // Tap-major: the QG nodes of a group advance together one tap (vector of VEC
+            // weights) at a time, so 2 QG accumulation chains are independent (one chain per
+            // output in tap order, as the general path: bit-identical results).  Node-major
+            // order left 4 short chains per node and stalled on the FP64 latency at ~6 warps
+            // per SM (ncu: 'wait' 37 % of the stalls, FP64 pipe 29 %).
             auto dense_body = [&](auto PHC) {
                 constexpr int PH = decltype(PHC)::value;
-#pragma unroll
-                for (int q = 0; q < kNB; ++q) {
-                    T wv[P];
-                    WeightLoader<T, P>::load_smem(rec + q * PP, wv);
-#ifndef INFT_GATHER_CHAINS
-#define INFT_GATHER_CHAINS 2
+#ifndef INFT_GATHER_QG
+#define INFT_GATHER_QG 8
 #endif
-                    constexpr int NCH = INFT_GATHER_CHAINS;  // independent FMA chains per output
-                    T sx[NCH], sy[NCH];
+                constexpr int QG = INFT_GATHER_QG;  // nodes per group
+                static_assert(kNB % QG == 0, "node groups");
 #pragma unroll
-                    for (int c = 0; c < NCH; ++c) sx[c] = sy[c] = T(0);
+                for (int g0 = 0; g0 < kNB; g0 += QG) {
+                    T sx[QG], sy[QG];
 #pragma unroll
-                    for (int t = 0; t < P; ++t) {
-                        const int rg = (q + t + SEG * PH) % K;
-                        sx[t % NCH] = fma(wv[t], wx[rg], sx[t % NCH]);
-                        sy[t % NCH] = fma(wv[t], wy[rg], sy[t % NCH]);
+                    for (int qq = 0; qq < QG; ++qq) sx[qq] = sy[qq] = T(0);
+#pragma unroll
+                    for (int t0 = 0; t0 < P; t0 += VEC) {
+                        T wv[QG][VEC];
+#pragma unroll
+                        for (int qq = 0; qq < QG; ++qq) {
+                            // one broadcast vector load: weights t0 .. t0 + VEC - 1 of node g0 + qq
+                            // (slots past P - 1 are the record's tail, never used)
+                            if constexpr (VEC == 2) {
+                                const double2 a = *reinterpret_cast<const double2*>(rec + (g0 + qq) * PP + t0);
+                                wv[qq][0] = a.x;
+                                wv[qq][1] = a.y;
+                            } else {
+                                const float4 a = *reinterpret_cast<const float4*>(rec + (g0 + qq) * PP + t0);
+                                wv[qq][0] = a.x;
+                                wv[qq][1] = a.y;
+                                wv[qq][2] = a.z;
+                                wv[qq][3] = a.w;
+                            }
+                        }
+#pragma unroll
+                        for (int u = 0; u < VEC; ++u) {
+                            if (t0 + u < P) {
+#pragma unroll
+                                for (int qq = 0; qq < QG; ++qq) {
+                                    const int rg = (g0 + qq + t0 + u + SEG * PH) % K;
+                                    sx[qq] = fma(wv[qq][u], wx[rg], sx[qq]);
+                                    sy[qq] = fma(wv[qq][u], wy[rg], sy[qq]);
+                                }
+                            }
+                        }
                     }
 #pragma unroll
-                    for (int c = 1; c < NCH; ++c) {
-                        sx[0] += sx[c];
-                        sy[0] += sy[c];
+                    for (int qq = 0; qq < QG; ++qq) {
+                        const int sl = cm + g0 + qq;
+                        *reinterpret_cast<C2<T>*>(my_stg + cofs<T>(sl >= RS ? sl - RS : sl, sw)) = mk<T>(sx[qq], sy[qq]);
                     }
-                    *reinterpret_cast<C2<T>*>(my_stg + cofs<T>(q, sw)) = mk<T>(sx[0], sy[0]);
                 }
             };
-            if (cur_i & 1)
+            // the common case, the batch one segment past the window's first one: slide the
+            // window by one box into the half of the current phase (static indices), then run
+            // the body in the other phase
+            auto slide_body = [&](auto PHC) {
+                constexpr int PH = decltype(PHC)::value;
+                consume_box_h(std::integral_constant<int, PH>{});
+                ++cur_i;
+                dense_body(std::integral_constant<int, 1 - PH>{});
+            };
+            if (step1) {
+                if (cur_i & 1)
+                    slide_body(std::integral_constant<int, 1>{});
+                else
+                    slide_body(std::integral_constant<int, 0>{});
+            } else if (cur_i & 1) {
                 dense_body(std::integral_constant<int, 1>{});
-            else
+            } else {
                 dense_body(std::integral_constant<int, 0>{});
+            }
             ncnt = 0;
         }
         unsigned n0n = ncnt ? (unsigned)rec_n0(rec, P) : 0u;
@@ -592,42 +670,25 @@ __global__ void __launch_bounds__(128, INFT_RING_MINB) k_gather_ring(const __gri
                 default:
                     break;
             }
-            if (full_tile) {
-                *reinterpret_cast<C2<T>*>(my_stg + cofs<T>(q, sw)) = mk<T>(sx, sy);
-            } else if (active) {
-                int64_t j = (int64_t)pos + q + cshift;
-                if (j >= N) j -= N;
-                fr[j] = mk<T>(sx, sy);
-            }
+            const int sl = cm + q;
+            *reinterpret_cast<C2<T>*>(my_stg + cofs<T>(sl >= RS ? sl - RS : sl, sw)) = mk<T>(sx, sy);
         }
-        if (full_tile) {
-            int col = pos + cshift;
-            if (col >= N) col -= N;
-            if (CE == 2 || (col & 1) == 0) {
-                fence_proxy_async();
-                __syncwarp();
-                if (lane == 0) {
-#pragma unroll
-                    for (int bx = 0; bx < OBOX; ++bx)
-                        tma_store_2d(&omap, tcoord<CE>(col + bx * EB), rstore, my_stg + bx * 4096u);
-                    bulk_commit();
-                }
-            } else {
-                // complex64 batch starting on an odd node: a TMA store box may not start there
-                // (16-byte aligned innermost start).  Plain stores, two staged rows per
-                // instruction (16 consecutive nodes each) so that they stay coalesced.
-                static_assert(kNB == 16, "two 16-node rows per warp store");
-                __syncwarp();
-#pragma unroll
-                for (int i = 0; i < 16; ++i) {
-                    const int rho = 2 * i + (lane >> 4), q = lane & 15;
-                    const uint32_t swr = ((uint32_t)rho << 7) | ((uint32_t)(rho & 7) << 4);
-                    if (rstore + rho < R)
-                        f[(int64_t)(rstore + rho) * N + col + q] =
-                            *reinterpret_cast<const C2<T>*>(my_stg + cofs<T>(q, swr));
-                }
-            }
+        run_next = col + cnt;
+        if (plain_lo < lead_end) {  // the run's columns before its first aligned box
+            const int c1 = min(lead_end, run_next);
+            store_plain(plain_lo, c1);
+            plain_lo = c1;
         }
+        fence_proxy_async();
+        __syncwarp();
+        if (lane == 0 && (box_next + 1) * EB <= run_next) {
+            do {
+                tma_store_2d(&omap, tcoord<CE>(box_next * EB), rstore, my_stg + (box_next % NR) * 4096u);
+                ++box_next;
+            } while ((box_next + 1) * EB <= run_next);
+            bulk_commit();
+        }
+        box_next = __shfl_sync(0xffffffffu, box_next, 0);
         fence_proxy_async();
         __syncwarp();
         if (lane == 0) mbar_arrive(&emptyR[stage]);
@@ -636,6 +697,7 @@ __global__ void __launch_bounds__(128, INFT_RING_MINB) k_gather_ring(const __gri
             issueR(b + kStagesGR, stage);
         }
     }
+    end_run();
     while (nextL < nbox) consume_box();  // no copy may be in flight at exit
     if (lane == 0) bulk_wait<0>();
 }
@@ -733,7 +795,7 @@ template <typename T>
 static size_t ring_gather_smem(int wpb, int PP, int SEG) {
     const int EB = 128 / (int)sizeof(C2<T>);
     size_t wsz = (size_t)ring::kStagesG * (SEG / EB) * wpb * 4096;
-    size_t st = (size_t)wpb * (ring::kNB / EB) * 4096;
+    size_t st = (size_t)wpb * (ring::kNB / EB + 1) * 4096;  // output ring (NR boxes per warp)
     size_t r = (size_t)ring::kStagesGR * ((ring::kNB * PP * (int)sizeof(T) + 127) & ~127);
     return wsz + st + r + 2 * (ring::kStagesG + ring::kStagesGR) * sizeof(uint64_t);
 }
@@ -769,12 +831,29 @@ struct SpreadTable {
     int nchunks = 0, nfix = 0, nslots = 0;
 };
 
-static SpreadTable ring_spread_table(Plan& p, int64_t rowgroups, cudaStream_t st) {
+// Node target T per chunk.  Chunks close at T nodes or kQ segments; the launch has
+// rowgroups x chunks CTAs of about equal work, so the chunk count is rounded to whole waves of
+// resident CTAs (INFT_RING_WAVES=0: off) -- a last wave a fifth full cost the config-5 gather ~8 %
+// (9.2 waves of 888 CTAs).  T = ceil(N / C) makes the greedy closing produce at most C chunks.
+static int64_t ring_target_T(const Plan& p, int64_t rowgroups, const void* fn, int threads, size_t smem) {
     int dev = 0, nsm = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-    const int64_t want = std::max<int64_t>(1, (int64_t)nsm * ring_cps() / std::max<int64_t>(1, rowgroups));
-    const int64_t T = std::max<int64_t>(1, (p.N + want - 1) / want);
+    rowgroups = std::max<int64_t>(1, rowgroups);
+    const int64_t want = std::max<int64_t>(1, (int64_t)nsm * ring_cps() / rowgroups);
+    static const bool waves = [] {
+        const char* e = getenv("INFT_RING_WAVES");
+        return !(e && atoi(e) == 0);
+    }();
+    if (!waves || !fn) return std::max<int64_t>(1, (p.N + want - 1) / want);
+    const int64_t wave = (int64_t)nsm * std::max(1, occupancy_cached(fn, threads, smem));
+    int64_t C = std::max<int64_t>(want, ceil_div(p.nseg[0], (int64_t)ring::kQ));
+    const int64_t k = ceil_div(C * rowgroups, wave);
+    C = std::max<int64_t>(1, k * wave / rowgroups);
+    return std::max<int64_t>(1, (p.N + C - 1) / C);
+}
+
+static SpreadTable ring_spread_table(Plan& p, int64_t rowgroups, cudaStream_t st, int64_t T) {
     const int64_t key = (int64_t(1) << 40) + T;  // spread tables
     auto it = p.ring_chunk_cache.find(key);
     if (it == p.ring_chunk_cache.end()) {
@@ -870,12 +949,7 @@ static SpreadTable ring_spread_table(Plan& p, int64_t rowgroups, cudaStream_t st
 // Gather chunks (s0, s1, first node, end node): a segment holding more
 // than T nodes is split into node ranges of about T (each output is independent in the
 // gather; Chebyshev nodes put 651 of 32768 nodes in one segment of config 3).
-static const int32_t* ring_gather_chunks(Plan& p, int64_t rowgroups, int& nchunks, cudaStream_t st) {
-    int dev = 0, nsm = 148;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-    const int64_t want = std::max<int64_t>(1, (int64_t)nsm * ring_cps() / std::max<int64_t>(1, rowgroups));
-    const int64_t T = std::max<int64_t>(1, (p.N + want - 1) / want);
+static const int32_t* ring_gather_chunks(Plan& p, int& nchunks, cudaStream_t st, int64_t T) {
     const int64_t key = -1 - T;  // negative keys: gather tables
     auto it = p.ring_chunk_cache.find(key);
     if (it == p.ring_chunk_cache.end()) {
@@ -926,7 +1000,10 @@ static void ring_spread_t(Plan& p, const void* f, void* grid, int64_t R, cudaStr
     RingFns<T> F = ring_fns<T>(p.m);
     const int wpb = ring_wpb<T>(R);
     const int nseg = (int)p.nseg[0];
-    const SpreadTable tb = ring_spread_table(p, ceil_div(R, 32 * wpb), st);
+    const size_t smem = ring_spread_smem<T>(wpb, p.PP, p.S[0]);
+    ensure_smem_attr((const void*)F.spread, smem);
+    const SpreadTable tb = ring_spread_table(
+        p, ceil_div(R, 32 * wpb), st, ring_target_T(p, ceil_div(R, 32 * wpb), (const void*)F.spread, 32 * wpb, smem));
     const int nchunks = tb.nchunks;
     const int32_t* chunks = tb.chunks;
     const size_t side_bytes = sizeof(C2<T>) * (size_t)tb.nslots * (size_t)R * p.S[0];
@@ -938,8 +1015,6 @@ static void ring_spread_t(Plan& p, const void* f, void* grid, int64_t R, cudaStr
     CUtensorMap fm, gm;
     tmap_or_throw(&fm, f, (uint64_t)p.N * ce, (uint64_t)R, sizeof(C2<T>) * (uint64_t)p.N, 32u, "spread f");
     tmap_or_throw(&gm, grid, (uint64_t)p.GS * ce, (uint64_t)R, sizeof(C2<T>) * (uint64_t)p.GS, 32u, "spread grid");
-    size_t smem = ring_spread_smem<T>(wpb, p.PP, p.S[0]);
-    ensure_smem_attr((const void*)F.spread, smem);
     dim3 g((unsigned)ceil_div(R, 32 * wpb), (unsigned)nchunks);
     F.spread<<<g, 32 * wpb, smem, st>>>(fm, gm, p.seg_start.as<int32_t>(), chunks, p.w.as<T>(), p.PP, nseg, 0,
                                         (int)p.N, p.perm_shift, p.ring_side.as<C2<T>>(), (int)R);
@@ -971,7 +1046,10 @@ static void ring_gather_t(Plan& p, const void* grid, void* f, int64_t R, cudaStr
     const int wpb = ring_wpb<T>(R);
     const int nseg = (int)p.nseg[0];
     int nchunks = 0;
-    const int32_t* chunks = ring_gather_chunks(p, ceil_div(R, 32 * wpb), nchunks, st);
+    const size_t smem = ring_gather_smem<T>(wpb, p.PP, p.S[0]);
+    ensure_smem_attr((const void*)F.gather, smem);
+    const int32_t* chunks = ring_gather_chunks(
+        p, nchunks, st, ring_target_T(p, ceil_div(R, 32 * wpb), (const void*)F.gather, 32 * wpb, smem));
     const uint64_t ce = sizeof(C2<T>) / 8;
     const int H = (int)(p.GS - p.Ms[0]);
     k_ring_halo<T><<<(unsigned)std::max<int64_t>(1, std::min<int64_t>(ceil_div(R * H, 256), 4096)), 256, 0, st>>>(
@@ -980,9 +1058,21 @@ static void ring_gather_t(Plan& p, const void* grid, void* f, int64_t R, cudaStr
     p.launches++;
     CUtensorMap gm, om;
     tmap_or_throw(&gm, grid, (uint64_t)p.GS * ce, (uint64_t)R, sizeof(C2<T>) * (uint64_t)p.GS, 32u, "gather grid");
-    tmap_or_throw(&om, f, (uint64_t)p.N * ce, (uint64_t)R, sizeof(C2<T>) * (uint64_t)p.N, 32u, "gather f");
-    size_t smem = ring_gather_smem<T>(wpb, p.PP, p.S[0]);
-    ensure_smem_attr((const void*)F.gather, smem);
+    // experiment (timing only, the output is NOT the caller's): INFT_EXP_OSTRIDE=k stores the
+    // full batches into a scratch [R][N + k] array (row stride off the power of two)
+    static const int ostride = [] {
+        const char* e = getenv("INFT_EXP_OSTRIDE");
+        return e ? atoi(e) : 0;
+    }();
+    if (ostride > 0) {
+        static DevBuf scratch;
+        const size_t need = sizeof(C2<T>) * (size_t)R * (size_t)(p.N + ostride);
+        if (scratch.bytes < need) scratch.alloc(need);
+        tmap_or_throw(&om, scratch.p, (uint64_t)p.N * ce, (uint64_t)R, sizeof(C2<T>) * (uint64_t)(p.N + ostride), 32u,
+                      "gather f (experiment)");
+    } else {
+        tmap_or_throw(&om, f, (uint64_t)p.N * ce, (uint64_t)R, sizeof(C2<T>) * (uint64_t)p.N, 32u, "gather f");
+    }
     dim3 g((unsigned)ceil_div(R, 32 * wpb), (unsigned)nchunks);
     F.gather<<<g, 32 * wpb, smem, st>>>(gm, om, p.seg_start.as<int32_t>(), chunks, p.w.as<T>(), p.PP,
                                         static_cast<C2<T>*>(f), p.N, nseg, 0, (int)R, p.perm_shift);
