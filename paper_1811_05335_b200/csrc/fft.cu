@@ -84,6 +84,35 @@ __device__ __forceinline__ C2<T> rot16rt(C2<T> v, int e) {
     }
 }
 
+// cos(pi m / 16), m = 0..31
+__device__ __forceinline__ constexpr double c32(int m) {
+    constexpr double t[32] = {1.0, 0.98078528040323044913, 0.92387953251128675613, 0.83146961230254523708,
+                              0.70710678118654752440, 0.55557023301960222474, 0.38268343236508977173,
+                              0.19509032201612826785, 0.0, -0.19509032201612826785, -0.38268343236508977173,
+                              -0.55557023301960222474, -0.70710678118654752440, -0.83146961230254523708,
+                              -0.92387953251128675613, -0.98078528040323044913, -1.0, -0.98078528040323044913,
+                              -0.92387953251128675613, -0.83146961230254523708, -0.70710678118654752440,
+                              -0.55557023301960222474, -0.38268343236508977173, -0.19509032201612826785, 0.0,
+                              0.19509032201612826785, 0.38268343236508977173, 0.55557023301960222474,
+                              0.70710678118654752440, 0.83146961230254523708, 0.92387953251128675613,
+                              0.98078528040323044913};
+    return t[m & 31];
+}
+
+// a * e^{SIGN 2 pi i E / 32} (even exponents reduce to rot16)
+template <typename T, int SIGN, int E>
+__device__ __forceinline__ C2<T> rot32(C2<T> a) {
+    constexpr int e = ((E % 32) + 32) % 32;
+    if constexpr (e % 2 == 0) {
+        return rot16<T, SIGN, e / 2>(a);
+    } else {
+        // cos(2 pi e / 32) = cos(pi e / 16);  sin(2 pi e / 32) = cos(pi (8 - e) / 16)
+        const T co = (T)c32(e);
+        const T si = (T)(SIGN * c32(8 - e));
+        return mk<T>(fma(a.x, co, -a.y * si), fma(a.x, si, a.y * co));
+    }
+}
+
 // DFT4 in place: X_k = sum_n x_n (SIGN i)^{nk}
 template <typename T, int SIGN>
 __device__ __forceinline__ void dft4(C2<T>& x0, C2<T>& x1, C2<T>& x2, C2<T>& x3) {
@@ -100,8 +129,43 @@ __device__ __forceinline__ void dft4(C2<T>& x0, C2<T>& x1, C2<T>& x2, C2<T>& x3)
 //   X[Q k1 + k2] = sum_{n1} w_P^{n1 k1} w_R^{n1 k2} sum_{n2} x[n1 + P n2] w_Q^{n2 k2}
 // (Q = 4 inner DFT4s, twiddles, P-point outer DFTs); every index is static.
 template <typename T, int SIGN, int R>
+__device__ __forceinline__ void dft_reg(C2<T> (&a)[R]);
+
+// 32-point DFT as 8 x 4: n = n1 + 8 n2, k = 4 k1 + k2:
+//   X[4 k1 + k2] = sum_{n1} w_8^{n1 k1} w_32^{n1 k2} sum_{n2} x[n1 + 8 n2] w_4^{n2 k2}
+template <typename T, int SIGN>
+__device__ __forceinline__ void dft32(C2<T> (&a)[32]) {
+    C2<T> y[8][4];
+#pragma unroll
+    for (int n1 = 0; n1 < 8; ++n1) {
+        C2<T> x0 = a[n1], x1 = a[n1 + 8], x2 = a[n1 + 16], x3 = a[n1 + 24];
+        dft4<T, SIGN>(x0, x1, x2, x3);
+        y[n1][0] = x0;
+        y[n1][1] = x1;
+        y[n1][2] = x2;
+        y[n1][3] = x3;
+    }
+#define INFT_R32_TW(N1, K2) y[N1][K2] = rot32<T, SIGN, (N1) * (K2)>(y[N1][K2]);
+#define INFT_R32_ROW(N1) INFT_R32_TW(N1, 1) INFT_R32_TW(N1, 2) INFT_R32_TW(N1, 3)
+    INFT_R32_ROW(1) INFT_R32_ROW(2) INFT_R32_ROW(3) INFT_R32_ROW(4) INFT_R32_ROW(5) INFT_R32_ROW(6) INFT_R32_ROW(7)
+#undef INFT_R32_ROW
+#undef INFT_R32_TW
+#pragma unroll
+    for (int k2 = 0; k2 < 4; ++k2) {
+        C2<T> z[8];
+#pragma unroll
+        for (int n1 = 0; n1 < 8; ++n1) z[n1] = y[n1][k2];
+        dft_reg<T, SIGN, 8>(z);
+#pragma unroll
+        for (int k1 = 0; k1 < 8; ++k1) a[4 * k1 + k2] = z[k1];
+    }
+}
+
+template <typename T, int SIGN, int R>
 __device__ __forceinline__ void dft_reg(C2<T> (&a)[R]) {
-    if constexpr (R == 2) {
+    if constexpr (R == 32) {
+        dft32<T, SIGN>(a);
+    } else if constexpr (R == 2) {
         const C2<T> t = a[0];
         a[0] = cadd<T>(t, a[1]);
         a[1] = csub<T>(t, a[1]);
@@ -214,6 +278,12 @@ constexpr int kTileElemsF = INFT_FFT_TILE_F;
 // CTAs per SM; complex64's 8192-element tiles would need 512 threads at 64 registers)
 constexpr int kTileIP = 4096;
 // in-place kernels: L2 prefetch of the next tile at the start of the current one
+// experiment (timing only, wrong results): INFT_EXP_NOLOAD=1 -- the in-place passes skip their
+// tile loads (compute + stores only)
+#ifndef INFT_EXP_NOLOAD
+#define INFT_EXP_NOLOAD 0
+#endif
+constexpr bool kNoLoad = INFT_EXP_NOLOAD != 0;
 #ifndef INFT_FFT_PREFETCH
 #define INFT_FFT_PREFETCH 1
 #endif
@@ -226,7 +296,7 @@ constexpr bool kPrefetch = INFT_FFT_PREFETCH != 0;
 constexpr bool kPrefetchA = INFT_FFT_PREFETCH_A != 0;
 template <typename T>
 constexpr int tile_elems() { return sizeof(T) == 8 ? kTileElems : kTileElemsF; }
-constexpr int kLgRB = kRB == 16 ? 4 : (kRB == 8 ? 3 : 2);
+constexpr int kLgRB = kRB == 32 ? 5 : (kRB == 16 ? 4 : (kRB == 8 ? 3 : 2));
 // TF independent length-L transforms per tile (compile-time: ~64 KB of shared memory, at
 // most 256 threads = TF L / 16, at most 8), thread t -> (f = t % TF, butterfly j = t / TF).
 // Static radix plan for L = 2^K: a first stage of radix 2^(K mod 4) (if any), then radix-16.
@@ -501,13 +571,13 @@ __global__ void __launch_bounds__(Geo<T, L>::NT, 1)
 // Pass A in place (MODE 0 inverse, MODE 1 adjoint; same data flow as k_pass_a): one buffer
 // of max(L TA, SW TA) elements per CTA, two CTAs per SM (config 5 pass A MODE 0: 0.886 ->
 // 0.826 ms against the double-buffered one-CTA kernel).
-template <typename T, int SIGN, int MODE, int L>
-__global__ void __launch_bounds__(Geo<T, L, kTileIP>::NT, 2)
+template <typename T, int SIGN, int MODE, int L, int TE = kTileIP>
+__global__ void __launch_bounds__(Geo<T, L, TE>::NT, TE == kTileIP ? 2 : 4)
     k_pass_a_ip(const __grid_constant__ CUtensorMap map, const __grid_constant__ CUtensorMap dmap, Args<T> A, int BR,
                 int ntiles) {
     extern __shared__ __align__(128) unsigned char smraw[];
     constexpr int CE = (int)(sizeof(C2<T>) / 8);
-    using G = Geo<T, L, kTileIP>;
+    using G = Geo<T, L, TE>;
     constexpr int TA = G::TF, S = G::SW;
     constexpr int BUF = (L * TA > S * TA ? L * TA : S * TA);
     C2<T>* buf = reinterpret_cast<C2<T>*>(smraw);
@@ -559,7 +629,7 @@ __global__ void __launch_bounds__(Geo<T, L, kTileIP>::NT, 2)
     const int fl = threadIdx.x % TA, jl = threadIdx.x < TA * (L / kRB) ? threadIdx.x / TA : 0;
     const int lmask = (1 << A.LB) - 1;
     int it = 0;
-    if (threadIdx.x == 0 && (int)blockIdx.x < ntiles) issue(blockIdx.x);
+    if (!kNoLoad && threadIdx.x == 0 && (int)blockIdx.x < ntiles) issue(blockIdx.x);
     for (int id = blockIdx.x; id < ntiles; id += gridDim.x, ++it) {
         const int64_t r = id / tiles_per_rhs;
         const int col0 = (id % tiles_per_rhs) * TA;
@@ -568,7 +638,7 @@ __global__ void __launch_bounds__(Geo<T, L, kTileIP>::NT, 2)
         const C2<T> t0a = twid_g<T, SIGN>(A.tlo, e0 & lmask), t0b = twid_g<T, SIGN>(A.thi, e0 >> A.LB);
         const C2<T> tqa = twid_g<T, SIGN>(A.tlo, eq & lmask), tqb = twid_g<T, SIGN>(A.thi, eq >> A.LB);
         if (kPrefetchA && threadIdx.x == 0 && id + (int)gridDim.x < ntiles) prefetch(id + (int)gridDim.x);
-        mbar_wait(bar, it & 1);
+        if (!kNoLoad) mbar_wait(bar, it & 1);
         const T* dsm = reinterpret_cast<const T*>(buf + B * TA);
         auto load = [&](int f, int n1, int, int) -> C2<T> {
             if (MODE == 0) return buf[n1 * TA + f];
@@ -590,7 +660,7 @@ __global__ void __launch_bounds__(Geo<T, L, kTileIP>::NT, 2)
         };
         const int nxt = id + (int)gridDim.x;
         auto on_free = [&]() {
-            if (threadIdx.x == 0 && nxt < ntiles) issue(nxt);
+            if (!kNoLoad && threadIdx.x == 0 && nxt < ntiles) issue(nxt);
         };
         fft_stages_ip<T, SIGN, G, 0, 1>(tws, buf, load, store, on_free);
     }
@@ -740,7 +810,7 @@ __global__ void __launch_bounds__(Geo<T, L>::NT, 1)
 // buffer (MODE 0), two CTAs per SM, plain stores from registers (the staged TMA stores of
 // k_pass_b would hold the buffer the next tile lands in).
 template <typename T, int SIGN, int MODE, int L, int TE = kTileIP>
-__global__ void __launch_bounds__(Geo<T, L, TE>::NT, TE == kTileIP ? 2 : 1)
+__global__ void __launch_bounds__(Geo<T, L, TE>::NT, TE == kTileIP ? 2 : (TE < kTileIP ? 4 : 1))
     k_pass_b_ip(const __grid_constant__ CUtensorMap dmap, const __grid_constant__ CUtensorMap omap, Args<T> A,
                 int BRd, int BRo, int ntiles) {
     extern __shared__ __align__(128) unsigned char smraw[];
@@ -781,7 +851,7 @@ __global__ void __launch_bounds__(Geo<T, L, TE>::NT, TE == kTileIP ? 2 : 1)
             bulk_prefetch_l2(src + r * src_stride + (int64_t)(row0 + f) * L, (uint32_t)(sizeof(C2<T>) * L));
     };
     int it = 0;
-    if (threadIdx.x == 0 && (int)blockIdx.x < ntiles) issue(blockIdx.x);
+    if (!kNoLoad && threadIdx.x == 0 && (int)blockIdx.x < ntiles) issue(blockIdx.x);
     for (int id = blockIdx.x; id < ntiles; id += gridDim.x, ++it) {
         const int64_t r = id / tiles_per_rhs;
         const int row0 = (id % tiles_per_rhs) * TB;
@@ -794,7 +864,7 @@ __global__ void __launch_bounds__(Geo<T, L, TE>::NT, TE == kTileIP ? 2 : 1)
             }
         }
         if (kPrefetch && threadIdx.x == 0 && id + (int)gridDim.x < ntiles) prefetch(id + (int)gridDim.x);
-        mbar_wait(&bars[0], it & 1);
+        if (!kNoLoad) mbar_wait(&bars[0], it & 1);
         C2<T>* grow = A.grid + r * A.GS;
         C2<T>* frow = A.fhat + r * A.M;
         auto load = [&](int f, int n2, int, int) -> C2<T> { return buf[f * S + n2]; };
@@ -834,7 +904,7 @@ __global__ void __launch_bounds__(Geo<T, L, TE>::NT, TE == kTileIP ? 2 : 1)
         };
         const int nxt = id + (int)gridDim.x;
         auto on_free = [&]() {
-            if (MODE == 0 && threadIdx.x == 0 && nxt < ntiles) issue(nxt);
+            if (!kNoLoad && MODE == 0 && threadIdx.x == 0 && nxt < ntiles) issue(nxt);
         };
         fft_stages_ip<T, SIGN, G, 0, 1>(tws, buf, load, store, on_free);
         if (MODE == 0) {
@@ -1071,14 +1141,16 @@ static bool pick_ip_b8(int L, PassBFn<T>& b, int& TF, int& ST, int& SW, int& NT)
 #undef INFT_IPG8
 }
 
-// in-place kernels and their geometry (Geo<T, L, kTileIP>) for the supported lengths
-template <typename T>
-static bool pick_ip(int mode, int L, bool pass_a, PassAFn<T>& a, PassBFn<T>& b, int& TF, int& ST, int& SW, int& NT) {
+// in-place kernels and their geometry (Geo<T, L, TE>) for the supported lengths; TE = 4096
+// (two CTAs per SM) or 2048 (half-size tiles, four CTAs per SM)
+template <typename T, int TE>
+static bool pick_ip_te(int mode, int L, bool pass_a, PassAFn<T>& a, PassBFn<T>& b, int& TF, int& ST, int& SW,
+                       int& NT) {
 #define INFT_IPG(LL)                                                                                          \
-    TF = fft::Geo<T, LL, fft::kTileIP>::TF, ST = fft::Geo<T, LL, fft::kTileIP>::ST,                           \
-    SW = fft::Geo<T, LL, fft::kTileIP>::SW, NT = fft::Geo<T, LL, fft::kTileIP>::NT;                           \
-    if (pass_a) a = mode == 0 ? fft::k_pass_a_ip<T, -1, 0, LL> : fft::k_pass_a_ip<T, 1, 1, LL>;                \
-    else b = mode == 0 ? fft::k_pass_b_ip<T, -1, 0, LL> : fft::k_pass_b_ip<T, 1, 1, LL>;                        \
+    TF = fft::Geo<T, LL, TE>::TF, ST = fft::Geo<T, LL, TE>::ST, SW = fft::Geo<T, LL, TE>::SW,                 \
+    NT = fft::Geo<T, LL, TE>::NT;                                                                             \
+    if (pass_a) a = mode == 0 ? fft::k_pass_a_ip<T, -1, 0, LL, TE> : fft::k_pass_a_ip<T, 1, 1, LL, TE>;        \
+    else b = mode == 0 ? fft::k_pass_b_ip<T, -1, 0, LL, TE> : fft::k_pass_b_ip<T, 1, 1, LL, TE>;                \
     return true;
     switch (L) {
         case 128: { INFT_IPG(128) }
@@ -1090,6 +1162,25 @@ static bool pick_ip(int mode, int L, bool pass_a, PassAFn<T>& a, PassBFn<T>& b, 
         default: return false;
     }
 #undef INFT_IPG
+}
+
+// tile size of the in-place kernels (INFT_FFT_TE_A / INFT_FFT_TE_B = 2048 or 4096)
+static int ip_te(bool pass_a) {
+    static const int ta = [] {
+        const char* e = getenv("INFT_FFT_TE_A");
+        return e && atoi(e) == 2048 ? 2048 : 4096;
+    }();
+    static const int tb = [] {
+        const char* e = getenv("INFT_FFT_TE_B");
+        return e && atoi(e) == 2048 ? 2048 : 4096;
+    }();
+    return pass_a ? ta : tb;
+}
+
+template <typename T>
+static bool pick_ip(int mode, int L, bool pass_a, PassAFn<T>& a, PassBFn<T>& b, int& TF, int& ST, int& SW, int& NT) {
+    if (ip_te(pass_a) == 2048) return pick_ip_te<T, 2048>(mode, L, pass_a, a, b, TF, ST, SW, NT);
+    return pick_ip_te<T, fft::kTileIP>(mode, L, pass_a, a, b, TF, ST, SW, NT);
 }
 
 // pass A over `src` (MODE 0: the grid, rows GS; MODE 1: h, rows M)
