@@ -288,41 +288,48 @@ constexpr bool kNoLoad = INFT_EXP_NOLOAD != 0;
 #define INFT_FFT_PREFETCH 1
 #endif
 constexpr bool kPrefetch = INFT_FFT_PREFETCH != 0;
-// pass A: off -- prefetching its strided column boxes slowed it (config 5: 0.825 -> 0.97 ms)
-// while pass B's contiguous rows gain (0.760 -> 0.735 ms)
+// pass A, L2 prefetch of the next tile at the start of the current one: on for the adjoint
+// (MODE 1: band rows of h; config 5: 0.742 -> 0.720 ms), off for the inverse (MODE 0: the whole
+// strided column tile; 0.826 -> 0.96 ms with it)
 #ifndef INFT_FFT_PREFETCH_A
 #define INFT_FFT_PREFETCH_A 0
 #endif
+#ifndef INFT_FFT_PREFETCH_A1
+#define INFT_FFT_PREFETCH_A1 1
+#endif
 constexpr bool kPrefetchA = INFT_FFT_PREFETCH_A != 0;
+constexpr bool kPrefetchA1 = INFT_FFT_PREFETCH_A1 != 0;
 template <typename T>
 constexpr int tile_elems() { return sizeof(T) == 8 ? kTileElems : kTileElemsF; }
 constexpr int kLgRB = kRB == 32 ? 5 : (kRB == 16 ? 4 : (kRB == 8 ? 3 : 2));
 // TF independent length-L transforms per tile (compile-time: ~64 KB of shared memory, at
 // most 256 threads = TF L / 16, at most 8), thread t -> (f = t % TF, butterfly j = t / TF).
 // Static radix plan for L = 2^K: a first stage of radix 2^(K mod 4) (if any), then radix-16.
-template <typename T, int L, int TE_ = 0>
+template <typename T, int L, int TE_ = 0, int RB_ = kRB>
 struct Geo {
+    static constexpr int RB = RB_;  // radix of the bulk stages
+    static constexpr int LgRB = RB == 32 ? 5 : (RB == 16 ? 4 : (RB == 8 ? 3 : 2));
     static constexpr int TE = TE_ > 0 ? TE_ : tile_elems<T>();
     static constexpr int TF = L >= TE / 8 ? (TE / L > 0 ? TE / L : 1) : 8;
-    static constexpr int NT = TF * L / kRB < 32 ? 32 : TF * L / kRB;  // threads per CTA
+    static constexpr int NT = TF * L / RB < 32 ? 32 : TF * L / RB;  // threads per CTA
     // row padding of the [f][L + PAD] layout: the lanes of one 128-byte shared wavefront cover
     // TF transforms x (wavefront / TF) consecutive positions
     static constexpr int WAVE = (int)(128 / sizeof(C2<T>));
     static constexpr int PAD = WAVE / TF > 1 ? WAVE / TF : 1;
     static constexpr int ST = L + PAD;  // row stride of pass B's bulk-copied tile rows
     static constexpr int K = __builtin_ctz(L);
-    static constexpr int R0 = 1 << (K % kLgRB);
-    static constexpr int RF = R0 > 1 ? R0 : kRB;  // radix of the first stage
-    static constexpr int PER0 = kRB / RF;         // butterflies per thread in the first stage
-    static constexpr int NST = K / kLgRB + (R0 > 1 ? 1 : 0);
-    static constexpr int LR = L / kRB;            // span of the last stage = twiddle table size
+    static constexpr int R0 = 1 << (K % LgRB);
+    static constexpr int RF = R0 > 1 ? R0 : RB;  // radix of the first stage
+    static constexpr int PER0 = RB / RF;         // butterflies per thread in the first stage
+    static constexpr int NST = K / LgRB + (R0 > 1 ? 1 : 0);
+    static constexpr int LR = L / RB;            // span of the last stage = twiddle table size
     // work buffer rows: position p lives at p + p / SKD with SKD = RF (one skew slot per
     // first-stage butterfly, so the first stage's strided writes RF j + m spread over the
     // banks) when one wavefront spans several butterflies of a transform (PAD > 1); row
     // stride SW = PAD (mod WAVE) like ST
     // (radix-8 build: one slot per 8 positions -- conflict-free for first-stage radices 2..8
     //  at 12.5 % extra rows, which keeps pass B of M_sigma = 2^21 inside 227 KB)
-    static constexpr int SKD = kRB == 8 ? (PAD > 1 ? 8 : L) : ((PAD > 1 && RF >= 4) ? RF : L);  // skew divisor (L: none)
+    static constexpr int SKD = RB == 8 ? (PAD > 1 ? 8 : L) : ((PAD > 1 && RF >= 4) ? RF : L);  // skew divisor (L: none)
     static constexpr int SW0 = L + L / SKD;
     static constexpr int SW = SW0 + ((PAD - SW0 % WAVE) % WAVE + WAVE) % WAVE;
 };
@@ -447,7 +454,7 @@ __device__ __forceinline__ void run_stage_ip(const C2<T>* tw, C2<T>* sm, Load&& 
 template <typename T, int SIGN, typename G, int SI, int NS, typename Load, typename Store, typename Free>
 __device__ __forceinline__ void fft_stages_ip(const C2<T>* tw, C2<T>* sm, Load&& load, Store&& store, Free&& on_free) {
     if constexpr (SI < G::NST) {
-        constexpr int R = (SI == 0) ? G::RF : kRB;
+        constexpr int R = (SI == 0) ? G::RF : G::RB;
         run_stage_ip<T, SIGN, G, R, NS, SI>(tw, sm, load, store, on_free);
         fft_stages_ip<T, SIGN, G, SI + 1, NS * R>(tw, sm, load, store, on_free);
     }
@@ -571,18 +578,21 @@ __global__ void __launch_bounds__(Geo<T, L>::NT, 1)
 // Pass A in place (MODE 0 inverse, MODE 1 adjoint; same data flow as k_pass_a): one buffer
 // of max(L TA, SW TA) elements per CTA, two CTAs per SM (config 5 pass A MODE 0: 0.886 ->
 // 0.826 ms against the double-buffered one-CTA kernel).
-template <typename T, int SIGN, int MODE, int L, int TE = kTileIP>
-__global__ void __launch_bounds__(Geo<T, L, TE>::NT, TE == kTileIP ? 2 : 4)
+#ifndef INFT_R32_MINB
+#define INFT_R32_MINB 2
+#endif
+template <typename T, int SIGN, int MODE, int L, int TE = kTileIP, int RB = kRB>
+__global__ void __launch_bounds__(Geo<T, L, TE, RB>::NT, TE == kTileIP ? (RB == 32 ? INFT_R32_MINB : 2) : 4)
     k_pass_a_ip(const __grid_constant__ CUtensorMap map, const __grid_constant__ CUtensorMap dmap, Args<T> A, int BR,
                 int ntiles) {
     extern __shared__ __align__(128) unsigned char smraw[];
     constexpr int CE = (int)(sizeof(C2<T>) / 8);
-    using G = Geo<T, L, TE>;
+    using G = Geo<T, L, TE, RB>;
     constexpr int TA = G::TF, S = G::SW;
     constexpr int BUF = (L * TA > S * TA ? L * TA : S * TA);
     C2<T>* buf = reinterpret_cast<C2<T>*>(smraw);
     C2<T>* tws = buf + BUF;
-    uint64_t* bar = reinterpret_cast<uint64_t*>(tws + L / kRB);
+    uint64_t* bar = reinterpret_cast<uint64_t*>(tws + L / RB);
     const int N2 = A.N2;
     const int tiles_per_rhs = N2 / TA;
     const int B = (int)(A.M / 2 / N2);  // band rows on each side (MODE 1)
@@ -595,7 +605,7 @@ __global__ void __launch_bounds__(Geo<T, L, TE>::NT, TE == kTileIP ? 2 : 4)
         mbar_init(bar, 1);
         fence_barrier_init();
     }
-    for (int i = threadIdx.x; i < L / kRB; i += blockDim.x) tws[i] = A.tw1[i];
+    for (int i = threadIdx.x; i < L / RB; i += blockDim.x) tws[i] = A.tw1[i];
     __syncthreads();
     // L2 prefetch of a tile's boxes (INFT_FFT_PREFETCH_A, off: slower here, see kPrefetchA): the
     // in-place buffer can only take the next tile after the last stage has read it
@@ -626,7 +636,7 @@ __global__ void __launch_bounds__(Geo<T, L, TE>::NT, TE == kTileIP ? 2 : 4)
             }
         }
     };
-    const int fl = threadIdx.x % TA, jl = threadIdx.x < TA * (L / kRB) ? threadIdx.x / TA : 0;
+    const int fl = threadIdx.x % TA, jl = threadIdx.x < TA * (L / RB) ? threadIdx.x / TA : 0;
     const int lmask = (1 << A.LB) - 1;
     int it = 0;
     if (!kNoLoad && threadIdx.x == 0 && (int)blockIdx.x < ntiles) issue(blockIdx.x);
@@ -634,10 +644,11 @@ __global__ void __launch_bounds__(Geo<T, L, TE>::NT, TE == kTileIP ? 2 : 4)
         const int64_t r = id / tiles_per_rhs;
         const int col0 = (id % tiles_per_rhs) * TA;
         const int n2l = col0 + fl;
-        const int e0 = n2l * jl, eq = n2l * (L / kRB);
+        const int e0 = n2l * jl, eq = n2l * (L / RB);
         const C2<T> t0a = twid_g<T, SIGN>(A.tlo, e0 & lmask), t0b = twid_g<T, SIGN>(A.thi, e0 >> A.LB);
         const C2<T> tqa = twid_g<T, SIGN>(A.tlo, eq & lmask), tqb = twid_g<T, SIGN>(A.thi, eq >> A.LB);
-        if (kPrefetchA && threadIdx.x == 0 && id + (int)gridDim.x < ntiles) prefetch(id + (int)gridDim.x);
+        if ((MODE == 1 ? kPrefetchA1 : kPrefetchA) && threadIdx.x == 0 && id + (int)gridDim.x < ntiles)
+            prefetch(id + (int)gridDim.x);
         if (!kNoLoad) mbar_wait(bar, it & 1);
         const T* dsm = reinterpret_cast<const T*>(buf + B * TA);
         auto load = [&](int f, int n1, int, int) -> C2<T> {
@@ -809,12 +820,12 @@ __global__ void __launch_bounds__(Geo<T, L>::NT, 1)
 // Pass B in place (complex128): one buffer of max(ST TB, SW TB) elements plus the d side
 // buffer (MODE 0), two CTAs per SM, plain stores from registers (the staged TMA stores of
 // k_pass_b would hold the buffer the next tile lands in).
-template <typename T, int SIGN, int MODE, int L, int TE = kTileIP>
-__global__ void __launch_bounds__(Geo<T, L, TE>::NT, TE == kTileIP ? 2 : (TE < kTileIP ? 4 : 1))
+template <typename T, int SIGN, int MODE, int L, int TE = kTileIP, int RB = kRB>
+__global__ void __launch_bounds__(Geo<T, L, TE, RB>::NT, TE == kTileIP ? (RB == 32 ? INFT_R32_MINB : 2) : (TE < kTileIP ? 4 : 1))
     k_pass_b_ip(const __grid_constant__ CUtensorMap dmap, const __grid_constant__ CUtensorMap omap, Args<T> A,
                 int BRd, int BRo, int ntiles) {
     extern __shared__ __align__(128) unsigned char smraw[];
-    using G = Geo<T, L, TE>;
+    using G = Geo<T, L, TE, RB>;
     constexpr int TB = G::TF, S = G::ST, SW = G::SW;
     constexpr int BUF = (S * TB > SW * TB ? S * TB : SW * TB);
     constexpr int DW = (int)(16 / sizeof(T)) > TB ? (int)(16 / sizeof(T)) : TB;
@@ -823,7 +834,7 @@ __global__ void __launch_bounds__(Geo<T, L, TE>::NT, TE == kTileIP ? 2 : (TE < k
     const int B2 = (int)(half / N1);
     C2<T>* buf = reinterpret_cast<C2<T>*>(smraw);
     C2<T>* tws = buf + BUF;
-    T* dsm = reinterpret_cast<T*>(smraw + ((sizeof(C2<T>) * (size_t)(BUF + L / kRB) + 127) / 128 * 128));
+    T* dsm = reinterpret_cast<T*>(smraw + ((sizeof(C2<T>) * (size_t)(BUF + L / RB) + 127) / 128 * 128));
     uint64_t* bars = reinterpret_cast<uint64_t*>(dsm + (MODE == 0 ? 2 * B2 * DW : 0));
     const int tiles_per_rhs = N1 / TB;
     const C2<T>* src = (MODE == 0) ? A.grid : A.ybuf;
@@ -834,7 +845,7 @@ __global__ void __launch_bounds__(Geo<T, L, TE>::NT, TE == kTileIP ? 2 : (TE < k
         mbar_init(&bars[1], 1);
         fence_barrier_init();
     }
-    for (int i = threadIdx.x; i < L / kRB; i += blockDim.x) tws[i] = A.tw2[i];
+    for (int i = threadIdx.x; i < L / RB; i += blockDim.x) tws[i] = A.tw2[i];
     __syncthreads();
     auto issue = [&](int id) {
         const int64_t r = id / tiles_per_rhs;
@@ -868,7 +879,7 @@ __global__ void __launch_bounds__(Geo<T, L, TE>::NT, TE == kTileIP ? 2 : (TE < k
         C2<T>* grow = A.grid + r * A.GS;
         C2<T>* frow = A.fhat + r * A.M;
         auto load = [&](int f, int n2, int, int) -> C2<T> { return buf[f * S + n2]; };
-        constexpr int NsL = L / kRB;
+        constexpr int NsL = L / RB;
         const bool fastband = (B2 % NsL) == 0;
         const int mlo = B2 / NsL;
         const int jl = threadIdx.x / TB, fl = threadIdx.x - (threadIdx.x / TB) * TB;
@@ -881,7 +892,7 @@ __global__ void __launch_bounds__(Geo<T, L, TE>::NT, TE == kTileIP ? 2 : (TE < k
                 if (fastband) {
                     if (m < mlo)
                         sr = jl + m * NsL;
-                    else if (m >= kRB - mlo)
+                    else if (m >= RB - mlo)
                         sr = jl + m * NsL - (L - 2 * B2);
                     else
                         return;
@@ -1143,14 +1154,14 @@ static bool pick_ip_b8(int L, PassBFn<T>& b, int& TF, int& ST, int& SW, int& NT)
 
 // in-place kernels and their geometry (Geo<T, L, TE>) for the supported lengths; TE = 4096
 // (two CTAs per SM) or 2048 (half-size tiles, four CTAs per SM)
-template <typename T, int TE>
+template <typename T, int TE, int RB>
 static bool pick_ip_te(int mode, int L, bool pass_a, PassAFn<T>& a, PassBFn<T>& b, int& TF, int& ST, int& SW,
                        int& NT) {
 #define INFT_IPG(LL)                                                                                          \
-    TF = fft::Geo<T, LL, TE>::TF, ST = fft::Geo<T, LL, TE>::ST, SW = fft::Geo<T, LL, TE>::SW,                 \
-    NT = fft::Geo<T, LL, TE>::NT;                                                                             \
-    if (pass_a) a = mode == 0 ? fft::k_pass_a_ip<T, -1, 0, LL, TE> : fft::k_pass_a_ip<T, 1, 1, LL, TE>;        \
-    else b = mode == 0 ? fft::k_pass_b_ip<T, -1, 0, LL, TE> : fft::k_pass_b_ip<T, 1, 1, LL, TE>;                \
+    TF = fft::Geo<T, LL, TE, RB>::TF, ST = fft::Geo<T, LL, TE, RB>::ST, SW = fft::Geo<T, LL, TE, RB>::SW,     \
+    NT = fft::Geo<T, LL, TE, RB>::NT;                                                                         \
+    if (pass_a) a = mode == 0 ? fft::k_pass_a_ip<T, -1, 0, LL, TE, RB> : fft::k_pass_a_ip<T, 1, 1, LL, TE, RB>; \
+    else b = mode == 0 ? fft::k_pass_b_ip<T, -1, 0, LL, TE, RB> : fft::k_pass_b_ip<T, 1, 1, LL, TE, RB>;        \
     return true;
     switch (L) {
         case 128: { INFT_IPG(128) }
@@ -1177,10 +1188,34 @@ static int ip_te(bool pass_a) {
     return pass_a ? ta : tb;
 }
 
+// radix of the in-place kernels' bulk stages per pass and direction (INFT_FFT_RB_A0 / _A1 /
+// _B0 / _B1 = 16 or 32; pass A / B, mode 0 = inverse, 1 = adjoint)
+static int ip_rb(bool pass_a, int mode) {
+    static int v[4] = {0, 0, 0, 0};
+    static const bool init = [] {
+        const char* names[4] = {"INFT_FFT_RB_A0", "INFT_FFT_RB_A1", "INFT_FFT_RB_B0", "INFT_FFT_RB_B1"};
+        const int dflt[4] = {16, 32, 16, 16};  // adjoint pass A: radix 32 (config 5: 0.826 -> 0.740 ms)
+        for (int i = 0; i < 4; ++i) {
+            const char* e = getenv(names[i]);
+            v[i] = e && atoi(e) == 32 ? 32 : (e && atoi(e) == 16 ? 16 : dflt[i]);
+        }
+        return true;
+    }();
+    (void)init;
+    return v[(pass_a ? 0 : 2) + (mode ? 1 : 0)];
+}
+
 template <typename T>
-static bool pick_ip(int mode, int L, bool pass_a, PassAFn<T>& a, PassBFn<T>& b, int& TF, int& ST, int& SW, int& NT) {
-    if (ip_te(pass_a) == 2048) return pick_ip_te<T, 2048>(mode, L, pass_a, a, b, TF, ST, SW, NT);
-    return pick_ip_te<T, fft::kTileIP>(mode, L, pass_a, a, b, TF, ST, SW, NT);
+static bool pick_ip(int mode, int L, bool pass_a, PassAFn<T>& a, PassBFn<T>& b, int& TF, int& ST, int& SW, int& NT,
+                    int& RB) {
+    RB = ip_rb(pass_a, mode);
+    if (ip_te(pass_a) == 2048) {
+        RB = fft::kRB;
+        return pick_ip_te<T, 2048, fft::kRB>(mode, L, pass_a, a, b, TF, ST, SW, NT);
+    }
+    if (RB == 32 && L >= 1024) return pick_ip_te<T, fft::kTileIP, 32>(mode, L, pass_a, a, b, TF, ST, SW, NT);
+    RB = fft::kRB;
+    return pick_ip_te<T, fft::kTileIP, fft::kRB>(mode, L, pass_a, a, b, TF, ST, SW, NT);
 }
 
 // pass A over `src` (MODE 0: the grid, rows GS; MODE 1: h, rows M)
@@ -1205,9 +1240,10 @@ static void launch_pass_a(Plan& p, fft::Args<T>& A, int mode, const void* src, i
     PassBFn<T> kunused = nullptr;
     // complex128 only: complex64's double-buffered 8192-element tiles are faster (config 5 c64
     // 3.06 ms/step against 3.21 in place with 4096-element tiles)
+    int rb = fft::kRB;
     if (ip && sizeof(T) == 8) {
         int tf, st_, sw, nt;
-        if (pick_ip<T>(mode, L, true, kip, kunused, tf, st_, sw, nt)) {
+        if (pick_ip<T>(mode, L, true, kip, kunused, tf, st_, sw, nt, rb)) {
             TA = tf, ST = st_, SW = sw, threads = nt;
         } else {
             kip = nullptr;
@@ -1237,7 +1273,7 @@ static void launch_pass_a(Plan& p, fft::Args<T>& A, int mode, const void* src, i
     }
     const int ntiles = (int)(R * (A.N2 / TA));
     if (kip) {
-        const size_t smem_ip = cs * (size_t)(std::max(L * TA, SW * TA) + L / fft::kRB) + 16;
+        const size_t smem_ip = cs * (size_t)(std::max(L * TA, SW * TA) + L / rb) + 16;
         ensure_smem_attr((const void*)kip, smem_ip);
         const int occ = occupancy_cached((const void*)kip, threads, smem_ip);
         kip<<<(unsigned)std::min(ntiles, num_sms() * std::max(1, occ)), threads, smem_ip, st>>>(map, dmap, A, BR,
@@ -1278,6 +1314,7 @@ static void launch_pass_b(Plan& p, fft::Args<T>& A, int mode, int64_t R, cudaStr
         return e && atoi(e);
     }();
     PassBFn<T> kip = nullptr;
+    int rb = fft::kRB;
     if (ipb && sizeof(T) == 8 && (mode == 0 || ipb1)) {
         PassAFn<T> unused = nullptr;
         int tf, st_, sw, nt;
@@ -1287,7 +1324,7 @@ static void launch_pass_b(Plan& p, fft::Args<T>& A, int mode, int64_t R, cudaStr
         }();
         if (mode == 0 && tile_b == 8192 && pick_ip_b8<T>(L, kip, tf, st_, sw, nt)) {
             TB = tf, ST = st_, SW = sw, threads = nt;
-        } else if (pick_ip<T>(mode, L, false, unused, kip, tf, st_, sw, nt)) {
+        } else if (pick_ip<T>(mode, L, false, unused, kip, tf, st_, sw, nt, rb)) {
             TB = tf, ST = st_, SW = sw, threads = nt;
         } else {
             kip = nullptr;
@@ -1324,7 +1361,7 @@ static void launch_pass_b(Plan& p, fft::Args<T>& A, int mode, int64_t R, cudaStr
     }
     const int ntiles = (int)(R * (A.N1 / TB));
     if (kip) {
-        const size_t head = (cs * (size_t)(std::max(ST * TB, SW * TB) + L / fft::kRB) + 127) / 128 * 128;
+        const size_t head = (cs * (size_t)(std::max(ST * TB, SW * TB) + L / rb) + 127) / 128 * 128;
         const size_t smem_ip = head + (mode == 0 ? sizeof(T) * (size_t)(2 * B2 * DW) : 0) + 32;
         ensure_smem_attr((const void*)kip, smem_ip);  // <= ~150 KB for L <= 4096
         const int occ = occupancy_cached((const void*)kip, threads, smem_ip);
