@@ -288,6 +288,12 @@ constexpr bool kNoLoad = INFT_EXP_NOLOAD != 0;
 #define INFT_FFT_PREFETCH 1
 #endif
 constexpr bool kPrefetch = INFT_FFT_PREFETCH != 0;
+// in-place pass B of the adjoint (INFT_FFT_IP_B1=1): plain stores of the grid from registers
+// (1) or staged TMA store boxes (0)
+#ifndef INFT_FFT_PLAIN_B1
+#define INFT_FFT_PLAIN_B1 1
+#endif
+constexpr bool kPlainB1 = INFT_FFT_PLAIN_B1 != 0;
 // pass A, L2 prefetch of the next tile at the start of the current one: on for the adjoint
 // (MODE 1: band rows of h; config 5: 0.742 -> 0.720 ms), off for the inverse (MODE 0: the whole
 // strided column tile; 0.826 -> 0.96 ms with it)
@@ -906,6 +912,9 @@ __global__ void __launch_bounds__(Geo<T, L, TE, RB>::NT, TE == kTileIP ? (RB == 
                 const T d = dsm[sr * DW + doff];
                 const int64_t c = (int64_t)(sr < B2 ? sr + B2 : sr - B2) * N1 + row0 + f;
                 frow[c] = mk<T>(d * v.x, d * v.y);
+            } else if (kPlainB1) {
+                grow[k] = v;
+                if (k < A.H) grow[A.N + k] = v;
             } else {
                 // staged in the buffer the last stage has just read, [k2][TB], left by TMA store
                 // boxes below; the halo copy of the first cells goes straight out
@@ -915,10 +924,10 @@ __global__ void __launch_bounds__(Geo<T, L, TE, RB>::NT, TE == kTileIP ? (RB == 
         };
         const int nxt = id + (int)gridDim.x;
         auto on_free = [&]() {
-            if (!kNoLoad && MODE == 0 && threadIdx.x == 0 && nxt < ntiles) issue(nxt);
+            if (!kNoLoad && (MODE == 0 || kPlainB1) && threadIdx.x == 0 && nxt < ntiles) issue(nxt);
         };
         fft_stages_ip<T, SIGN, G, 0, 1>(tws, buf, load, store, on_free);
-        if (MODE == 0) {
+        if (MODE == 0 || kPlainB1) {
             __syncthreads();  // every d read of this tile before the next tile's d copy
         } else {
             fence_proxy_async();  // staged outputs before the TMA store
@@ -932,7 +941,7 @@ __global__ void __launch_bounds__(Geo<T, L, TE, RB>::NT, TE == kTileIP ? (RB == 
             }
         }
     }
-    if (MODE == 1 && threadIdx.x == 0) bulk_wait<0>();
+    if (MODE == 1 && !kPlainB1 && threadIdx.x == 0) bulk_wait<0>();
 }
 
 }  // namespace fft
@@ -1302,16 +1311,20 @@ static void launch_pass_b(Plan& p, fft::Args<T>& A, int mode, int64_t R, cudaStr
         throw Fail{INFT_ERR_UNSUPPORTED};
     }
     // in-place pass B for the inverse (MODE 0: plain stores of the kept half; two CTAs per SM)
-    // unless INFT_FFT_IP_B=0.  Config 5: 0.854 -> 0.766 ms.  MODE 1 writes the whole grid + halo
-    // and keeps the staged TMA stores of k_pass_b (in place with plain stores: 0.885 -> 0.917
-    // ms; with staged stores, INFT_FFT_IP_B1=1: 1.00 ms).
+    // unless INFT_FFT_IP_B=0.  Config 5: 0.854 -> 0.766 ms (0.735 with the L2 prefetch of the
+    // next tile).  MODE 1 writes the whole grid + halo, also in place with plain stores and the
+    // prefetch (0.883 -> 0.84 ms; round 1 without the prefetch: 0.917, with staged TMA stores
+    // -DINFT_FFT_PLAIN_B1=0: 1.0-1.3 ms).
     static const bool ipb = [] {
         const char* e = getenv("INFT_FFT_IP_B");
         return !(e && atoi(e) == 0);
     }();
+    // adjoint (MODE 1) in place too: plain stores of the grid and an L2 prefetch of the next
+    // tile (config 5: 0.883 -> 0.837 ms against the double-buffered k_pass_b); INFT_FFT_IP_B1=0:
+    // the double-buffered kernel
     static const bool ipb1 = [] {
         const char* e = getenv("INFT_FFT_IP_B1");
-        return e && atoi(e);
+        return !(e && atoi(e) == 0);
     }();
     PassBFn<T> kip = nullptr;
     int rb = fft::kRB;
