@@ -755,9 +755,185 @@ __global__ void __launch_bounds__(256) k_gather_2d_tile(const int2* __restrict__
     }
 }
 
+// 2-D gather with register row windows (default; INFT_GATHER2D_SMEM=1: k_gather_2d_tile).
+// Same chunks (<= kG2 nodes of one tile x 32 RHS, lane = RHS) and the same streamed grid rows,
+// but each warp loads the staged row ONCE into registers (W complex per lane) and every node of
+// the warp whose footprint covers the row takes its P1 taps from registers (warp-uniform switch
+// on the node's column offset: static register indices) -- k_gather_2d_tile read each tap from
+// shared memory (4 wavefronts per tap and warp: shared-memory bound).  The node's weight row for
+// the current grid row is staged with the grid row (cp.async, double-buffered), so the CTA keeps
+// ~40 KB of shared memory instead of the chunk's whole weight block.  Deterministic: every
+// node sums its rows in order, one store per (node, RHS).
+template <typename T, int MC, int WPC, bool RWIN>
+__global__ void __launch_bounds__(32 * WPC) k_gather_2d_rw(const int2* __restrict__ chunks,
+                                                           const int32_t* __restrict__ seg_start,
+                                                           const int32_t* __restrict__ n0s,
+                                                           const int32_t* __restrict__ perm, const T* __restrict__ w,
+                                                           int PP, const C2<T>* __restrict__ grid, C2<T>* __restrict__ f,
+                                                           int64_t N, int Ms1, int Ms2, int nseg2, int R, int64_t GS) {
+    constexpr int P1 = 2 * MC + 1;
+    constexpr int W = 16 + P1 - 1;   // rows and columns covered by the tile's footprints
+    constexpr int NPW = kG2 / WPC;   // nodes per warp
+    constexpr int NT = 32 * WPC;
+    constexpr int WRB = kG2 * P1;    // weight-row buffer (elements) per stage
+    extern __shared__ __align__(128) unsigned char sg[];
+    C2<T>* gsm = reinterpret_cast<C2<T>*>(sg);                        // [2][W][32]
+    T* wrs = reinterpret_cast<T*>(gsm + 2 * W * 32);                  // [2][kG2][P1]
+    int* meta = reinterpret_cast<int*>(wrs + 2 * WRB);                // [kG2]: d1 | c2 << 16
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int2 ch = chunks[blockIdx.x];
+    const int tile = ch.x, first = ch.y;
+    const int nn = min(kG2, __ldg(seg_start + tile + 1) - first);
+    const int s1 = tile / nseg2, s2 = tile - (tile / nseg2) * nseg2;
+    const int row0 = s1 * 16, col0 = s2 * 16;
+    const int rbase = blockIdx.y * 32;
+    const int r = rbase + lane;
+    for (int i = threadIdx.x; i < kG2; i += NT) {
+        int v = 1 << 14;  // d1 out of range: never active
+        if (i < nn) v = (__ldg(n0s + 2 * (first + i)) - row0) | ((__ldg(n0s + 2 * (first + i) + 1) - col0) << 16);
+        meta[i] = v;
+    }
+    __syncthreads();
+    auto stage_row = [&](int rho) {
+        int grow = row0 + rho;
+        if (grow >= Ms1) grow -= Ms1;
+        C2<T>* dst = gsm + (rho & 1) * W * 32;
+        for (int e = threadIdx.x; e < W * 32; e += NT) {
+            const int c = e >> 5, l = e & 31;
+            int gc = col0 + c;
+            if (gc >= Ms2) gc -= Ms2;
+            const bool ok = rbase + l < R;
+            cp_async<(int)sizeof(C2<T>)>(dst + e, grid + (int64_t)(ok ? rbase + l : 0) * GS + (int64_t)grow * Ms2 + gc,
+                                         ok ? (int)sizeof(C2<T>) : 0);
+        }
+        // weight rows t1 = rho - d1 of the nodes whose footprint covers grid row rho
+        T* wd = wrs + (rho & 1) * WRB;
+        for (int e = threadIdx.x; e < nn * P1; e += NT) {
+            const int i = e / P1, t2 = e - (e / P1) * P1;
+            const int t1 = rho - (meta[i] & 0xffff);
+            if (t1 >= 0 && t1 < P1) cp_async<(int)sizeof(T)>(wd + e, w + (int64_t)(first + i) * PP + t1 * P1 + t2, (int)sizeof(T));
+        }
+        cp_async_commit();
+    };
+    T ax[NPW], ay[NPW];
+#pragma unroll
+    for (int q = 0; q < NPW; ++q) ax[q] = ay[q] = T(0);
+    stage_row(0);
+#pragma unroll 1
+    for (int rho = 0; rho < W; ++rho) {
+        if (rho + 1 < W) {
+            stage_row(rho + 1);
+            cp_async_wait<1>();
+        } else {
+            cp_async_wait<0>();
+        }
+        __syncthreads();
+        const C2<T>* g = gsm + (rho & 1) * W * 32 + lane;
+        const T* wd = wrs + (rho & 1) * WRB;
+        if constexpr (!RWIN) {
+            // taps straight from the staged row (k_gather_2d_tile's inner loop)
+#pragma unroll
+            for (int q = 0; q < NPW; ++q) {
+                const int mqq = meta[warp + WPC * q];
+                const int t1 = rho - (mqq & 0xffff);
+                if (t1 >= 0 && t1 < P1) {
+                    const T* wr = wd + (warp + WPC * q) * P1;
+                    const C2<T>* gq = g + (mqq >> 16) * 32;
+                    T sx = 0, sy = 0;
+#pragma unroll
+                    for (int t2 = 0; t2 < P1; ++t2) {
+                        const C2<T> gv = gq[t2 * 32];
+                        sx = fma(wr[t2], gv.x, sx);
+                        sy = fma(wr[t2], gv.y, sy);
+                    }
+                    ax[q] += sx;
+                    ay[q] += sy;
+                }
+            }
+            __syncthreads();
+            continue;
+        }
+        T gx[W], gy[W];
+#pragma unroll
+        for (int c = 0; c < W; ++c) {
+            const C2<T> v = g[c * 32];
+            gx[c] = v.x;
+            gy[c] = v.y;
+        }
+#pragma unroll
+        for (int q = 0; q < NPW; ++q) {
+            const int mqq = meta[warp + WPC * q];  // broadcast
+            const int t1 = rho - (mqq & 0xffff);
+            if (t1 >= 0 && t1 < P1) {  // warp-uniform
+                const T* wr = wd + (warp + WPC * q) * P1;
+                T wv[P1];
+#pragma unroll
+                for (int t2 = 0; t2 < P1; ++t2) wv[t2] = wr[t2];
+                T sx0 = 0, sy0 = 0, sx1 = 0, sy1 = 0;
+                switch (mqq >> 16) {
+#define INFT_G2RW_CASE(C)                                                \
+    case C: {                                                            \
+        _Pragma("unroll") for (int t2 = 0; t2 < P1; t2 += 2) {           \
+            sx0 = fma(wv[t2], gx[C + t2], sx0);                          \
+            sy0 = fma(wv[t2], gy[C + t2], sy0);                          \
+            if (t2 + 1 < P1) {                                           \
+                sx1 = fma(wv[t2 + 1], gx[C + t2 + 1], sx1);              \
+                sy1 = fma(wv[t2 + 1], gy[C + t2 + 1], sy1);              \
+            }                                                            \
+        }                                                                \
+    } break;
+                    INFT_CASES_16(INFT_G2RW_CASE)
+#undef INFT_G2RW_CASE
+                    default:
+                        break;
+                }
+                ax[q] += sx0 + sx1;
+                ay[q] += sy0 + sy1;
+            }
+        }
+        __syncthreads();  // row buffer (rho & 1) free for row rho + 2
+    }
+    if (r < R) {
+#pragma unroll
+        for (int q = 0; q < NPW; ++q) {
+            const int j = warp + WPC * q;
+            if (j < nn) f[(int64_t)r * N + __ldg(perm + first + j)] = mk<T>(ax[q], ay[q]);
+        }
+    }
+}
+
 template <typename T>
 using Gather2dFn = void (*)(const int2*, const int32_t*, const int32_t*, const int32_t*, const T*, int, const C2<T>*,
                             C2<T>*, int64_t, int, int, int, int, int64_t);
+
+// register windows (INFT_G2RW=1, 4 warps x 16 nodes) or taps from shared memory (default: 8
+// warps x 8 nodes, the weight-row staging keeps two CTAs per SM where k_gather_2d_tile's
+// whole-chunk weight block allowed one)
+#ifndef INFT_G2RW
+#define INFT_G2RW 0
+#endif
+constexpr bool kG2Rwin = INFT_G2RW != 0;
+constexpr int kG2rwWpc = kG2Rwin ? 4 : 8;  // warps per chunk
+
+template <typename T>
+static Gather2dFn<T> gather2d_rw_fn(int m) {
+    switch (m) {
+        case 1: return k_gather_2d_rw<T, 1, kG2rwWpc, kG2Rwin>;
+        case 2: return k_gather_2d_rw<T, 2, kG2rwWpc, kG2Rwin>;
+        case 3: return k_gather_2d_rw<T, 3, kG2rwWpc, kG2Rwin>;
+        case 4: return k_gather_2d_rw<T, 4, kG2rwWpc, kG2Rwin>;
+        case 5: return k_gather_2d_rw<T, 5, kG2rwWpc, kG2Rwin>;
+        case 6: return k_gather_2d_rw<T, 6, kG2rwWpc, kG2Rwin>;
+        case 7: return k_gather_2d_rw<T, 7, kG2rwWpc, kG2Rwin>;
+    }
+    return nullptr;
+}
+
+template <typename T>
+static size_t gather2d_rw_smem(int P1) {
+    const int W = 16 + P1 - 1;
+    return sizeof(C2<T>) * 2 * W * 32 + sizeof(T) * 2 * (size_t)kG2 * P1 + sizeof(int) * kG2;
+}
 
 template <typename T>
 static Gather2dFn<T> gather2d_fn(int m) {
@@ -804,11 +980,13 @@ static void gather(Plan& p, const C2<T>* grid, C2<T>* f, int64_t R, cudaStream_t
         ensure_gather2d_chunks(p, st);
         if (p.chunks2d_n > 0) {
             const int W = 16 + p.P1 - 1;
-            const size_t smem = sizeof(C2<T>) * 2 * W * 32 + sizeof(T) * (size_t)kG2 * p.PP;
-            Gather2dFn<T> fn = gather2d_fn<T>(p.m);
+            const bool rw = !getenv_flag("INFT_GATHER2D_SMEM");
+            const size_t smem = rw ? gather2d_rw_smem<T>(p.P1)
+                                   : sizeof(C2<T>) * 2 * W * 32 + sizeof(T) * (size_t)kG2 * p.PP;
+            Gather2dFn<T> fn = rw ? gather2d_rw_fn<T>(p.m) : gather2d_fn<T>(p.m);
             ensure_smem_attr((const void*)fn, smem);
             dim3 g((unsigned)p.chunks2d_n, (unsigned)ceil_div(R, 32));
-            fn<<<g, 256, smem, st>>>(p.chunks2d.as<int2>(), p.seg_start.as<int32_t>(), p.n0s.as<int32_t>(),
+            fn<<<g, rw ? 32 * kG2rwWpc : 256, smem, st>>>(p.chunks2d.as<int2>(), p.seg_start.as<int32_t>(), p.n0s.as<int32_t>(),
                                      p.perm.as<int32_t>(), w, p.PP, grid, f, p.N, (int)p.Ms[0], (int)p.Ms[1],
                                      (int)p.nseg[1], (int)R, p.GS);
             INFT_CHECK_LAUNCH();

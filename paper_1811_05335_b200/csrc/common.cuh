@@ -94,6 +94,9 @@ __device__ __forceinline__ int rec_n0(const float* rec, int P) { return __float_
 __device__ __forceinline__ double n0_as(double, int n0) { return __longlong_as_double((long long)n0); }
 __device__ __forceinline__ float n0_as(float, int n0) { return __int_as_float(n0); }
 
+#define INFT_CASES_16(X) \
+    X(0) X(1) X(2) X(3) X(4) X(5) X(6) X(7) X(8) X(9) X(10) X(11) X(12) X(13) X(14) X(15)
+
 #define INFT_CASES_32(X) \
     X(0) X(1) X(2) X(3) X(4) X(5) X(6) X(7) X(8) X(9) X(10) X(11) X(12) X(13) X(14) X(15) \
     X(16) X(17) X(18) X(19) X(20) X(21) X(22) X(23) X(24) X(25) X(26) X(27) X(28) X(29) X(30) X(31)
