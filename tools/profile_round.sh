@@ -4,7 +4,7 @@
 #   3. one `ncu --set full` capture of the six apply kernels of one step.
 # Outputs land in gpurun_out/ (scratch); summarise into profiles/ with tools/ncu_summary.py.
 set -e
-TAG=${1:-r01}
+TAG=${1:-r02}
 python bench.py > gpurun_out/bench_${TAG}.log 2>&1
 tail -1 gpurun_out/bench_${TAG}.log > gpurun_out/bench_${TAG}.json
 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_${TAG}.csv \
