@@ -588,7 +588,7 @@ __global__ void __launch_bounds__(Geo<T, L>::NT, 1)
 #define INFT_R32_MINB 2
 #endif
 template <typename T, int SIGN, int MODE, int L, int TE = kTileIP, int RB = kRB>
-__global__ void __launch_bounds__(Geo<T, L, TE, RB>::NT, TE == kTileIP ? (RB == 32 ? INFT_R32_MINB : 2) : 4)
+__global__ void __launch_bounds__(Geo<T, L, TE, RB>::NT, TE == kTileIP ? (RB == 32 ? INFT_R32_MINB : 2) : (TE < kTileIP ? 4 : 2))
     k_pass_a_ip(const __grid_constant__ CUtensorMap map, const __grid_constant__ CUtensorMap dmap, Args<T> A, int BR,
                 int ntiles) {
     extern __shared__ __align__(128) unsigned char smraw[];
@@ -827,7 +827,7 @@ __global__ void __launch_bounds__(Geo<T, L>::NT, 1)
 // buffer (MODE 0), two CTAs per SM, plain stores from registers (the staged TMA stores of
 // k_pass_b would hold the buffer the next tile lands in).
 template <typename T, int SIGN, int MODE, int L, int TE = kTileIP, int RB = kRB>
-__global__ void __launch_bounds__(Geo<T, L, TE, RB>::NT, TE == kTileIP ? (RB == 32 ? INFT_R32_MINB : 2) : (TE < kTileIP ? 4 : 1))
+__global__ void __launch_bounds__(Geo<T, L, TE, RB>::NT, TE == kTileIP ? (RB == 32 ? INFT_R32_MINB : 2) : (TE < kTileIP ? 4 : (RB == 32 ? 2 : 1)))
     k_pass_b_ip(const __grid_constant__ CUtensorMap dmap, const __grid_constant__ CUtensorMap omap, Args<T> A,
                 int BRd, int BRo, int ntiles) {
     extern __shared__ __align__(128) unsigned char smraw[];
@@ -1214,9 +1214,30 @@ static int ip_rb(bool pass_a, int mode) {
     return v[(pass_a ? 0 : 2) + (mode ? 1 : 0)];
 }
 
+// complex64 in place: 8192-element tiles (64-byte column runs) with radix-32 stages (256 threads
+// at two CTAs per SM).  Pass A by default (config 5 c64: inverse 0.451 -> 0.425 ms, adjoint
+// 0.507 -> 0.428 ms; INFT_FFT_IP_C64A=0: double-buffered); pass B only with INFT_FFT_IP_C64=1
+// (slower: 0.468 -> 0.512 ms, 0.434 -> 0.487 ms -- three stages for L = 2048)
+static bool ip_c64(bool pass_a) {
+    static const bool a = [] {
+        const char* e = getenv("INFT_FFT_IP_C64A");
+        return !(e && atoi(e) == 0);
+    }();
+    static const bool b = [] {
+        const char* e = getenv("INFT_FFT_IP_C64");
+        return e && atoi(e);
+    }();
+    return pass_a ? a : b;
+}
+
 template <typename T>
 static bool pick_ip(int mode, int L, bool pass_a, PassAFn<T>& a, PassBFn<T>& b, int& TF, int& ST, int& SW, int& NT,
                     int& RB) {
+    if (sizeof(T) == 4) {
+        RB = 32;
+        if (L < 1024) return false;
+        return pick_ip_te<T, 8192, 32>(mode, L, pass_a, a, b, TF, ST, SW, NT);
+    }
     RB = ip_rb(pass_a, mode);
     if (ip_te(pass_a) == 2048) {
         RB = fft::kRB;
@@ -1247,10 +1268,10 @@ static void launch_pass_a(Plan& p, fft::Args<T>& A, int mode, const void* src, i
     }();
     PassAFn<T> kip = nullptr;
     PassBFn<T> kunused = nullptr;
-    // complex128 only: complex64's double-buffered 8192-element tiles are faster (config 5 c64
-    // 3.06 ms/step against 3.21 in place with 4096-element tiles)
+    // complex64: in place with 8192-element radix-32 tiles (ip_c64; the 4096-element in-place
+    // tiles were slower than the double-buffered kernel: 3.21 vs 3.06 ms/step)
     int rb = fft::kRB;
-    if (ip && sizeof(T) == 8) {
+    if (ip && (sizeof(T) == 8 || ip_c64(true))) {
         int tf, st_, sw, nt;
         if (pick_ip<T>(mode, L, true, kip, kunused, tf, st_, sw, nt, rb)) {
             TA = tf, ST = st_, SW = sw, threads = nt;
@@ -1328,7 +1349,7 @@ static void launch_pass_b(Plan& p, fft::Args<T>& A, int mode, int64_t R, cudaStr
     }();
     PassBFn<T> kip = nullptr;
     int rb = fft::kRB;
-    if (ipb && sizeof(T) == 8 && (mode == 0 || ipb1)) {
+    if (ipb && (sizeof(T) == 8 || ip_c64(false)) && (mode == 0 || ipb1)) {
         PassAFn<T> unused = nullptr;
         int tf, st_, sw, nt;
         static const int tile_b = [] {
