@@ -81,6 +81,44 @@ __device__ __forceinline__ uint32_t cofs(int v, uint32_t sw) {
     return (uint32_t)bx * 4096u + (sw ^ ((uint32_t)(c >> 1) << 4)) + (uint32_t)(c & 1) * 8u;
 }
 
+// Complex accumulator / window value: two doubles (two DFMA per tap), or a packed float pair for
+// complex64, updated by ONE sm_100 paired FMA per tap (FFMA2: both lanes of the pair times the
+// real weight as a scalar operand) -- the same two correctly rounded fused products as two FFMA.
+template <typename T>
+struct CA;
+template <>
+struct CA<double> {
+    double x, y;
+};
+template <>
+struct CA<float> {
+    unsigned long long v;
+};
+__device__ __forceinline__ CA<double> ca_zero(double) { return CA<double>{0.0, 0.0}; }
+__device__ __forceinline__ CA<float> ca_zero(float) { return CA<float>{0ull}; }
+__device__ __forceinline__ CA<double> ca_from(C2<double> g) { return CA<double>{g.x, g.y}; }
+__device__ __forceinline__ CA<float> ca_from(C2<float> g) {
+    return CA<float>{((unsigned long long)__float_as_uint(g.y) << 32) | __float_as_uint(g.x)};
+}
+__device__ __forceinline__ C2<double> ca_to(CA<double> a) { return mk<double>(a.x, a.y); }
+__device__ __forceinline__ C2<float> ca_to(CA<float> a) {
+    return mk<float>(__uint_as_float((unsigned)(a.v & 0xffffffffull)), __uint_as_float((unsigned)(a.v >> 32)));
+}
+// a += w v
+__device__ __forceinline__ void ca_fma(CA<double>& a, double w, CA<double> v) {
+    a.x = fma(w, v.x, a.x);
+    a.y = fma(w, v.y, a.y);
+}
+__device__ __forceinline__ void ca_fma(CA<float>& a, float w, CA<float> v) {
+    const unsigned long long wp = ((unsigned long long)__float_as_uint(w) << 32) | __float_as_uint(w);
+    asm("fma.rn.f32x2 %0, %1, %2, %0;" : "+l"(a.v) : "l"(v.v), "l"(wp));
+}
+// C2 load straight into the accumulator type (complex64: one 8-byte load)
+template <typename T>
+__device__ __forceinline__ CA<T> ca_load(const unsigned char* p) {
+    return ca_from(*reinterpret_cast<const C2<T>*>(p));
+}
+
 // ------------------------------------------------------------------------- spread
 template <typename T, int MC>
 __global__ void __launch_bounds__(128, INFT_RING_MINB) k_spread_ring(const __grid_constant__ CUtensorMap fmap,
@@ -180,9 +218,9 @@ __global__ void __launch_bounds__(128, INFT_RING_MINB) k_spread_ring(const __gri
     if (threadIdx.x == 0)
         for (int b = 0; b < min(kStages, nb); ++b) issue(b, b);
 
-    T ax[K], ay[K];
+    CA<T> acc[K];
 #pragma unroll
-    for (int u = 0; u < K; ++u) ax[u] = ay[u] = T(0);
+    for (int u = 0; u < K; ++u) acc[u] = ca_zero(T(0));
     int cur_k = 0;  // 0 = prologue segment sp, k >= 1 = main segment s0 + k - 1; phase = cur_k & 1
     const int rstore = row0 + warp * 32;
 
@@ -193,7 +231,7 @@ __global__ void __launch_bounds__(128, INFT_RING_MINB) k_spread_ring(const __gri
         if (row0 + (int)threadIdx.x < R) {
             C2<T>* dst = side + ((int64_t)q * R + row0 + threadIdx.x) * SEG;
 #pragma unroll
-            for (int u = 0; u < SEG; ++u) dst[u] = mk<T>(ax[H0 + u], ay[H0 + u]);
+            for (int u = 0; u < SEG; ++u) dst[u] = ca_to(acc[H0 + u]);
         }
     };
     auto store_half = [&](auto HALF) {
@@ -205,7 +243,7 @@ __global__ void __launch_bounds__(128, INFT_RING_MINB) k_spread_ring(const __gri
             __syncwarp();
 #pragma unroll
             for (int u = 0; u < SEG; ++u)
-                *reinterpret_cast<C2<T>*>(my_stg + cofs<T>(u, sw)) = mk<T>(ax[H0 + u], ay[H0 + u]);
+                *reinterpret_cast<C2<T>*>(my_stg + cofs<T>(u, sw)) = ca_to(acc[H0 + u]);
             fence_proxy_async();
             __syncwarp();
             if (lane == 0) {
@@ -216,20 +254,14 @@ __global__ void __launch_bounds__(128, INFT_RING_MINB) k_spread_ring(const __gri
             }
         }
 #pragma unroll
-        for (int u = 0; u < SEG; ++u) {
-            ax[H0 + u] = T(0);
-            ay[H0 + u] = T(0);
-        }
+        for (int u = 0; u < SEG; ++u) acc[H0 + u] = ca_zero(T(0));
     };
     // (the spread keeps a shifting window: a two-phase register ring costs more
     //  registers here than the SEG moves per segment it saves)
     auto flush = [&]() {
         store_half(std::integral_constant<int, 0>{});
 #pragma unroll
-        for (int u = 0; u < K; ++u) {
-            ax[u] = (u + SEG < K) ? ax[u + SEG] : T(0);
-            ay[u] = (u + SEG < K) ? ay[u + SEG] : T(0);
-        }
+        for (int u = 0; u < K; ++u) acc[u] = (u + SEG < K) ? acc[u + SEG] : ca_zero(T(0));
         ++cur_k;
     };
 
@@ -268,15 +300,12 @@ __global__ void __launch_bounds__(128, INFT_RING_MINB) k_spread_ring(const __gri
             while (cur_k < kq) flush();
 #pragma unroll
             for (int q = 0; q < kNB; ++q) {
-                const C2<T> fv = *reinterpret_cast<const C2<T>*>(fb + cofs<T>(q + fo, sw));
+                const CA<T> fv = ca_load<T>(fb + cofs<T>(q + fo, sw));
                 T wv[P];
                 WeightLoader<T, P>::load_smem(rec + q * PP, wv);
 #pragma unroll
                 for (int t = 0; t < P; ++t) {
-                    if (q + t < K) {
-                        ax[q + t] = fma(wv[t], fv.x, ax[q + t]);
-                        ay[q + t] = fma(wv[t], fv.y, ay[q + t]);
-                    }
+                    if (q + t < K) ca_fma(acc[q + t], wv[t], fv);
                 }
             }
             cnt = 0;  // skip the general loop
@@ -289,7 +318,7 @@ __global__ void __launch_bounds__(128, INFT_RING_MINB) k_spread_ring(const __gri
             const int dl = (int)(n0 % SEG);
             const int kq = pro ? 0 : seg - s0 + 1;
             while (cur_k < kq) flush();
-            const C2<T> fv = *reinterpret_cast<const C2<T>*>(fb + cofs<T>(q + fo, sw));
+            const CA<T> fv = ca_load<T>(fb + cofs<T>(q + fo, sw));
             T wv[P];
             WeightLoader<T, P>::load_smem(rec, wv);
             switch (dl) {
@@ -297,8 +326,7 @@ __global__ void __launch_bounds__(128, INFT_RING_MINB) k_spread_ring(const __gri
     case D: {                                                              \
         if constexpr (D < SEG) {                                           \
             _Pragma("unroll") for (int t = 0; t < P; ++t) {                \
-                ax[D + t] = fma(wv[t], fv.x, ax[D + t]);                   \
-                ay[D + t] = fma(wv[t], fv.y, ay[D + t]);                   \
+                ca_fma(acc[D + t], wv[t], fv);                             \
             }                                                              \
         }                                                                  \
     } break;
@@ -473,7 +501,7 @@ __global__ void __launch_bounds__(128, INFT_RING_MINB) k_gather_ring(const __gri
         for (int b = 0; b < min(kStagesGR, nbat); ++b) issueR(b, b);
     }
 
-    T wx[K], wy[K];
+    CA<T> win[K];
     int nextL = 0;
     const uint32_t wrow = (uint32_t)warp * SBOX * 4096u;
     // box L -> registers of half H = L & 1, H a compile-time constant (static register
@@ -487,11 +515,7 @@ __global__ void __launch_bounds__(128, INFT_RING_MINB) k_gather_ring(const __gri
         mbar_wait(&fullW[stage], parity);
         const unsigned char* wb = wbuf + stage * wstage + wrow;
 #pragma unroll
-        for (int v = 0; v < SEG; ++v) {
-            const C2<T> g = *reinterpret_cast<const C2<T>*>(wb + cofs<T>(v, sw));
-            wx[H * SEG + v] = g.x;
-            wy[H * SEG + v] = g.y;
-        }
+        for (int v = 0; v < SEG; ++v) win[H * SEG + v] = ca_load<T>(wb + cofs<T>(v, sw));
         fence_proxy_async();
         __syncwarp();
         if (lane == 0) mbar_arrive(&emptyW[stage]);
@@ -578,9 +602,9 @@ __global__ void __launch_bounds__(128, INFT_RING_MINB) k_gather_ring(const __gri
                 static_assert(kNB % QG == 0, "node groups");
 #pragma unroll
                 for (int g0 = 0; g0 < kNB; g0 += QG) {
-                    T sx[QG], sy[QG];
+                    CA<T> sacc[QG];
 #pragma unroll
-                    for (int qq = 0; qq < QG; ++qq) sx[qq] = sy[qq] = T(0);
+                    for (int qq = 0; qq < QG; ++qq) sacc[qq] = ca_zero(T(0));
 #pragma unroll
                     for (int t0 = 0; t0 < P; t0 += VEC) {
                         T wv[QG][VEC];
@@ -606,8 +630,7 @@ __global__ void __launch_bounds__(128, INFT_RING_MINB) k_gather_ring(const __gri
 #pragma unroll
                                 for (int qq = 0; qq < QG; ++qq) {
                                     const int rg = (g0 + qq + t0 + u + SEG * PH) % K;
-                                    sx[qq] = fma(wv[qq][u], wx[rg], sx[qq]);
-                                    sy[qq] = fma(wv[qq][u], wy[rg], sy[qq]);
+                                    ca_fma(sacc[qq], wv[qq][u], win[rg]);
                                 }
                             }
                         }
@@ -615,7 +638,7 @@ __global__ void __launch_bounds__(128, INFT_RING_MINB) k_gather_ring(const __gri
 #pragma unroll
                     for (int qq = 0; qq < QG; ++qq) {
                         const int sl = cm + g0 + qq;
-                        *reinterpret_cast<C2<T>*>(my_stg + cofs<T>(sl >= RS ? sl - RS : sl, sw)) = mk<T>(sx[qq], sy[qq]);
+                        *reinterpret_cast<C2<T>*>(my_stg + cofs<T>(sl >= RS ? sl - RS : sl, sw)) = ca_to(sacc[qq]);
                     }
                 }
             };
@@ -652,7 +675,7 @@ __global__ void __launch_bounds__(128, INFT_RING_MINB) k_gather_ring(const __gri
             }
             T wv[P];
             WeightLoader<T, P>::load_smem(rec, wv);
-            T sx = 0, sy = 0;
+            CA<T> sa = ca_zero(T(0));
             switch ((cur_i & 1) * 32 + dl) {
 #define INFT_RG_CASE(CID)                                                  \
     case CID: {                                                            \
@@ -660,8 +683,7 @@ __global__ void __launch_bounds__(128, INFT_RING_MINB) k_gather_ring(const __gri
         if constexpr (D < SEG) {                                           \
             _Pragma("unroll") for (int t = 0; t < P; ++t) {                \
                 const int rg = (D + t + SEG * PH) % K;                     \
-                sx = fma(wv[t], wx[rg], sx);                               \
-                sy = fma(wv[t], wy[rg], sy);                               \
+                ca_fma(sa, wv[t], win[rg]);                                \
             }                                                              \
         }                                                                  \
     } break;
@@ -671,7 +693,7 @@ __global__ void __launch_bounds__(128, INFT_RING_MINB) k_gather_ring(const __gri
                     break;
             }
             const int sl = cm + q;
-            *reinterpret_cast<C2<T>*>(my_stg + cofs<T>(sl >= RS ? sl - RS : sl, sw)) = mk<T>(sx, sy);
+            *reinterpret_cast<C2<T>*>(my_stg + cofs<T>(sl >= RS ? sl - RS : sl, sw)) = ca_to(sa);
         }
         run_next = col + cnt;
         if (plain_lo < lead_end) {  // the run's columns before its first aligned box
