@@ -1184,19 +1184,6 @@ static bool pick_ip_te(int mode, int L, bool pass_a, PassAFn<T>& a, PassBFn<T>& 
 #undef INFT_IPG
 }
 
-// tile size of the in-place kernels (INFT_FFT_TE_A / INFT_FFT_TE_B = 2048 or 4096)
-static int ip_te(bool pass_a) {
-    static const int ta = [] {
-        const char* e = getenv("INFT_FFT_TE_A");
-        return e && atoi(e) == 2048 ? 2048 : 4096;
-    }();
-    static const int tb = [] {
-        const char* e = getenv("INFT_FFT_TE_B");
-        return e && atoi(e) == 2048 ? 2048 : 4096;
-    }();
-    return pass_a ? ta : tb;
-}
-
 // radix of the in-place kernels' bulk stages per pass and direction (INFT_FFT_RB_A0 / _A1 /
 // _B0 / _B1 = 16 or 32; pass A / B, mode 0 = inverse, 1 = adjoint)
 static int ip_rb(bool pass_a, int mode) {
@@ -1233,19 +1220,16 @@ static bool ip_c64(bool pass_a) {
 template <typename T>
 static bool pick_ip(int mode, int L, bool pass_a, PassAFn<T>& a, PassBFn<T>& b, int& TF, int& ST, int& SW, int& NT,
                     int& RB) {
-    if (sizeof(T) == 4) {
+    if constexpr (sizeof(T) == 4) {
         RB = 32;
         if (L < 1024) return false;
         return pick_ip_te<T, 8192, 32>(mode, L, pass_a, a, b, TF, ST, SW, NT);
-    }
-    RB = ip_rb(pass_a, mode);
-    if (ip_te(pass_a) == 2048) {
+    } else {
+        RB = ip_rb(pass_a, mode);
+        if (RB == 32 && L >= 1024) return pick_ip_te<T, fft::kTileIP, 32>(mode, L, pass_a, a, b, TF, ST, SW, NT);
         RB = fft::kRB;
-        return pick_ip_te<T, 2048, fft::kRB>(mode, L, pass_a, a, b, TF, ST, SW, NT);
+        return pick_ip_te<T, fft::kTileIP, fft::kRB>(mode, L, pass_a, a, b, TF, ST, SW, NT);
     }
-    if (RB == 32 && L >= 1024) return pick_ip_te<T, fft::kTileIP, 32>(mode, L, pass_a, a, b, TF, ST, SW, NT);
-    RB = fft::kRB;
-    return pick_ip_te<T, fft::kTileIP, fft::kRB>(mode, L, pass_a, a, b, TF, ST, SW, NT);
 }
 
 // pass A over `src` (MODE 0: the grid, rows GS; MODE 1: h, rows M)
