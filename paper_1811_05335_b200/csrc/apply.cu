@@ -1113,6 +1113,62 @@ __device__ void small_fft(C2<T>* g, const C2<T>* tw, int Ms, int lg) {
     }
 }
 
+// Stockham (self-sorting, out of place) radix-4 FFT of natural-order input, a radix-2 first stage
+// when lg is odd: ceil(lg / 2) barriers instead of lg (config 1: 9 radix-2 stages took ~5000
+// cycles of the single-CTA inverse's ~15600).  in -> out alternate between a and b; returns the
+// buffer holding the result.  tw[k] = e^{-2 pi i k / Ms}, k < Ms/2.
+template <typename T, int SIGN>
+__device__ C2<T>* small_fft4(C2<T>* a, C2<T>* b, const C2<T>* tw, int Ms, int lg) {
+    C2<T>* in = a;
+    C2<T>* out = b;
+    int ns = 1;
+    auto twid = [&](int e) {  // e^{SIGN 2 pi i e / Ms}, 0 <= e < Ms
+        C2<T> w = e < Ms / 2 ? tw[e] : mk<T>(-tw[e - Ms / 2].x, -tw[e - Ms / 2].y);
+        if (SIGN > 0) w.y = -w.y;
+        return w;
+    };
+    if (lg & 1) {  // radix 2, span 1: out[2 j + m] = in[j] +- in[j + Ms/2]
+        for (int j = threadIdx.x; j < Ms / 2; j += blockDim.x) {
+            const C2<T> u = in[j], v = in[j + Ms / 2];
+            out[2 * j] = mk<T>(u.x + v.x, u.y + v.y);
+            out[2 * j + 1] = mk<T>(u.x - v.x, u.y - v.y);
+        }
+        __syncthreads();
+        C2<T>* t = in;
+        in = out;
+        out = t;
+        ns = 2;
+    }
+    for (; ns < Ms; ns *= 4) {
+        for (int j = threadIdx.x; j < Ms / 4; j += blockDim.x) {
+            const int k = j & (ns - 1);
+            C2<T> x0 = in[j], x1 = in[j + Ms / 4], x2 = in[j + Ms / 2], x3 = in[j + 3 * (Ms / 4)];
+            if (ns > 1) {
+                const int e = k * (Ms / (4 * ns));
+                const C2<T> w1 = twid(e), w2 = twid(2 * e), w3 = twid(3 * e);
+                x1 = mk<T>(x1.x * w1.x - x1.y * w1.y, x1.x * w1.y + x1.y * w1.x);
+                x2 = mk<T>(x2.x * w2.x - x2.y * w2.y, x2.x * w2.y + x2.y * w2.x);
+                x3 = mk<T>(x3.x * w3.x - x3.y * w3.y, x3.x * w3.y + x3.y * w3.x);
+            }
+            // DFT4 with (SIGN i)^{nk}
+            const C2<T> u0 = mk<T>(x0.x + x2.x, x0.y + x2.y), u1 = mk<T>(x0.x - x2.x, x0.y - x2.y);
+            const C2<T> u2 = mk<T>(x1.x + x3.x, x1.y + x3.y);
+            const C2<T> d = mk<T>(x1.x - x3.x, x1.y - x3.y);
+            const C2<T> u3 = SIGN > 0 ? mk<T>(-d.y, d.x) : mk<T>(d.y, -d.x);
+            const int base = (j - k) * 4 + k;
+            out[base] = mk<T>(u0.x + u2.x, u0.y + u2.y);
+            out[base + ns] = mk<T>(u1.x + u3.x, u1.y + u3.y);
+            out[base + 2 * ns] = mk<T>(u0.x - u2.x, u0.y - u2.y);
+            out[base + 3 * ns] = mk<T>(u1.x - u3.x, u1.y - u3.y);
+        }
+        __syncthreads();
+        C2<T>* t = in;
+        in = out;
+        out = t;
+    }
+    return in;
+}
+
 template <typename T>
 __device__ void small_twiddles(C2<T>* tw, int Ms) {
     for (int k = threadIdx.x; k < Ms / 2; k += blockDim.x) {
@@ -1128,12 +1184,20 @@ __global__ void __launch_bounds__(kSmallThreads) k_small_inverse(const int32_t* 
                                                        const int32_t* __restrict__ perm, const T* __restrict__ w,
                                                        int PP, int P, const C2<T>* __restrict__ f,
                                                        C2<T>* __restrict__ fhat, const T* __restrict__ dk, int64_t N,
-                                                       int Ms, int lg, int M, int S, int stage_bytes) {
+                                                       int Ms, int lg, int M, int S, int stage_bytes, int pshift) {
     extern __shared__ __align__(16) unsigned char smraw[];
     C2<T>* g = reinterpret_cast<C2<T>*>(smraw);
-    C2<T>* tw = g + Ms;
+    C2<T>* gb = g + Ms;  // the Stockham FFT's second buffer
+    C2<T>* tw = gb + Ms;
     const int r = blockIdx.x;
     const C2<T>* fr = f + (int64_t)r * N;
+#ifdef INFT_SMALL_TIMING
+    long long tcl[6];
+    tcl[0] = clock64();
+#define INFT_ST(i) if (threadIdx.x == 0) tcl[i] = clock64();
+#else
+#define INFT_ST(i)
+#endif
     small_twiddles<T>(tw, Ms);
     const int64_t nseg = (Ms + S - 1) / S;
     // staged (when the plan's tables fit): f in sorted node order, slot bases, segment table and
@@ -1143,16 +1207,48 @@ __global__ void __launch_bounds__(kSmallThreads) k_small_inverse(const int32_t* 
     C2<T>* fs = tw + Ms / 2;
     int32_t* ns = reinterpret_cast<int32_t*>(fs + N);
     int32_t* ss = ns + N;
-    T* ws = reinterpret_cast<T*>(smraw + ((((size_t)(Ms + Ms / 2 + N) * sizeof(C2<T>) + 4 * (N + nseg + 1)) + 15) & ~(size_t)15));
+    T* ws = reinterpret_cast<T*>(smraw + ((((size_t)(2 * Ms + Ms / 2 + N) * sizeof(C2<T>) + 4 * (N + nseg + 1)) + 15) & ~(size_t)15));
     if (staged) {
+        // the weight block (and the slot bases when their size is a 16-byte multiple) by one bulk
+        // copy each, issued first so that they are in flight while the threads gather f through
+        // perm: the per-thread copy loops waited for one global load after another (config 1:
+        // ~4 us of the kernel's ~10)
+        __shared__ uint64_t sbar;
+        const uint32_t wbytes = (uint32_t)(sizeof(T) * (size_t)N * PP * (WC ? 2 : 1));
+        const bool nbulk = (N * 4) % 16 == 0;
+        if (threadIdx.x == 0) {
+            mbar_init(&sbar, 1);
+            fence_barrier_init();
+            mbar_arrive_expect_tx(&sbar, wbytes + (nbulk ? (uint32_t)(4 * N) : 0u));
+            bulk_g2s(ws, w, wbytes, &sbar);
+            if (nbulk) bulk_g2s(ns, n0s, (uint32_t)(4 * N), &sbar);
+        }
+        // f in sorted order: a cyclic shift of the caller's order needs no perm load (one global
+        // latency instead of two)
         for (int i = threadIdx.x; i < N; i += blockDim.x) {
-            fs[i] = fr[perm[i]];
-            ns[i] = n0s[i];
+            int j;
+            if (pshift >= 0) {
+                j = i + pshift;
+                if (j >= N) j -= (int)N;
+            } else {
+                j = perm[i];
+            }
+            fs[i] = fr[j];
+            if (!nbulk) ns[i] = n0s[i];
         }
         for (int i = threadIdx.x; i <= nseg; i += blockDim.x) ss[i] = seg_start[i];
-        const int64_t nw = (int64_t)N * PP * (WC ? 2 : 1);
-        for (int64_t e = threadIdx.x; e < nw; e += blockDim.x) ws[e] = w[e];
-        __syncthreads();
+        __syncthreads();  // also orders the barrier init before every thread's wait
+        mbar_wait(&sbar, 0);
+    }
+    INFT_ST(1)
+    // the deconvolution factors of this thread's outputs, loaded now (their latency overlaps the
+    // spread and the FFT instead of following them)
+    constexpr int kMaxOut = 4;
+    T dv[kMaxOut];
+#pragma unroll
+    for (int q = 0; q < kMaxOut; ++q) {
+        const int c = threadIdx.x + q * (int)blockDim.x;
+        dv[q] = c < M ? dk[c] : T(0);
     }
     const int32_t* n0p = staged ? ns : n0s;
     const int32_t* ssp = staged ? ss : seg_start;
@@ -1201,16 +1297,26 @@ __global__ void __launch_bounds__(kSmallThreads) k_small_inverse(const int32_t* 
                 }
             });
         }
-        g[bitrev_n(n, lg)] = mk<T>(sx, sy);
+        g[n] = mk<T>(sx, sy);
     }
     __syncthreads();
-    small_fft<T, -1>(g, tw, Ms, lg);  // a3: F^*
-    for (int c = threadIdx.x; c < M; c += blockDim.x) {  // a4: truncate + s D^*
+    INFT_ST(2)
+    const C2<T>* gf = small_fft4<T, -1>(g, gb, tw, Ms, lg);  // a3: F^*
+    INFT_ST(3)
+    for (int c = threadIdx.x, q = 0; c < M; c += blockDim.x, ++q) {  // a4: truncate + s D^*
         const int k = c - M / 2;
-        const C2<T> v = g[k < 0 ? k + Ms : k];
-        const T d = dk[c];
+        const C2<T> v = gf[k < 0 ? k + Ms : k];
+        const T d = q < kMaxOut ? dv[q] : dk[c];
         fhat[(int64_t)r * M + c] = mk<T>(d * v.x, d * v.y);
     }
+#ifdef INFT_SMALL_TIMING
+    if (threadIdx.x == 0 && r == 0) {
+        tcl[4] = clock64();
+        printf("small_inverse cycles: stage %lld spread %lld fft %lld out %lld\n", tcl[1] - tcl[0], tcl[2] - tcl[1],
+               tcl[3] - tcl[2], tcl[4] - tcl[3]);
+    }
+#endif
+#undef INFT_ST
 }
 
 template <typename T, bool WC>
@@ -1270,7 +1376,7 @@ static void small_inverse(Plan& p, const void* f, void* fhat, int64_t R, cudaStr
     const int Ms = (int)p.Ms[0];
     const int lg = __builtin_ctz((unsigned)Ms);
     const int64_t nseg = (Ms + p.S[0] - 1) / p.S[0];
-    const size_t base = sizeof(C2<T>) * (size_t)(Ms + Ms / 2);
+    const size_t base = sizeof(C2<T>) * (size_t)(2 * Ms + Ms / 2);  // grid, FFT buffer, twiddles
     // staged tables: f (sorted order), slot bases, segment table, weights
     const size_t staged = ((base + sizeof(C2<T>) * p.N + 4 * (p.N + nseg + 1) + 15) & ~(size_t)15) +
                           sizeof(T) * (size_t)p.N * p.PP * (p.wt == INFT_WEIGHTS_COMPLEX ? 2 : 1);
@@ -1281,7 +1387,7 @@ static void small_inverse(Plan& p, const void* f, void* fhat, int64_t R, cudaStr
     kfn<<<(unsigned)R, kSmallThreads, smem, st>>>(p.seg_start.as<int32_t>(), p.n0s.as<int32_t>(), p.perm.as<int32_t>(),
                                         p.w.as<T>(), p.PP, p.P, static_cast<const C2<T>*>(f),
                                         static_cast<C2<T>*>(fhat), dtable<T>(p), p.N, Ms, lg, (int)p.M[0],
-                                        p.S[0], stage ? (int)staged : 0);
+                                        p.S[0], stage ? (int)staged : 0, p.perm_shift);
     INFT_CHECK_LAUNCH();
     p.launches++;
 }
