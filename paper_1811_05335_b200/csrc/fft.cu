@@ -234,9 +234,33 @@ __device__ __forceinline__ C2<T> twid_g(const C2<T>* __restrict__ tab, int e) {
 // One Stockham stage on registers: given a[m] = data[j + m L/R] (already loaded), multiply
 // by e^{SIGN 2 pi i m (j mod Ns) / (Ns R)} (table entry m (j mod Ns) L/(Ns R) of length L),
 // DFT_R; outputs a[m] belong at index (j / Ns) Ns R + (j mod Ns) + m Ns.
+#ifndef INFT_R32_BLOCKTW
+#define INFT_R32_BLOCKTW 1
+#endif
+#ifndef INFT_R16_BLOCKTW
+#define INFT_R16_BLOCKTW 1
+#endif
 template <typename T, int SIGN, int R, int L, int NS>
 __device__ __forceinline__ void stage_regs(C2<T> (&a)[R], int j, const C2<T>* __restrict__ tw) {
-    if constexpr (NS > 1) {
+    if constexpr (NS > 1 && ((R == 32 && INFT_R32_BLOCKTW) || (R == 16 && INFT_R16_BLOCKTW))) {
+        // radix 32: twiddles in blocks of four, a[4b + i] *= w^i w^{4b} with w^{4b} by a running
+        // product (depth <= 8): six live twiddles instead of 31 (the full table held ~120
+        // registers of the 246 the radix-32 passes used)
+        const int k = j % NS;
+        const C2<T> w1 = twid<T, SIGN>(tw, k * (L / (NS * R)));
+        const C2<T> w2 = cmul<T>(w1, w1);
+        const C2<T> w3 = cmul<T>(w2, w1);
+        const C2<T> w4 = cmul<T>(w2, w2);
+        C2<T> wb = w4;
+#pragma unroll
+        for (int b = 0; b < R / 4; ++b) {
+            if (b > 0) a[4 * b] = cmul<T>(a[4 * b], wb);
+            a[4 * b + 1] = cmul<T>(a[4 * b + 1], b > 0 ? cmul<T>(wb, w1) : w1);
+            a[4 * b + 2] = cmul<T>(a[4 * b + 2], b > 0 ? cmul<T>(wb, w2) : w2);
+            a[4 * b + 3] = cmul<T>(a[4 * b + 3], b > 0 ? cmul<T>(wb, w3) : w3);
+            if (b > 0 && b + 1 < R / 4) wb = cmul<T>(wb, w4);
+        }
+    } else if constexpr (NS > 1) {
         const int k = j % NS;
         // one table load, the other powers by multiplication (depth <= 4, a few ulps)
         C2<T> w[R];
