@@ -124,22 +124,39 @@ __device__ __forceinline__ void dft4(C2<T>& x0, C2<T>& x1, C2<T>& x2, C2<T>& x3)
     x3 = csub<T>(u1, u3);
 }
 
+// DFT4 of the first-level sub-transforms; Z: inputs x1 = x2 = 0 (the zero band of the adjoint's
+// first stage, see run_stage_ip): X = (x0 + x3, x0 - SIGN i x3, x0 - x3, x0 + SIGN i x3)
+template <typename T, int SIGN, bool Z>
+__device__ __forceinline__ void dft4g(C2<T>& x0, C2<T>& x1, C2<T>& x2, C2<T>& x3) {
+    if constexpr (Z) {
+        const C2<T> u3 = rot16<T, SIGN, 4>(mk<T>(-x3.x, -x3.y));
+        const C2<T> a = x0, b = x3;
+        x0 = cadd<T>(a, b);
+        x2 = csub<T>(a, b);
+        x1 = cadd<T>(a, u3);
+        x3 = csub<T>(a, u3);
+    } else {
+        dft4<T, SIGN>(x0, x1, x2, x3);
+    }
+}
+
 // In-register DFT of size R (2, 4, 8, 16): a[k] <- sum_n a[n] e^{SIGN 2 pi i n k / R}.
 // R = P*Q with n = n1 + P n2, k = Q k1 + k2:
 //   X[Q k1 + k2] = sum_{n1} w_P^{n1 k1} w_R^{n1 k2} sum_{n2} x[n1 + P n2] w_Q^{n2 k2}
 // (Q = 4 inner DFT4s, twiddles, P-point outer DFTs); every index is static.
-template <typename T, int SIGN, int R>
+// Z: a[m] = 0 for m in [R/4, 3R/4) (inputs n2 = 1, 2 of every inner DFT4), the zeros never read.
+template <typename T, int SIGN, int R, bool Z = false>
 __device__ __forceinline__ void dft_reg(C2<T> (&a)[R]);
 
 // 32-point DFT as 8 x 4: n = n1 + 8 n2, k = 4 k1 + k2:
 //   X[4 k1 + k2] = sum_{n1} w_8^{n1 k1} w_32^{n1 k2} sum_{n2} x[n1 + 8 n2] w_4^{n2 k2}
-template <typename T, int SIGN>
+template <typename T, int SIGN, bool Z = false>
 __device__ __forceinline__ void dft32(C2<T> (&a)[32]) {
     C2<T> y[8][4];
 #pragma unroll
     for (int n1 = 0; n1 < 8; ++n1) {
         C2<T> x0 = a[n1], x1 = a[n1 + 8], x2 = a[n1 + 16], x3 = a[n1 + 24];
-        dft4<T, SIGN>(x0, x1, x2, x3);
+        dft4g<T, SIGN, Z>(x0, x1, x2, x3);
         y[n1][0] = x0;
         y[n1][1] = x1;
         y[n1][2] = x2;
@@ -161,16 +178,16 @@ __device__ __forceinline__ void dft32(C2<T> (&a)[32]) {
     }
 }
 
-template <typename T, int SIGN, int R>
+template <typename T, int SIGN, int R, bool Z>
 __device__ __forceinline__ void dft_reg(C2<T> (&a)[R]) {
     if constexpr (R == 32) {
-        dft32<T, SIGN>(a);
+        dft32<T, SIGN, Z>(a);
     } else if constexpr (R == 2) {
         const C2<T> t = a[0];
         a[0] = cadd<T>(t, a[1]);
         a[1] = csub<T>(t, a[1]);
     } else if constexpr (R == 4) {
-        dft4<T, SIGN>(a[0], a[1], a[2], a[3]);
+        dft4g<T, SIGN, Z>(a[0], a[1], a[2], a[3]);
     } else {
         constexpr int P = R / 4;  // 2 or 4
         C2<T> y[P][4];
@@ -178,7 +195,7 @@ __device__ __forceinline__ void dft_reg(C2<T> (&a)[R]) {
         for (int n1 = 0; n1 < P; ++n1) {
 #pragma unroll
             for (int n2 = 0; n2 < 4; ++n2) y[n1][n2] = a[n1 + P * n2];
-            dft4<T, SIGN>(y[n1][0], y[n1][1], y[n1][2], y[n1][3]);
+            dft4g<T, SIGN, Z>(y[n1][0], y[n1][1], y[n1][2], y[n1][3]);
 #pragma unroll
             for (int k2 = 1; k2 < 4; ++k2) y[n1][k2] = rot16rt<T, SIGN>(y[n1][k2], n1 * k2 * (16 / R));
         }
@@ -240,7 +257,7 @@ __device__ __forceinline__ C2<T> twid_g(const C2<T>* __restrict__ tab, int e) {
 #ifndef INFT_R16_BLOCKTW
 #define INFT_R16_BLOCKTW 1
 #endif
-template <typename T, int SIGN, int R, int L, int NS>
+template <typename T, int SIGN, int R, int L, int NS, bool Z = false>
 __device__ __forceinline__ void stage_regs(C2<T> (&a)[R], int j, const C2<T>* __restrict__ tw) {
     if constexpr (NS > 1 && ((R == 32 && INFT_R32_BLOCKTW) || (R == 16 && INFT_R16_BLOCKTW))) {
         // radix 32: twiddles in blocks of four, a[4b + i] *= w^i w^{4b} with w^{4b} by a running
@@ -277,7 +294,7 @@ __device__ __forceinline__ void stage_regs(C2<T> (&a)[R], int j, const C2<T>* __
 #pragma unroll
         for (int m = 1; m < R; ++m) a[m] = cmul<T>(a[m], w[m]);
     }
-    dft_reg<T, SIGN, R>(a);
+    dft_reg<T, SIGN, R, Z>(a);
 }
 
 // ------------------------------------------------------------------ CTA transform geometry
@@ -436,8 +453,13 @@ __device__ __forceinline__ void cta_fft(const C2<T>* tw, C2<T>* sm, Load&& load,
 // CTA needs one ~80 KB buffer and two CTAs share an SM; stage 0 reads the landed tile, waits
 // for every thread, then writes the skewed work layout into the same buffer; after the last
 // stage has read the buffer, on_free() (thread 0) issues the next tile's copy into it.
-template <typename T, int SIGN, typename G, int R, int NS, int SI, typename Load, typename Store, typename Free>
+// HZ (first stage of the adjoint's pass A when the band is L/4 rows on each side, sigma = 2):
+// rows [L/4, 3L/4) are zero and, with a first-stage radix RF >= 4, they are exactly the legs
+// m in [RF/4, 3RF/4) of every butterfly -- never loaded, and the inner DFT4s skip them.
+template <typename T, int SIGN, typename G, int R, int NS, int SI, bool HZ, typename Load, typename Store,
+          typename Free>
 __device__ __forceinline__ void run_stage_ip(const C2<T>* tw, C2<T>* sm, Load&& load, Store&& store, Free&& on_free) {
+    constexpr bool Z = HZ && SI == 0 && R >= 4;
     constexpr int L = G::ST - G::PAD;
     constexpr int TF = G::TF;
     constexpr int nbut = L / R;
@@ -453,6 +475,9 @@ __device__ __forceinline__ void run_stage_ip(const C2<T>* tw, C2<T>* sm, Load&& 
 #pragma unroll
         for (int m = 0; m < R; ++m) {
             const int n = j + m * nbut;
+            if constexpr (Z) {
+                if (m >= R / 4 && m < 3 * R / 4) continue;
+            }
             if constexpr (SI == 0)
                 a[p][m] = load(f, n, p, m);
             else
@@ -467,7 +492,7 @@ __device__ __forceinline__ void run_stage_ip(const C2<T>* tw, C2<T>* sm, Load&& 
         const int t = threadIdx.x + p * G::NT;
         if (total % G::NT != 0 && t >= total) break;
         const int f = t % TF, j = t / TF;
-        stage_regs<T, SIGN, R, L, NS>(a[p], j, tw);
+        stage_regs<T, SIGN, R, L, NS, Z>(a[p], j, tw);
         const int base = (j / NS) * NS * R + (j % NS);
 #pragma unroll
         for (int m = 0; m < R; ++m) {
@@ -481,12 +506,12 @@ __device__ __forceinline__ void run_stage_ip(const C2<T>* tw, C2<T>* sm, Load&& 
     if constexpr (!last) __syncthreads();
 }
 
-template <typename T, int SIGN, typename G, int SI, int NS, typename Load, typename Store, typename Free>
+template <typename T, int SIGN, typename G, int SI, int NS, bool HZ, typename Load, typename Store, typename Free>
 __device__ __forceinline__ void fft_stages_ip(const C2<T>* tw, C2<T>* sm, Load&& load, Store&& store, Free&& on_free) {
     if constexpr (SI < G::NST) {
         constexpr int R = (SI == 0) ? G::RF : G::RB;
-        run_stage_ip<T, SIGN, G, R, NS, SI>(tw, sm, load, store, on_free);
-        fft_stages_ip<T, SIGN, G, SI + 1, NS * R>(tw, sm, load, store, on_free);
+        run_stage_ip<T, SIGN, G, R, NS, SI, HZ>(tw, sm, load, store, on_free);
+        fft_stages_ip<T, SIGN, G, SI + 1, NS * R, HZ>(tw, sm, load, store, on_free);
     }
 }
 
@@ -611,7 +636,9 @@ __global__ void __launch_bounds__(Geo<T, L>::NT, 1)
 #ifndef INFT_R32_MINB
 #define INFT_R32_MINB 2
 #endif
-template <typename T, int SIGN, int MODE, int L, int TE = kTileIP, int RB = kRB>
+// HZ (MODE 1 only): the band is exactly L/4 rows on each side (sigma = 2), so the first stage
+// skips the zero rows at compile time (run_stage_ip); the host picks it when M / 2 / N2 == L / 4.
+template <typename T, int SIGN, int MODE, int L, int TE = kTileIP, int RB = kRB, bool HZ = false>
 __global__ void __launch_bounds__(Geo<T, L, TE, RB>::NT, TE == kTileIP ? (RB == 32 ? INFT_R32_MINB : 2) : (TE < kTileIP ? 4 : 2))
     k_pass_a_ip(const __grid_constant__ CUtensorMap map, const __grid_constant__ CUtensorMap dmap, Args<T> A, int BR,
                 int ntiles) {
@@ -703,7 +730,7 @@ __global__ void __launch_bounds__(Geo<T, L, TE, RB>::NT, TE == kTileIP ? (RB == 
         auto on_free = [&]() {
             if (!kNoLoad && threadIdx.x == 0 && nxt < ntiles) issue(nxt);
         };
-        fft_stages_ip<T, SIGN, G, 0, 1>(tws, buf, load, store, on_free);
+        fft_stages_ip<T, SIGN, G, 0, 1, MODE == 1 && HZ>(tws, buf, load, store, on_free);
     }
 }
 
@@ -950,7 +977,7 @@ __global__ void __launch_bounds__(Geo<T, L, TE, RB>::NT, TE == kTileIP ? (RB == 
         auto on_free = [&]() {
             if (!kNoLoad && (MODE == 0 || kPlainB1) && threadIdx.x == 0 && nxt < ntiles) issue(nxt);
         };
-        fft_stages_ip<T, SIGN, G, 0, 1>(tws, buf, load, store, on_free);
+        fft_stages_ip<T, SIGN, G, 0, 1, false>(tws, buf, load, store, on_free);
         if (MODE == 0 || kPlainB1) {
             __syncthreads();  // every d read of this tile before the next tile's d copy
         } else {
@@ -1189,11 +1216,13 @@ static bool pick_ip_b8(int L, PassBFn<T>& b, int& TF, int& ST, int& SW, int& NT)
 // (two CTAs per SM) or 2048 (half-size tiles, four CTAs per SM)
 template <typename T, int TE, int RB>
 static bool pick_ip_te(int mode, int L, bool pass_a, PassAFn<T>& a, PassBFn<T>& b, int& TF, int& ST, int& SW,
-                       int& NT) {
+                       int& NT, bool hz) {
 #define INFT_IPG(LL)                                                                                          \
     TF = fft::Geo<T, LL, TE, RB>::TF, ST = fft::Geo<T, LL, TE, RB>::ST, SW = fft::Geo<T, LL, TE, RB>::SW,     \
     NT = fft::Geo<T, LL, TE, RB>::NT;                                                                         \
-    if (pass_a) a = mode == 0 ? fft::k_pass_a_ip<T, -1, 0, LL, TE, RB> : fft::k_pass_a_ip<T, 1, 1, LL, TE, RB>; \
+    if (pass_a) a = mode == 0 ? fft::k_pass_a_ip<T, -1, 0, LL, TE, RB>                                      \
+                              : (hz ? fft::k_pass_a_ip<T, 1, 1, LL, TE, RB, true>                            \
+                                    : fft::k_pass_a_ip<T, 1, 1, LL, TE, RB>);                                \
     else b = mode == 0 ? fft::k_pass_b_ip<T, -1, 0, LL, TE, RB> : fft::k_pass_b_ip<T, 1, 1, LL, TE, RB>;        \
     return true;
     switch (L) {
@@ -1243,16 +1272,16 @@ static bool ip_c64(bool pass_a) {
 
 template <typename T>
 static bool pick_ip(int mode, int L, bool pass_a, PassAFn<T>& a, PassBFn<T>& b, int& TF, int& ST, int& SW, int& NT,
-                    int& RB) {
+                    int& RB, bool hz = false) {
     if constexpr (sizeof(T) == 4) {
         RB = 32;
         if (L < 1024) return false;
-        return pick_ip_te<T, 8192, 32>(mode, L, pass_a, a, b, TF, ST, SW, NT);
+        return pick_ip_te<T, 8192, 32>(mode, L, pass_a, a, b, TF, ST, SW, NT, hz);
     } else {
         RB = ip_rb(pass_a, mode);
-        if (RB == 32 && L >= 1024) return pick_ip_te<T, fft::kTileIP, 32>(mode, L, pass_a, a, b, TF, ST, SW, NT);
+        if (RB == 32 && L >= 1024) return pick_ip_te<T, fft::kTileIP, 32>(mode, L, pass_a, a, b, TF, ST, SW, NT, hz);
         RB = fft::kRB;
-        return pick_ip_te<T, fft::kTileIP, fft::kRB>(mode, L, pass_a, a, b, TF, ST, SW, NT);
+        return pick_ip_te<T, fft::kTileIP, fft::kRB>(mode, L, pass_a, a, b, TF, ST, SW, NT, hz);
     }
 }
 
@@ -1281,7 +1310,14 @@ static void launch_pass_a(Plan& p, fft::Args<T>& A, int mode, const void* src, i
     int rb = fft::kRB;
     if (ip && (sizeof(T) == 8 || ip_c64(true))) {
         int tf, st_, sw, nt;
-        if (pick_ip<T>(mode, L, true, kip, kunused, tf, st_, sw, nt, rb)) {
+        // adjoint with a band of L/4 rows on each side (sigma = 2): first stage skips the zero rows
+        // (INFT_FFT_HZ=0: off)
+        static const bool hz_on = [] {
+            const char* e = getenv("INFT_FFT_HZ");
+            return !(e && atoi(e) == 0);
+        }();
+        const bool hz = hz_on && mode == 1 && A.M / 2 / A.N2 == L / 4;
+        if (pick_ip<T>(mode, L, true, kip, kunused, tf, st_, sw, nt, rb, hz)) {
             TA = tf, ST = st_, SW = sw, threads = nt;
         } else {
             kip = nullptr;

@@ -46,7 +46,13 @@ constexpr int kStages = INFT_RING_STAGES;  // spread load pipeline depth (2: mor
 #ifndef INFT_RING_STAGES_G
 #define INFT_RING_STAGES_G 2
 #endif
-constexpr int kStagesG = INFT_RING_STAGES_G;  // gather window pipeline depth (config 5, aligned output ring: 2 -> 0.894 ms at 6 CTAs/SM, 3 -> 0.938 at 5)
+// gather window pipeline depth: complex128 2 (config 5, aligned output ring: 2 -> 0.894 ms at 6
+// CTAs/SM, 3 -> 0.938 at 5); complex64 3 (its 4-KB window boxes: 0.567 -> 0.534 ms, 8 CTAs/SM)
+#ifndef INFT_RING_STAGES_GF
+#define INFT_RING_STAGES_GF 3
+#endif
+template <typename T>
+constexpr int stages_g() { return sizeof(T) == 8 ? INFT_RING_STAGES_G : INFT_RING_STAGES_GF; }
 #ifndef INFT_RING_STAGES_GR
 #define INFT_RING_STAGES_GR 2
 #endif
@@ -422,6 +428,7 @@ __global__ void __launch_bounds__(128, INFT_RING_MINB) k_gather_ring(const __gri
     // run's first aligned box and after its last one are stored from the ring by plain stores.
     constexpr int NR = OBOX + 1;
     constexpr int RS = NR * EB;
+    constexpr int kStagesG = stages_g<T>();
     static_assert(SEG % EB == 0 && kNB % EB == 0, "tile shapes");
     const int N = (int)Nl;
     const int WPB = blockDim.x >> 5;
@@ -816,10 +823,11 @@ static size_t ring_spread_smem(int wpb, int PP, int SEG) {
 template <typename T>
 static size_t ring_gather_smem(int wpb, int PP, int SEG) {
     const int EB = 128 / (int)sizeof(C2<T>);
-    size_t wsz = (size_t)ring::kStagesG * (SEG / EB) * wpb * 4096;
+    constexpr int kStagesG = ring::stages_g<T>();
+    size_t wsz = (size_t)kStagesG * (SEG / EB) * wpb * 4096;
     size_t st = (size_t)wpb * (ring::kNB / EB + 1) * 4096;  // output ring (NR boxes per warp)
     size_t r = (size_t)ring::kStagesGR * ((ring::kNB * PP * (int)sizeof(T) + 127) & ~127);
-    return wsz + st + r + 2 * (ring::kStagesG + ring::kStagesGR) * sizeof(uint64_t);
+    return wsz + st + r + 2 * (kStagesG + ring::kStagesGR) * sizeof(uint64_t);
 }
 
 static void tmap_or_throw(CUtensorMap* m, const void* base, uint64_t inner, uint64_t rows, uint64_t stride,
