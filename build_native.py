@@ -66,7 +66,7 @@ def build(force=False, verbose=False):
     if failed:
         raise RuntimeError("libinft build failed")
     tmp = LIB + ".tmp"
-    link = [NVCC, *ARCH, "-shared", "-o", tmp, *objs, "-L" + os.path.join(CUDA_HOME, "lib64"), "-lcufft",
+    link = [NVCC, *ARCH, "-shared", "-o", tmp, *objs, "-L" + os.path.join(CUDA_HOME, "lib64"), "-lcufft", "-ldl",
             "-Xlinker", "-rpath," + os.path.join(CUDA_HOME, "lib64")]
     subprocess.check_call(link)
     os.replace(tmp, LIB)

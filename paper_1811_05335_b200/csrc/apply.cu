@@ -17,6 +17,8 @@
 #include <cstring>
 #include <vector>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include "common.cuh"
 #include "inft_internal.cuh"
 #include "tma.cuh"
@@ -1057,19 +1059,25 @@ const float* dtable<float>(const Plan& p) {
     return p.dkf.as<float>();
 }
 
-// RAII stage timer: CUDA events on the launching stream around one stage.
+// RAII stage timer: an NVTX range (header-only NVTX 3: a no-op unless a tool is attached)
+// named after the SURVEY 8(a) row, and -- while profiling -- CUDA events on the launching
+// stream around one stage.
+static const char* const kStageNames[6] = {"inft:a2 spread",      "inft:a3 fft_forward", "inft:a4 trunc_deconv",
+                                           "inft:a5 deconv_pad",  "inft:a6 fft_inverse", "inft:a7 gather"};
 struct StageTimer {
     Plan& p;
     int stage;
     cudaStream_t st;
     cudaEvent_t a = nullptr;
     StageTimer(Plan& pp, int sg, cudaStream_t s) : p(pp), stage(sg), st(s) {
+        nvtxRangePushA(kStageNames[sg]);
         if (p.profiling) {
             a = p.take_event();
             INFT_CUDA(cudaEventRecord(a, st));
         }
     }
     ~StageTimer() {
+        nvtxRangePop();
         if (a) {
             cudaEvent_t b = p.take_event();
             cudaEventRecord(b, st);

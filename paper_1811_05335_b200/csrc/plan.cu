@@ -12,6 +12,8 @@
 #include <cstring>
 #include <limits>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include "common.cuh"
 #include <mutex>
 #include <map>
@@ -579,6 +581,13 @@ using inft::Plan;
     }                                                     \
     return INFT_OK;
 
+// NVTX range over one C-ABI call (a0 plan, a1 setup, the two apply directions); the per-stage
+// ranges a2-a7 nest inside (apply.cu StageTimer).  Header-only NVTX 3: no cost without a tool.
+struct ApiRange {
+    explicit ApiRange(const char* name) { nvtxRangePushA(name); }
+    ~ApiRange() { nvtxRangePop(); }
+};
+
 extern "C" {
 
 const char* inft_status_string(inft_status s) {
@@ -610,6 +619,7 @@ inft_status inft_plan(inft_plan_t* out, int d, const int64_t* M, int64_t N, cons
         return INFT_ERR_INVALID_ARG;
     }
     Plan* p = nullptr;
+    ApiRange nvtx_("inft_plan (a0)");
     INFT_API_BEGIN
     int ndev = 0;
     INFT_CUDA(cudaGetDeviceCount(&ndev));
@@ -668,6 +678,7 @@ inft_status inft_precompute(inft_plan_t plan, inft_method method, inft_weights w
     Plan* p = reinterpret_cast<Plan*>(plan);
     if (method < INFT_AUTO || method > INFT_PLAIN_NFFT || (wt != INFT_WEIGHTS_REAL && wt != INFT_WEIGHTS_COMPLEX))
         return INFT_ERR_INVALID_ARG;
+    ApiRange nvtx_("inft_precompute (a1)");
     INFT_API_BEGIN
     inft::DeviceGuard g(p->device);
     inft::precompute(*p, method, wt, tau > 0 ? tau : 1e-6, (cudaStream_t)stream);
@@ -680,6 +691,7 @@ inft_status inft_apply(inft_plan_t plan, const void* f, void* fhat, int64_t R, i
     if (p->method < 0) return INFT_ERR_NOT_PRECOMPUTED;
     if (R == 0) return INFT_OK;
     if ((!f && p->N > 0) || !fhat) return INFT_ERR_INVALID_ARG;
+    ApiRange nvtx_("inft_apply (a2-a4)");
     INFT_API_BEGIN
     inft::DeviceGuard g(p->device);
     inft::apply_inverse(*p, f, fhat, R, (cudaStream_t)stream);
@@ -692,6 +704,7 @@ inft_status inft_adjoint_apply(inft_plan_t plan, const void* h, void* f, int64_t
     if (p->method < 0) return INFT_ERR_NOT_PRECOMPUTED;
     if (R == 0) return INFT_OK;
     if (!h || (!f && p->N > 0)) return INFT_ERR_INVALID_ARG;
+    ApiRange nvtx_("inft_adjoint_apply (a5-a7)");
     INFT_API_BEGIN
     inft::DeviceGuard g(p->device);
     inft::apply_adjoint(*p, h, f, R, (cudaStream_t)stream);

@@ -53,6 +53,25 @@ constexpr int kStages = INFT_RING_STAGES;  // spread load pipeline depth (2: mor
 #endif
 template <typename T>
 constexpr int stages_g() { return sizeof(T) == 8 ? INFT_RING_STAGES_G : INFT_RING_STAGES_GF; }
+// gather window ring in 4-KB boxes (one mbarrier pair per box).  complex128 with m = 8 (two
+// boxes per segment): 3 boxes = 1.5 segments ahead instead of 2 whole-segment stages (4 boxes):
+// 33.3 -> 29.2 KB per CTA, and with the node-record ring in half batches 8 CTAs per SM instead of 6
+#ifndef INFT_RING_WBOXES_G
+#define INFT_RING_WBOXES_G 3
+#endif
+// dense gather body: explicit double buffer of the weight vectors (experiment)
+#ifndef INFT_GATHER_WPRE
+#define INFT_GATHER_WPRE 0
+#endif
+constexpr bool kGatherWPre = INFT_GATHER_WPRE != 0;
+#ifndef INFT_GATHER_LATE_WAIT
+#define INFT_GATHER_LATE_WAIT 1
+#endif
+constexpr bool kLateWait = INFT_GATHER_LATE_WAIT != 0;
+template <typename T, int SBOX>
+constexpr int win_boxes() {
+    return (sizeof(T) == 8 && SBOX == 2) ? INFT_RING_WBOXES_G : stages_g<T>() * SBOX;
+}
 #ifndef INFT_RING_STAGES_GR
 #define INFT_RING_STAGES_GR 2
 #endif
@@ -60,6 +79,12 @@ constexpr int stages_g() { return sizeof(T) == 8 ? INFT_RING_STAGES_G : INFT_RIN
 // instead of 5 with 3 record stages)
 constexpr int kStagesGR = INFT_RING_STAGES_GR;
 
+// experiment (timing only, wrong results): INFT_EXP_NOCOMPUTE=1 -- the dense gather body copies
+// window values to the outputs (no weight loads, no FMAs): the kernel's data-movement skeleton
+#ifndef INFT_EXP_NOCOMPUTE
+#define INFT_EXP_NOCOMPUTE 0
+#endif
+constexpr bool kExpNoCompute = INFT_EXP_NOCOMPUTE != 0;
 #define INFT_CASES_64(X)                                                                                      \
     X(0) X(1) X(2) X(3) X(4) X(5) X(6) X(7) X(8) X(9) X(10) X(11) X(12) X(13) X(14) X(15) X(16) X(17) X(18)   \
     X(19) X(20) X(21) X(22) X(23) X(24) X(25) X(26) X(27) X(28) X(29) X(30) X(31) X(32) X(33) X(34) X(35)     \
@@ -307,6 +332,10 @@ __global__ void __launch_bounds__(128, INFT_RING_MINB) k_spread_ring(const __gri
 #pragma unroll
             for (int q = 0; q < kNB; ++q) {
                 const CA<T> fv = ca_load<T>(fb + cofs<T>(q + fo, sw));
+                if constexpr (kExpNoCompute) {  // timing experiment: the data-movement skeleton
+                    acc[q] = fv;
+                    continue;
+                }
                 T wv[P];
                 WeightLoader<T, P>::load_smem(rec + q * PP, wv);
 #pragma unroll
@@ -428,7 +457,7 @@ __global__ void __launch_bounds__(128, INFT_RING_MINB) k_gather_ring(const __gri
     // run's first aligned box and after its last one are stored from the ring by plain stores.
     constexpr int NR = OBOX + 1;
     constexpr int RS = NR * EB;
-    constexpr int kStagesG = stages_g<T>();
+    constexpr int NWB = win_boxes<T, SBOX>();  // window ring, in boxes
     static_assert(SEG % EB == 0 && kNB % EB == 0, "tile shapes");
     const int N = (int)Nl;
     const int WPB = blockDim.x >> 5;
@@ -439,14 +468,14 @@ __global__ void __launch_bounds__(128, INFT_RING_MINB) k_gather_ring(const __gri
     const bool active = r < R;
 
     extern __shared__ __align__(1024) unsigned char smem[];
-    const uint32_t wstage = (uint32_t)SBOX * WPB * 4096u;
+    const uint32_t wbox = (uint32_t)WPB * 4096u;  // one ring slot: a box per warp
     const uint32_t rstage = (uint32_t)((kNB * PP * (int)sizeof(T) + 127) & ~127);
     unsigned char* wbuf = smem;
-    unsigned char* stg = smem + kStagesG * wstage;  // [WPB][NR][32][128]
+    unsigned char* stg = smem + NWB * wbox;  // [WPB][NR][32][128]
     unsigned char* rbuf = stg + (size_t)WPB * NR * 4096u;
     uint64_t* fullW = reinterpret_cast<uint64_t*>(rbuf + kStagesGR * rstage);
-    uint64_t* emptyW = fullW + kStagesG;
-    uint64_t* fullR = emptyW + kStagesG;
+    uint64_t* emptyW = fullW + NWB;
+    uint64_t* fullR = emptyW + NWB;
     uint64_t* emptyR = fullR + kStagesGR;
     unsigned char* my_stg = stg + (size_t)warp * NR * 4096u;
 
@@ -456,7 +485,8 @@ __global__ void __launch_bounds__(128, INFT_RING_MINB) k_gather_ring(const __gri
     const int cid = (int)blockIdx.y;  // grid (row groups, chunks), as the spread
     const int s0 = chunks ? __ldg(chunks + 4 * cid) : cid * Q;
     const int s1 = chunks ? __ldg(chunks + 4 * cid + 1) : min(s0 + Q, nseg);
-    const int nbox = s1 - s0 + 1;  // box L = grid points of segment s0 + L (halo covers L = nseg)
+    const int nbox = s1 - s0 + 1;  // window L = grid points of segment s0 + L (halo covers L = nseg)
+    const int nwb = nbox * SBOX;   // ... = boxes L SBOX .. L SBOX + SBOX - 1
     const int b0 = chunks ? __ldg(chunks + 4 * cid + 2) : __ldg(seg_start + s0);
     const int b1 = chunks ? __ldg(chunks + 4 * cid + 3) : __ldg(seg_start + s1);
     const int wrap = N - cshift;
@@ -472,14 +502,11 @@ __global__ void __launch_bounds__(128, INFT_RING_MINB) k_gather_ring(const __gri
             cnt = min(kNB, b1 - pos);
         }
     };
-    auto issueW = [&](int L, int stage) {
-        mbar_arrive_expect_tx(&fullW[stage], wstage);
-        const int col = (s0 + L) * SEG;
+    auto issueW = [&](int bi, int stage) {
+        mbar_arrive_expect_tx(&fullW[stage], wbox);
+        const int col = s0 * SEG + bi * EB;
         for (int wi = 0; wi < WPB; ++wi)
-#pragma unroll
-            for (int bx = 0; bx < SBOX; ++bx)
-                tma_load_2d(wbuf + stage * wstage + (wi * SBOX + bx) * 4096u, &gmap, tcoord<CE>(col + bx * EB),
-                            row0 + wi * 32, &fullW[stage]);
+            tma_load_2d(wbuf + stage * wbox + wi * 4096u, &gmap, tcoord<CE>(col), row0 + wi * 32, &fullW[stage]);
     };
     auto issueR = [&](int b, int stage) {
         int pos, cnt;
@@ -492,7 +519,7 @@ __global__ void __launch_bounds__(128, INFT_RING_MINB) k_gather_ring(const __gri
     if (threadIdx.x == 0) {
         prefetch_tmap(&gmap);
         prefetch_tmap(&omap);
-        for (int i = 0; i < kStagesG; ++i) {
+        for (int i = 0; i < NWB; ++i) {
             mbar_init(&fullW[i], 1);
             mbar_init(&emptyW[i], WPB);
         }
@@ -504,31 +531,35 @@ __global__ void __launch_bounds__(128, INFT_RING_MINB) k_gather_ring(const __gri
     }
     __syncthreads();
     if (threadIdx.x == 0) {
-        for (int L = 0; L < min(kStagesG, nbox); ++L) issueW(L, L);
+        for (int bi = 0; bi < min(NWB, nwb); ++bi) issueW(bi, bi);
         for (int b = 0; b < min(kStagesGR, nbat); ++b) issueR(b, b);
     }
 
     CA<T> win[K];
     int nextL = 0;
-    const uint32_t wrow = (uint32_t)warp * SBOX * 4096u;
+    const uint32_t wrow = (uint32_t)warp * 4096u;
     // box L -> registers of half H = L & 1, H a compile-time constant (static register
     // indices: a run-time half made ptxas select every window register with FSEL, 2K extra
     // instructions per box)
     auto consume_box_h = [&](auto HC) {
         constexpr int H = decltype(HC)::value;
         const int L = nextL++;
-        const int stage = L % kStagesG;
-        const uint32_t parity = (uint32_t)((L / kStagesG) & 1);
-        mbar_wait(&fullW[stage], parity);
-        const unsigned char* wb = wbuf + stage * wstage + wrow;
 #pragma unroll
-        for (int v = 0; v < SEG; ++v) win[H * SEG + v] = ca_load<T>(wb + cofs<T>(v, sw));
-        fence_proxy_async();
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&emptyW[stage]);
-        if (threadIdx.x == 0 && L + kStagesG < nbox) {
-            mbar_wait(&emptyW[stage], parity);
-            issueW(L + kStagesG, stage);
+        for (int bx = 0; bx < SBOX; ++bx) {
+            const int bi = L * SBOX + bx;
+            const int stage = bi % NWB;
+            const uint32_t parity = (uint32_t)((bi / NWB) & 1);
+            mbar_wait(&fullW[stage], parity);
+            const unsigned char* wb = wbuf + stage * wbox + wrow;
+#pragma unroll
+            for (int v = 0; v < EB; ++v) win[H * SEG + bx * EB + v] = ca_load<T>(wb + cofs<T>(v, sw));
+            fence_proxy_async();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&emptyW[stage]);
+            if (threadIdx.x == 0 && bi + NWB < nwb) {
+                mbar_wait(&emptyW[stage], parity);
+                issueW(bi + NWB, stage);
+            }
         }
     };
     auto consume_box = [&]() {
@@ -573,9 +604,18 @@ __global__ void __launch_bounds__(128, INFT_RING_MINB) k_gather_ring(const __gri
             lead_end = box_next * EB;
         }
         const int cm = col % RS;  // ring slot of the batch's first output
-        // ring slots free: every earlier TMA store has read its box
-        if (lane == 0) bulk_wait_read<0>();
-        __syncwarp();
+        // ring slots free: every earlier TMA store has read its box -- waited for just before
+        // the batch's first write into the ring (INFT_GATHER_LATE_WAIT=0: at the batch start), so
+        // the store's shared-memory read overlaps the window slide and the first node group
+        bool ring_ok = false;
+        auto ring_wait = [&]() {
+            if (!ring_ok) {
+                if (lane == 0) bulk_wait_read<0>();
+                __syncwarp();
+                ring_ok = true;
+            }
+        };
+        if (!kLateWait) ring_wait();
         bool dense = false;
         if constexpr (SEG == kNB) {
             if (full_tile) {
@@ -612,13 +652,15 @@ __global__ void __launch_bounds__(128, INFT_RING_MINB) k_gather_ring(const __gri
                     CA<T> sacc[QG];
 #pragma unroll
                     for (int qq = 0; qq < QG; ++qq) sacc[qq] = ca_zero(T(0));
+                    if constexpr (kExpNoCompute) {  // timing experiment: the data-movement skeleton
 #pragma unroll
-                    for (int t0 = 0; t0 < P; t0 += VEC) {
-                        T wv[QG][VEC];
+                        for (int qq = 0; qq < QG; ++qq) sacc[qq] = win[(g0 + qq + SEG * PH) % K];
+                    }
+                    // weights t0 .. t0 + VEC - 1 of the group's nodes: one broadcast vector load per
+                    // node (slots past P - 1 are the record's tail, never used)
+                    auto load_w = [&](T (&wv)[QG][VEC], int t0) {
 #pragma unroll
                         for (int qq = 0; qq < QG; ++qq) {
-                            // one broadcast vector load: weights t0 .. t0 + VEC - 1 of node g0 + qq
-                            // (slots past P - 1 are the record's tail, never used)
                             if constexpr (VEC == 2) {
                                 const double2 a = *reinterpret_cast<const double2*>(rec + (g0 + qq) * PP + t0);
                                 wv[qq][0] = a.x;
@@ -631,6 +673,23 @@ __global__ void __launch_bounds__(128, INFT_RING_MINB) k_gather_ring(const __gri
                                 wv[qq][3] = a.w;
                             }
                         }
+                    };
+                    T wvn[QG][VEC];
+                    if constexpr (kGatherWPre && !kExpNoCompute) load_w(wvn, 0);
+#pragma unroll
+                    for (int t0 = 0; t0 < (kExpNoCompute ? 0 : P); t0 += VEC) {
+                        T wv[QG][VEC];
+                        if constexpr (kGatherWPre) {
+                            // explicit double buffer: the next tap vector's loads are issued before
+                            // this one's FMAs
+#pragma unroll
+                            for (int qq = 0; qq < QG; ++qq)
+#pragma unroll
+                                for (int u = 0; u < VEC; ++u) wv[qq][u] = wvn[qq][u];
+                            if (t0 + VEC < P) load_w(wvn, t0 + VEC);
+                        } else {
+                            load_w(wv, t0);
+                        }
 #pragma unroll
                         for (int u = 0; u < VEC; ++u) {
                             if (t0 + u < P) {
@@ -642,6 +701,7 @@ __global__ void __launch_bounds__(128, INFT_RING_MINB) k_gather_ring(const __gri
                             }
                         }
                     }
+                    if (g0 == 0) ring_wait();
 #pragma unroll
                     for (int qq = 0; qq < QG; ++qq) {
                         const int sl = cm + g0 + qq;
@@ -700,6 +760,7 @@ __global__ void __launch_bounds__(128, INFT_RING_MINB) k_gather_ring(const __gri
                     break;
             }
             const int sl = cm + q;
+            ring_wait();
             *reinterpret_cast<C2<T>*>(my_stg + cofs<T>(sl >= RS ? sl - RS : sl, sw)) = ca_to(sa);
         }
         run_next = col + cnt;
@@ -823,11 +884,12 @@ static size_t ring_spread_smem(int wpb, int PP, int SEG) {
 template <typename T>
 static size_t ring_gather_smem(int wpb, int PP, int SEG) {
     const int EB = 128 / (int)sizeof(C2<T>);
-    constexpr int kStagesG = ring::stages_g<T>();
-    size_t wsz = (size_t)kStagesG * (SEG / EB) * wpb * 4096;
+    const int sbox = SEG / EB;
+    const int nwb = (sizeof(T) == 8 && sbox == 2) ? ring::win_boxes<T, 2>() : ring::stages_g<T>() * sbox;
+    size_t wsz = (size_t)nwb * wpb * 4096;
     size_t st = (size_t)wpb * (ring::kNB / EB + 1) * 4096;  // output ring (NR boxes per warp)
     size_t r = (size_t)ring::kStagesGR * ((ring::kNB * PP * (int)sizeof(T) + 127) & ~127);
-    return wsz + st + r + 2 * (kStagesG + ring::kStagesGR) * sizeof(uint64_t);
+    return wsz + st + r + 2 * (nwb + ring::kStagesGR) * sizeof(uint64_t);
 }
 
 static void tmap_or_throw(CUtensorMap* m, const void* base, uint64_t inner, uint64_t rows, uint64_t stride,
