@@ -59,6 +59,12 @@ constexpr int stages_g() { return sizeof(T) == 8 ? INFT_RING_STAGES_G : INFT_RIN
 #ifndef INFT_RING_WBOXES_G
 #define INFT_RING_WBOXES_G 3
 #endif
+// complex64 spread: a full batch on an odd node reads its last f value from the next batch's
+// tile instead of fetching a second box of its own (0: always the own box)
+#ifndef INFT_SPREAD_BORROW
+#define INFT_SPREAD_BORROW 1
+#endif
+constexpr bool kBorrowTail = INFT_SPREAD_BORROW != 0;
 // dense gather body: explicit double buffer of the weight vectors (experiment)
 #ifndef INFT_GATHER_WPRE
 #define INFT_GATHER_WPRE 0
@@ -221,6 +227,24 @@ __global__ void __launch_bounds__(128, INFT_RING_MINB) k_spread_ring(const __gri
         cnt = min(kNB, e - pos);
     };
     const int row0 = (int)blockIdx.x * WPB * 32;
+    // complex64: does batch b fetch its own extra box?  Only a full batch on an odd node reads
+    // past its first NBOX boxes (its last node), and when the next batch's tile starts right
+    // there (consecutive batches of one node range -- every batch of config 5) that node is read
+    // from the next stage's tile instead: one box per batch, not two (the second box was an L2
+    // hit, but the spread moves ~6 TB/s between L2 and the SMs with or without the FMAs).
+    auto own_tail = [&](int b, int pos, int cnt) -> int {  // 0: no 17th value, 1: own box, 2: next stage
+        if (CE != 1) return 0;
+        int col = pos + cshift;
+        if (col >= N) col -= N;
+        if (!(col & 1) || cnt < kNB) return 0;
+        if (!kBorrowTail || b + 1 >= nb) return 1;
+        int p2, c2n;
+        bool pr2;
+        batch_pos(b + 1, p2, c2n, pr2);
+        int col2 = p2 + cshift;
+        if (col2 >= N) col2 -= N;
+        return (col2 & ~1) == (col & ~1) + kNB ? 2 : 1;
+    };
     auto issue = [&](int b, int stage) {
         int pos, cnt;
         bool pro;
@@ -229,10 +253,10 @@ __global__ void __launch_bounds__(128, INFT_RING_MINB) k_spread_ring(const __gri
         int col = pos + cshift;
         if (col >= N) col -= N;
         if (CE == 1) col &= ~1;
-        mbar_arrive_expect_tx(&full[stage], fstage + rbytes);
+        const int nbx = CE == 1 ? NBOX + (own_tail(b, pos, cnt) == 1 ? 1 : 0) : NBF;
+        mbar_arrive_expect_tx(&full[stage], (uint32_t)nbx * WPB * 4096u + rbytes);
         for (int wi = 0; wi < WPB; ++wi)
-#pragma unroll
-            for (int bx = 0; bx < NBF; ++bx)
+            for (int bx = 0; bx < nbx; ++bx)
                 tma_load_2d(fbuf + stage * fstage + (wi * NBF + bx) * 4096u, &fmap, tcoord<CE>(col + bx * EB),
                             row0 + wi * 32, &full[stage]);
         bulk_g2s(rbuf + stage * rstage, w + (int64_t)pos * PP, rbytes, &full[stage]);
@@ -307,11 +331,18 @@ __global__ void __launch_bounds__(128, INFT_RING_MINB) k_spread_ring(const __gri
         const unsigned char* fb = fbuf + stage * fstage + frow;
         const T* rec = reinterpret_cast<const T*>(rbuf + stage * rstage);
         int fo = 0;  // complex64: offset of the batch's first node inside the fetched tile
+        const unsigned char* ft = fb + NBOX * 4096u;  // values kNB.. of the tile: the extra box
         if (CE == 1) {
             int col = pos + cshift;
             if (col >= N) col -= N;
             fo = col & 1;
+            if (own_tail(b, pos, cnt) == 2) {  // ... or the next batch's tile (see own_tail)
+                const int b2 = b + 1;
+                mbar_wait(&full[b2 % kStages], (uint32_t)((b2 / kStages) & 1));
+                ft = fbuf + (b2 % kStages) * fstage + frow;
+            }
         }
+        auto f_at = [&](int v) { return v < kNB ? fb + cofs<T>(v, sw) : ft + cofs<T>(v - kNB, sw); };
         // Dense batch: the kNB nodes are exactly one segment with slot offsets
         // 0..SEG-1 (jittered nodes with N = M_sigma).  Straight-line code, no
         // per-node dispatch: node q adds into window registers q .. q+2m.
@@ -331,7 +362,7 @@ __global__ void __launch_bounds__(128, INFT_RING_MINB) k_spread_ring(const __gri
             while (cur_k < kq) flush();
 #pragma unroll
             for (int q = 0; q < kNB; ++q) {
-                const CA<T> fv = ca_load<T>(fb + cofs<T>(q + fo, sw));
+                const CA<T> fv = ca_load<T>(q + 1 < kNB ? fb + cofs<T>(q + fo, sw) : f_at(q + fo));
                 if constexpr (kExpNoCompute) {  // timing experiment: the data-movement skeleton
                     acc[q] = fv;
                     continue;
@@ -353,7 +384,7 @@ __global__ void __launch_bounds__(128, INFT_RING_MINB) k_spread_ring(const __gri
             const int dl = (int)(n0 % SEG);
             const int kq = pro ? 0 : seg - s0 + 1;
             while (cur_k < kq) flush();
-            const CA<T> fv = ca_load<T>(fb + cofs<T>(q + fo, sw));
+            const CA<T> fv = ca_load<T>(f_at(q + fo));
             T wv[P];
             WeightLoader<T, P>::load_smem(rec, wv);
             switch (dl) {
