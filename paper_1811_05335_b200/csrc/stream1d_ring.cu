@@ -65,6 +65,12 @@ constexpr int stages_g() { return sizeof(T) == 8 ? INFT_RING_STAGES_G : INFT_RIN
 #define INFT_SPREAD_BORROW 1
 #endif
 constexpr bool kBorrowTail = INFT_SPREAD_BORROW != 0;
+// gather: one-phase window (register moves per slide, one copy of the bodies) or the two-phase
+// register ring (0)
+#ifndef INFT_GATHER_1PH
+#define INFT_GATHER_1PH 1
+#endif
+constexpr bool kOnePhase = INFT_GATHER_1PH != 0;
 // dense gather body: explicit double buffer of the weight vectors (experiment)
 #ifndef INFT_GATHER_WPRE
 #define INFT_GATHER_WPRE 0
@@ -593,11 +599,27 @@ __global__ void __launch_bounds__(128, INFT_RING_MINB) k_gather_ring(const __gri
             }
         }
     };
+    // One phase (INFT_GATHER_1PH, default): the window always starts at register 0 -- a slide
+    // moves the upper half down (SEG register moves) and loads the new box into the upper half,
+    // so there is ONE copy of the node bodies.  The two-phase register ring (no moves, the
+    // bodies specialised on the segment parity) made the dense path's hot code ~60 KB: past the
+    // 32-KB instruction cache, 17 % of the warp stall samples were instruction fetches.
     auto consume_box = [&]() {
-        if (nextL & 1)
+        if constexpr (kOnePhase) {
+            if (nextL == 0) {
+                consume_box_h(std::integral_constant<int, 0>{});
+            } else {
+                if (nextL >= 2) {
+#pragma unroll
+                    for (int v = 0; v < SEG; ++v) win[v] = win[v + SEG];
+                }
+                consume_box_h(std::integral_constant<int, 1>{});
+            }
+        } else if (nextL & 1) {
             consume_box_h(std::integral_constant<int, 1>{});
-        else
+        } else {
             consume_box_h(std::integral_constant<int, 0>{});
+        }
     };
     consume_box();
     consume_box();
@@ -749,7 +771,13 @@ __global__ void __launch_bounds__(128, INFT_RING_MINB) k_gather_ring(const __gri
                 ++cur_i;
                 dense_body(std::integral_constant<int, 1 - PH>{});
             };
-            if (step1) {
+            if constexpr (kOnePhase) {
+                if (step1) {
+                    consume_box();
+                    ++cur_i;
+                }
+                dense_body(std::integral_constant<int, 0>{});
+            } else if (step1) {
                 if (cur_i & 1)
                     slide_body(std::integral_constant<int, 1>{});
                 else
@@ -774,7 +802,7 @@ __global__ void __launch_bounds__(128, INFT_RING_MINB) k_gather_ring(const __gri
             T wv[P];
             WeightLoader<T, P>::load_smem(rec, wv);
             CA<T> sa = ca_zero(T(0));
-            switch ((cur_i & 1) * 32 + dl) {
+            switch ((kOnePhase ? 0 : (cur_i & 1)) * 32 + dl) {
 #define INFT_RG_CASE(CID)                                                  \
     case CID: {                                                            \
         constexpr int PH = (CID) / 32, D = (CID) % 32;                     \
