@@ -51,3 +51,29 @@ open(f"profiles/{tag}_ncu_full.txt", "w").write("\n".join(head) + raw)
 subprocess.check_call([sys.executable, "tools/ncu_traffic.py", f"gpurun_out/full_{tag}.ncu-rep", "profiles/ncu_traffic.json",
                        tag, "c128", "64"], stdout=subprocess.DEVNULL)
 print("\n".join(L[:16]))
+
+# hot-path shares: the config-5 c128 launches only (the launch list also holds the per-config
+# record's kernels -- config 3 runs the same ring templates at < 0.3 ms, config 5 c64 the float ones)
+sel = [("spread", "ring::k_spread_ring<double, 8>", 0.3), ("fft_forward", "k_pass_a_ip<double, (int)-1, 0, 1024", 0.0),
+       ("trunc_deconv", "k_pass_b_ip<double, (int)-1, 0, 2048", 0.0), ("deconv_pad", "k_pass_a_ip<double, 1, 1, 1024", 0.0),
+       ("fft_inverse", "k_pass_b_ip<double, 1, 1, 2048", 0.0), ("gather", "ring::k_gather_ring<double, 8>", 0.3)]
+acc = {s[0]: [0.0, 0] for s in sel}
+for r in rows[hi + 1:]:
+    try:
+        v = float(r[iv].replace(",", ""))
+    except ValueError:
+        continue
+    ms = v * {"ns": 1e-6, "nsecond": 1e-6, "us": 1e-3, "usecond": 1e-3, "ms": 1.0, "msecond": 1.0}.get(r[iu], 1e-6)
+    for name, pat, lo in sel:
+        if pat in r[ik] and ms > lo:
+            acc[name][0] += ms
+            acc[name][1] += 1
+tot5 = sum(a[0] for a in acc.values())
+S = ["# config-5 c128 hot-path kernels in the launch list of `bench.py --steps 3 --warmup 3` (cold, serialised",
+     "# ncu durations; the config-3 launches of the same kernel templates, < 0.3 ms, excluded)",
+     f"{'stage':14s} {'launches':>8s} {'ms/launch':>10s} {'share':>7s}"]
+for name, _, _ in sel:
+    t, c = acc[name]
+    S.append(f"{name:14s} {c:8d} {t / max(c, 1):10.4f} {100 * t / tot5:6.1f}%")
+open(f"profiles/{tag}_launch_shares.txt", "w").write("\n".join(S) + "\n")
+print("\n".join(S))
