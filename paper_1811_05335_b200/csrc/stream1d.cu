@@ -720,6 +720,19 @@ static void tmap_store(const TmapKey& k, const CUtensorMap& m) {
     tmap_cache()[k] = m;
 }
 
+// L2 promotion of the tensor maps' requests (experiment knob INFT_TMAP_L2 = 0 | 64 | 128 | 256,
+// default 256 bytes)
+static CUtensorMapL2promotion tmap_l2() {
+    static const CUtensorMapL2promotion v = [] {
+        const char* e = getenv("INFT_TMAP_L2");
+        const int x = e ? atoi(e) : 256;
+        return x == 0 ? CU_TENSOR_MAP_L2_PROMOTION_NONE
+                      : (x == 64 ? CU_TENSOR_MAP_L2_PROMOTION_L2_64B
+                                 : (x == 128 ? CU_TENSOR_MAP_L2_PROMOTION_L2_128B : CU_TENSOR_MAP_L2_PROMOTION_L2_256B));
+    }();
+    return v;
+}
+
 bool make_tmap_3d(CUtensorMap* out, const void* base, uint64_t d0, uint64_t d1, uint64_t d2, uint64_t s1,
                   uint64_t s2, uint32_t b0, uint32_t b1, int esize) {
     const TmapKey key{base, {d0, d1, d2, s1, s2, b0, b1, (uint64_t)esize}};
@@ -732,7 +745,7 @@ bool make_tmap_3d(CUtensorMap* out, const void* base, uint64_t d0, uint64_t d1, 
     cuuint32_t estr[3] = {1, 1, 1};
     CUresult r = encode(out, esize == 4 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3,
                         const_cast<void*>(base), dims, strides, box, estr,
-                        CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                        CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, tmap_l2(),
                         CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS) return false;
     tmap_store(key, *out);
@@ -751,7 +764,7 @@ bool make_tmap_2d(CUtensorMap* out, const void* base, uint64_t inner, uint64_t r
     cuuint32_t estr[2] = {1, 1};
     CUresult r = encode(out, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2,
                         const_cast<void*>(base), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                        CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                        CU_TENSOR_MAP_SWIZZLE_128B, tmap_l2(),
                         CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS) return false;
     tmap_store(key, *out);
