@@ -23,14 +23,14 @@ for r in rows[hi + 1:]:
     tot[k] += v * sc
     cnt[k] += 1
 apply = [k for k in tot if any(s in k for s in ("k_pass_", "k_spread", "k_gather", "k_ring_halo", "ring::"))]
-steps = 6  # 3 warm-up + 3 timed steps of bench.py --steps 3 --warmup 3
+steps = max(cnt[k] for k in apply)  # 3 warm-up + 3 timed + 3 stage-timed steps of bench.py --steps 3 --warmup 3
 app = sum(tot[k] for k in apply)
 L = [f"# Round {tag[1:]} launch list -- config 5 (M=2^20, N=2^21 jittered, m=8, sigma=2, 64 RHS, complex128), 1x B200",
      "# Command (tools/profile_round.sh): ncu --metrics gpu__time_duration.sum --clock-control none --csv \\",
-     f"#   --log-file launches_{tag}.csv python bench.py --steps 3 --warmup 3 --no-cpu-baseline --no-e2e",
+     f"#   --log-file launches_{tag}.csv python bench.py --steps 3 --warmup 3 --no-cpu-baseline --no-e2e --no-configs",
      "# Per-launch times are cold-cache and serialised (ncu); bench.py's live CUDA-event stage times are the",
      "# numbers in the bench line -- the SHARE of each kernel in the step is what must agree.",
-     "", "Apply kernels (6 steps = 3 warm-up + 3 timed; one launch of each per step):",
+     "", f"Apply kernels ({steps} steps = 3 warm-up + 3 timed + 3 with per-stage events; one launch of each per step):",
      f"{'kernel':60s} {'launches':>8s} {'ms/launch':>10s} {'share':>7s}"]
 for k in sorted(apply, key=lambda k: -tot[k]):
     L.append(f"{k[:60]:60s} {cnt[k]:8d} {tot[k] / cnt[k]:10.3f} {100 * tot[k] / app:6.1f}%")
@@ -44,7 +44,7 @@ raw = subprocess.run([sys.executable, "tools/ncu_summary.py", "raw", f"gpurun_ou
                      capture_output=True, text=True).stdout
 head = [f"# Round {tag[1:]} ncu --set full summary -- config 5 c128, 64 RHS, one launch of each apply kernel",
         "# Command (tools/profile_round.sh): ncu --set full --import-source on --clock-control none \\",
-        "#   -k regex:'k_pass_|k_spread|k_gather|ring::' -c 6 python bench.py --steps 1 --warmup 3 --no-cpu-baseline --no-e2e",
+        "#   -k regex:'k_pass_|k_spread|k_gather|ring::' -c 6 python bench.py --steps 1 --warmup 3 --no-cpu-baseline --no-e2e --no-configs",
         "# Algorithmic bytes per launch (DESIGN.md 7): spread 4.59 GB, pass A fwd 4.29 GB, pass B fwd 3.22 GB,",
         "#   pass A adj 3.22 GB, pass B adj 4.29 GB, gather 4.59 GB; dram bytes below are what the kernel moved.", ""]
 open(f"profiles/{tag}_ncu_full.txt", "w").write("\n".join(head) + raw)
