@@ -1198,11 +1198,11 @@ static size_t pass_b_smem(int L, int N1, int64_t M, int mode) {
 // pass B of the inverse in place with 8192-element tiles (INFT_FFT_TILE_B=8192): 4 rows of 2048,
 // so each kept output column leaves as a 64-byte run instead of 32 (one CTA per SM)
 template <typename T>
-static bool pick_ip_b8(int L, PassBFn<T>& b, int& TF, int& ST, int& SW, int& NT) {
+static bool pick_ip_b8(int L, PassBFn<T>& b, int& TF, int& ST, int& SW, int& NT, int mode = 0) {
 #define INFT_IPG8(LL)                                                                                    \
     TF = fft::Geo<T, LL, 8192>::TF, ST = fft::Geo<T, LL, 8192>::ST, SW = fft::Geo<T, LL, 8192>::SW,      \
     NT = fft::Geo<T, LL, 8192>::NT;                                                                      \
-    b = fft::k_pass_b_ip<T, -1, 0, LL, 8192>;                                                            \
+    b = mode == 0 ? fft::k_pass_b_ip<T, -1, 0, LL, 8192> : fft::k_pass_b_ip<T, 1, 1, LL, 8192>;          \
     return true;
     switch (L) {
         case 1024: { INFT_IPG8(1024) }
@@ -1400,7 +1400,20 @@ static void launch_pass_b(Plan& p, fft::Args<T>& A, int mode, int64_t R, cudaStr
             const char* e = getenv("INFT_FFT_TILE_B");
             return e ? atoi(e) : 4096;
         }();
-        if (mode == 0 && tile_b == 8192 && pick_ip_b8<T>(L, kip, tf, st_, sw, nt)) {
+        // adjoint (MODE 1), complex128: 8192-element tiles by default -- four rows per tile, so the
+        // grid leaves in 64-byte runs instead of 32 (one 512-thread CTA per SM; config 5: 0.849 ->
+        // 0.794 ms; the source view had 18 % of this pass's stall samples on its 32-byte-run stores
+        // and 15 % in MIO throttle).  INFT_FFT_TILE_B1=4096: two CTAs per SM on 4096-element tiles.
+        // The same tiles are slower for the inverse (0.709 -> 0.762 ms, INFT_FFT_TILE_B=8192) and
+        // for pass A (0.82 -> 0.83 ms inverse, 0.64 -> 0.83-0.86 ms adjoint).
+        static const int tile_b1 = [] {
+            const char* e = getenv("INFT_FFT_TILE_B1");
+            return e ? atoi(e) : 8192;
+        }();
+        // (big tiles only when they still give every SM two or more: small batches keep 4096)
+        const bool many = L <= 8192 && R * (int64_t)(A.N1 / std::max(1, 8192 / L)) >= 2 * (int64_t)num_sms();
+        if (sizeof(T) == 8 && ((mode == 0 && tile_b == 8192) || (mode == 1 && tile_b1 == 8192 && many)) &&
+            pick_ip_b8<T>(L, kip, tf, st_, sw, nt, mode)) {
             TB = tf, ST = st_, SW = sw, threads = nt;
         } else if (pick_ip<T>(mode, L, false, unused, kip, tf, st_, sw, nt, rb)) {
             TB = tf, ST = st_, SW = sw, threads = nt;
