@@ -1212,6 +1212,23 @@ static bool pick_ip_b8(int L, PassBFn<T>& b, int& TF, int& ST, int& SW, int& NT,
 #undef INFT_IPG8
 }
 
+// complex64 pass B of the inverse in place on 16384-element tiles (128 KB: eight rows of 2048, the
+// kept band leaves in 64-byte runs; one 1024-thread CTA per SM at 64 registers): config 5 c64
+// 0.464 -> 0.437 ms against the double-buffered 8192-element kernel (INFT_FFT_C64_B0=0: that one).
+// The adjoint's pass B measured slower on these tiles (0.460 against 0.431 ms) and keeps it.
+template <typename T>
+static bool pick_ip_b16f(int L, PassBFn<T>& b, int& TF, int& ST, int& SW, int& NT) {
+    if constexpr (sizeof(T) == 4) {
+        if (L == 2048) {
+            using G = fft::Geo<T, 2048, 16384, 16>;
+            TF = G::TF, ST = G::ST, SW = G::SW, NT = G::NT;
+            b = fft::k_pass_b_ip<T, -1, 0, 2048, 16384, 16>;
+            return true;
+        }
+    }
+    return false;
+}
+
 // in-place kernels and their geometry (Geo<T, L, TE>) for the supported lengths; TE = 4096
 // (two CTAs per SM) or 2048 (half-size tiles, four CTAs per SM)
 template <typename T, int TE, int RB>
@@ -1393,7 +1410,10 @@ static void launch_pass_b(Plan& p, fft::Args<T>& A, int mode, int64_t R, cudaStr
     }();
     PassBFn<T> kip = nullptr;
     int rb = fft::kRB;
-    if (ipb && (sizeof(T) == 8 || ip_c64(false)) && (mode == 0 || ipb1)) {
+    static const int c64_b0 = getenv("INFT_FFT_C64_B0") ? atoi(getenv("INFT_FFT_C64_B0")) : 16384;
+    const bool c64big = sizeof(T) == 4 && mode == 0 && c64_b0 == 16384 && L == 2048 &&
+                        R * (int64_t)(A.N1 / 8) >= 2 * (int64_t)num_sms();
+    if (ipb && (sizeof(T) == 8 || ip_c64(false) || c64big) && (mode == 0 || ipb1)) {
         PassAFn<T> unused = nullptr;
         int tf, st_, sw, nt;
         static const int tile_b = [] {
@@ -1412,7 +1432,10 @@ static void launch_pass_b(Plan& p, fft::Args<T>& A, int mode, int64_t R, cudaStr
         }();
         // (big tiles only when they still give every SM two or more: small batches keep 4096)
         const bool many = L <= 8192 && R * (int64_t)(A.N1 / std::max(1, 8192 / L)) >= 2 * (int64_t)num_sms();
-        if (sizeof(T) == 8 && ((mode == 0 && tile_b == 8192) || (mode == 1 && tile_b1 == 8192 && many)) &&
+        if (c64big && pick_ip_b16f<T>(L, kip, tf, st_, sw, nt)) {
+            TB = tf, ST = st_, SW = sw, threads = nt;
+            rb = 16;
+        } else if (sizeof(T) == 8 && ((mode == 0 && tile_b == 8192) || (mode == 1 && tile_b1 == 8192 && many)) &&
             pick_ip_b8<T>(L, kip, tf, st_, sw, nt, mode)) {
             TB = tf, ST = st_, SW = sw, threads = nt;
         } else if (pick_ip<T>(mode, L, false, unused, kip, tf, st_, sw, nt, rb)) {
