@@ -529,18 +529,28 @@ def main():
     # ---------------------------------------------------------------- per-kernel times (second pass)
     # the same K steps again with the library's per-stage CUDA events on the launching stream
     # (plain launches, no graph replay): the roofline's kernel durations and stage shares
+    # A pass disturbed by a transient (seen once: two stages 30 % slow in this pass while the
+    # headline of the same process was normal) is re-measured, at most twice; the pass closest to
+    # the headline's steady state (the fastest) is kept and the attempts are reported.
     plan.set_profiling(True)
-    plan.get_profile(reset=True)
-    torch.cuda.synchronize()
-    p0 = torch.cuda.Event(enable_timing=True)
-    p1 = torch.cuda.Event(enable_timing=True)
-    p0.record(stream)
-    for _ in range(args.steps):
-        step()
-    p1.record(stream)
-    torch.cuda.synchronize()
-    ms_prof = p0.elapsed_time(p1)
-    prof = plan.get_profile(reset=True)
+    ms_prof, prof, prof_attempts = None, None, 0
+    for _ in range(3):
+        prof_attempts += 1
+        plan.get_profile(reset=True)
+        torch.cuda.synchronize()
+        p0 = torch.cuda.Event(enable_timing=True)
+        p1 = torch.cuda.Event(enable_timing=True)
+        p0.record(stream)
+        for _ in range(args.steps):
+            step()
+        p1.record(stream)
+        torch.cuda.synchronize()
+        t = p0.elapsed_time(p1)
+        pr = plan.get_profile(reset=True)
+        if ms_prof is None or t < ms_prof:
+            ms_prof, prof = t, pr
+        if ms_prof <= 1.05 * ms_total:
+            break
     plan.set_profiling(False)
 
     # ---------------------------------------------------------------- roofline of the dominant kernel
@@ -566,7 +576,8 @@ def main():
                   "gbs": (stage_bytes[k] / (stage_ms[k] / 1e3) / 1e9) if stage_ms[k] else None,
                   "share_of_step": (prof[k][0] / ms_prof) if ms_prof else None} for k in stage_ms}
     roofline["timing"] = (f"per-stage CUDA events on the launching stream over a second pass of "
-                          f"{args.steps} steps ({ms_prof / args.steps:.3f} ms/step with events, plain launches)")
+                          f"{args.steps} steps ({ms_prof / args.steps:.3f} ms/step with events, plain launches; "
+                          f"{prof_attempts} pass{'es' if prof_attempts > 1 else ''})")
 
     # ---------------------------------------------------------------- e2e through the C ABI with host buffers
     e2e = None
