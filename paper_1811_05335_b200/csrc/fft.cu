@@ -639,7 +639,13 @@ __global__ void __launch_bounds__(Geo<T, L>::NT, 1)
 // HZ (MODE 1 only): the band is exactly L/4 rows on each side (sigma = 2), so the first stage
 // skips the zero rows at compile time (run_stage_ip); the host picks it when M / 2 / N2 == L / 4.
 template <typename T, int SIGN, int MODE, int L, int TE = kTileIP, int RB = kRB, bool HZ = false>
-__global__ void __launch_bounds__(Geo<T, L, TE, RB>::NT, TE == kTileIP ? (RB == 32 ? INFT_R32_MINB : 2) : (TE < kTileIP ? 4 : 2))
+// (complex64 adjoint, 8192-element radix-32 tiles: ONE 256-thread CTA per SM with all the registers
+//  it wants (246, no spills) instead of two at 128 with spills -- config 5 c64: 0.444 -> 0.375 ms;
+//  the inverse's pass A is the other way round, 0.400 -> 0.500 ms.  -DINFT_C64_A1_MINB=2: two CTAs)
+#ifndef INFT_C64_A1_MINB
+#define INFT_C64_A1_MINB 1
+#endif
+__global__ void __launch_bounds__(Geo<T, L, TE, RB>::NT, TE == kTileIP ? (RB == 32 ? INFT_R32_MINB : 2) : (TE < kTileIP ? 4 : (sizeof(T) == 4 && MODE == 1 ? INFT_C64_A1_MINB : 2)))
     k_pass_a_ip(const __grid_constant__ CUtensorMap map, const __grid_constant__ CUtensorMap dmap, Args<T> A, int BR,
                 int ntiles) {
     extern __shared__ __align__(128) unsigned char smraw[];
