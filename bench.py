@@ -549,7 +549,7 @@ def main():
         pr = plan.get_profile(reset=True)
         if ms_prof is None or t < ms_prof:
             ms_prof, prof = t, pr
-        if ms_prof <= 1.05 * ms_total:
+        if ms_prof <= 1.03 * ms_total:
             break
     plan.set_profiling(False)
 
