@@ -257,9 +257,27 @@ __device__ __forceinline__ C2<T> twid_g(const C2<T>* __restrict__ tab, int e) {
 #ifndef INFT_R16_BLOCKTW
 #define INFT_R16_BLOCKTW 1
 #endif
-template <typename T, int SIGN, int R, int L, int NS, bool Z = false>
-__device__ __forceinline__ void stage_regs(C2<T> (&a)[R], int j, const C2<T>* __restrict__ tw) {
-    if constexpr (NS > 1 && ((R == 32 && INFT_R32_BLOCKTW) || (R == 16 && INFT_R16_BLOCKTW))) {
+// Stage twiddle table (in-place radix-16 passes, stages with a span NS <= 8): the stage has only
+// NS distinct twiddle sets, so all R - 1 powers of each sit in a small shared table [R - 1][NS]
+// (built once per CTA) and are loaded (a warp touches <= 8 consecutive entries: one wavefront)
+// instead of derived from one table entry by 14 complex products per butterfly.
+#ifndef INFT_FFT_STAGE_TAB
+#define INFT_FFT_STAGE_TAB 1
+#endif
+constexpr bool kStageTab = INFT_FFT_STAGE_TAB != 0;
+constexpr int kStageTabNS = 8;                         // largest span served by the table
+constexpr int kStageTabElems = 15 * kStageTabNS;       // entries (radix 16)
+template <int R, int NS>
+constexpr bool stage_tab() { return kStageTab && R == 16 && NS > 1 && NS <= kStageTabNS; }
+
+template <typename T, int SIGN, int R, int L, int NS, bool Z = false, bool TAB = false>
+__device__ __forceinline__ void stage_regs(C2<T> (&a)[R], int j, const C2<T>* __restrict__ tw,
+                                           const C2<T>* __restrict__ tw2 = nullptr) {
+    if constexpr (TAB) {
+        const int k = j % NS;
+#pragma unroll
+        for (int m = 1; m < R; ++m) a[m] = cmul<T>(a[m], twid<T, SIGN>(tw2, (m - 1) * NS + k));
+    } else if constexpr (NS > 1 && ((R == 32 && INFT_R32_BLOCKTW) || (R == 16 && INFT_R16_BLOCKTW))) {
         // radix 32: twiddles in blocks of four, a[4b + i] *= w^i w^{4b} with w^{4b} by a running
         // product (depth <= 8): six live twiddles instead of 31 (the full table held ~120
         // registers of the 246 the radix-32 passes used)
@@ -458,7 +476,8 @@ __device__ __forceinline__ void cta_fft(const C2<T>* tw, C2<T>* sm, Load&& load,
 // m in [RF/4, 3RF/4) of every butterfly -- never loaded, and the inner DFT4s skip them.
 template <typename T, int SIGN, typename G, int R, int NS, int SI, bool HZ, typename Load, typename Store,
           typename Free>
-__device__ __forceinline__ void run_stage_ip(const C2<T>* tw, C2<T>* sm, Load&& load, Store&& store, Free&& on_free) {
+__device__ __forceinline__ void run_stage_ip(const C2<T>* tw, const C2<T>* tw2, C2<T>* sm, Load&& load, Store&& store,
+                                             Free&& on_free) {
     constexpr bool Z = HZ && SI == 0 && R >= 4;
     constexpr int L = G::ST - G::PAD;
     constexpr int TF = G::TF;
@@ -492,7 +511,7 @@ __device__ __forceinline__ void run_stage_ip(const C2<T>* tw, C2<T>* sm, Load&& 
         const int t = threadIdx.x + p * G::NT;
         if (total % G::NT != 0 && t >= total) break;
         const int f = t % TF, j = t / TF;
-        stage_regs<T, SIGN, R, L, NS, Z>(a[p], j, tw);
+        stage_regs<T, SIGN, R, L, NS, Z, stage_tab<R, NS>()>(a[p], j, tw, tw2);
         const int base = (j / NS) * NS * R + (j % NS);
 #pragma unroll
         for (int m = 0; m < R; ++m) {
@@ -507,12 +526,35 @@ __device__ __forceinline__ void run_stage_ip(const C2<T>* tw, C2<T>* sm, Load&& 
 }
 
 template <typename T, int SIGN, typename G, int SI, int NS, bool HZ, typename Load, typename Store, typename Free>
-__device__ __forceinline__ void fft_stages_ip(const C2<T>* tw, C2<T>* sm, Load&& load, Store&& store, Free&& on_free) {
+__device__ __forceinline__ void fft_stages_ip(const C2<T>* tw, const C2<T>* tw2, C2<T>* sm, Load&& load, Store&& store,
+                                              Free&& on_free) {
     if constexpr (SI < G::NST) {
         constexpr int R = (SI == 0) ? G::RF : G::RB;
-        run_stage_ip<T, SIGN, G, R, NS, SI, HZ>(tw, sm, load, store, on_free);
-        fft_stages_ip<T, SIGN, G, SI + 1, NS * R, HZ>(tw, sm, load, store, on_free);
+        run_stage_ip<T, SIGN, G, R, NS, SI, HZ>(tw, tw2, sm, load, store, on_free);
+        fft_stages_ip<T, SIGN, G, SI + 1, NS * R, HZ>(tw, tw2, sm, load, store, on_free);
     }
+}
+
+// The in-place kernels keep the stage twiddle table in the LAST kStageTabElems entries of their
+// dynamic shared memory (the host adds the room); it serves the stage whose span is RF, the
+// first-stage radix (the only stage with 1 < NS <= 8 in a radix-16 plan).
+__device__ __forceinline__ uint32_t dyn_smem_bytes() {
+    uint32_t v;
+    asm("mov.u32 %0, %%dynamic_smem_size;" : "=r"(v));
+    return v;
+}
+template <typename T, typename G>
+__device__ __forceinline__ const C2<T>* stage_tab_fill(unsigned char* smraw, const C2<T>* __restrict__ gtab) {
+    constexpr int L = G::ST - G::PAD;
+    constexpr int NS = G::RF;  // span of the stage after the first one
+    C2<T>* t2 = reinterpret_cast<C2<T>*>(smraw + dyn_smem_bytes() - sizeof(C2<T>) * kStageTabElems);
+    if constexpr (stage_tab<G::RB, NS>() && G::NST >= 2) {
+        for (int i = threadIdx.x; i < 15 * NS; i += blockDim.x) {
+            const int m = i / NS + 1, k = i % NS;
+            t2[i] = gtab[m * k * (L / (NS * 16))];
+        }
+    }
+    return t2;
 }
 
 // byte offset of pass B's deconvolution tile: after tile[2] | work | twiddles, 128-aligned
@@ -669,6 +711,7 @@ __global__ void __launch_bounds__(Geo<T, L, TE, RB>::NT, TE == kTileIP ? (RB == 
         fence_barrier_init();
     }
     for (int i = threadIdx.x; i < L / RB; i += blockDim.x) tws[i] = A.tw1[i];
+    const C2<T>* tws2 = stage_tab_fill<T, G>(smraw, A.tw1);
     __syncthreads();
     // L2 prefetch of a tile's boxes (INFT_FFT_PREFETCH_A, off: slower here, see kPrefetchA): the
     // in-place buffer can only take the next tile after the last stage has read it
@@ -736,7 +779,7 @@ __global__ void __launch_bounds__(Geo<T, L, TE, RB>::NT, TE == kTileIP ? (RB == 
         auto on_free = [&]() {
             if (!kNoLoad && threadIdx.x == 0 && nxt < ntiles) issue(nxt);
         };
-        fft_stages_ip<T, SIGN, G, 0, 1, MODE == 1 && HZ>(tws, buf, load, store, on_free);
+        fft_stages_ip<T, SIGN, G, 0, 1, MODE == 1 && HZ>(tws, tws2, buf, load, store, on_free);
     }
 }
 
@@ -909,6 +952,7 @@ __global__ void __launch_bounds__(Geo<T, L, TE, RB>::NT, TE == kTileIP ? (RB == 
         fence_barrier_init();
     }
     for (int i = threadIdx.x; i < L / RB; i += blockDim.x) tws[i] = A.tw2[i];
+    const C2<T>* tws2 = stage_tab_fill<T, G>(smraw, A.tw2);
     __syncthreads();
     auto issue = [&](int id) {
         const int64_t r = id / tiles_per_rhs;
@@ -983,7 +1027,7 @@ __global__ void __launch_bounds__(Geo<T, L, TE, RB>::NT, TE == kTileIP ? (RB == 
         auto on_free = [&]() {
             if (!kNoLoad && (MODE == 0 || kPlainB1) && threadIdx.x == 0 && nxt < ntiles) issue(nxt);
         };
-        fft_stages_ip<T, SIGN, G, 0, 1, false>(tws, buf, load, store, on_free);
+        fft_stages_ip<T, SIGN, G, 0, 1, false>(tws, tws2, buf, load, store, on_free);
         if (MODE == 0 || kPlainB1) {
             __syncthreads();  // every d read of this tile before the next tile's d copy
         } else {
@@ -1370,7 +1414,8 @@ static void launch_pass_a(Plan& p, fft::Args<T>& A, int mode, const void* src, i
     }
     const int ntiles = (int)(R * (A.N2 / TA));
     if (kip) {
-        const size_t smem_ip = cs * (size_t)(std::max(L * TA, SW * TA) + L / rb) + 16;
+        const size_t smem_ip = ((cs * (size_t)(std::max(L * TA, SW * TA) + L / rb) + 16 + 15) & ~(size_t)15) +
+                               cs * fft::kStageTabElems;  // + the stage twiddle table at the end
         ensure_smem_attr((const void*)kip, smem_ip);
         const int occ = occupancy_cached((const void*)kip, threads, smem_ip);
         kip<<<(unsigned)std::min(ntiles, num_sms() * std::max(1, occ)), threads, smem_ip, st>>>(map, dmap, A, BR,
@@ -1482,7 +1527,8 @@ static void launch_pass_b(Plan& p, fft::Args<T>& A, int mode, int64_t R, cudaStr
     const int ntiles = (int)(R * (A.N1 / TB));
     if (kip) {
         const size_t head = (cs * (size_t)(std::max(ST * TB, SW * TB) + L / rb) + 127) / 128 * 128;
-        const size_t smem_ip = head + (mode == 0 ? sizeof(T) * (size_t)(2 * B2 * DW) : 0) + 32;
+        const size_t smem_ip = ((head + (mode == 0 ? sizeof(T) * (size_t)(2 * B2 * DW) : 0) + 32 + 15) & ~(size_t)15) +
+                               cs * fft::kStageTabElems;  // + the stage twiddle table at the end
         ensure_smem_attr((const void*)kip, smem_ip);  // <= ~150 KB for L <= 4096
         const int occ = occupancy_cached((const void*)kip, threads, smem_ip);
         kip<<<(unsigned)std::min(ntiles, num_sms() * std::max(1, occ)), threads, smem_ip, st>>>(dmap, omap, A, BRd,
